@@ -1,0 +1,135 @@
+/*
+ * ssn.h -- C ABI of the B200-native SSNet secure-inference hot path (libssn_b200.so).
+ *
+ * The reference (SSNet, /root/reference/pkg/src/ssnet) is a pure-Python package with no
+ * FFI: its "plugin boundary" is the Python API (ssnet.*).  These entry points are what a
+ * maintainer would bind (ctypes / cffi) to replace the numpy
+ * dtype=object expressions on that path; each declaration cites the reference code it
+ * replaces.  The Python mirror of the ssnet API lives in paper_2406_02629_b200/ and calls
+ * nothing else.
+ *
+ * Conventions
+ *   - field elements: canonical uint64 in [0, p), p prime, p < 2^62 (reference: p < 2^57,
+ *     S/field.py:64-75); signed plaintext: int64.
+ *   - every pointer named like a tensor is a caller-owned DEVICE pointer; `ids`, `w`,
+ *     `rt`, `ext` are small HOST arrays baked into kernel parameters.
+ *   - multi-party / multi-image operands are strided views: element (b, j, i) of a
+ *     "pts" view lives at pts[b*bstride + j*jstride + i].
+ *   - `stream` is a cudaStream_t; calls are asynchronous and reentrant per stream;
+ *     no hidden allocation.
+ *   - return 0 on success, < 0 on error (SSN_ERR_*); the Python layer maps errors to the
+ *     reference's exception types.
+ */
+#ifndef SSN_H
+#define SSN_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSN_ABI_VERSION 1
+#define SSN_OK 0
+#define SSN_ERR_ARG (-1)
+#define SSN_ERR_CUDA (-2)
+#define SSN_ERR_UNSUPPORTED (-3)
+
+int ssn_version(void);
+
+/* out[i] = a[i] OP b[bidx(i)], bidx(i) = (i / b_div) % b_mod + (i / b_div2) * b_mul2.
+ * op: 0 add, 1 sub, 2 mul, 3 neg (b unused).
+ * Replaces share_add/share_sub/share_mul (S/sss.py:238-276), PrimeField.add/sub/mul/neg
+ * (S/field.py:89-99), the bias broadcast `vals + b[:, None]` (S/layers.py:261-265),
+ * the masks `x * beta` (S/layers.py:341) and the unmask `plain * beta_inv` (S/layers.py:379). */
+int ssn_ewise(int op, const uint64_t *a, const uint64_t *b, uint64_t *out, uint64_t n, uint64_t b_div,
+              uint64_t b_mod, uint64_t b_div2, uint64_t b_mul2, uint64_t p, void *stream);
+
+/* Shamir share generation, SssScheme.gen (S/sss.py:118-147):
+ * out[b][t][i] = secret[b][i] + sum_{j<km1} c_j[b][i] * ids[t]^(j+1) mod p.
+ * Coefficients: coeffs[b][j][i] (host-fed, draw order c_1..c_{k-1}: parity mode) or, when
+ * coeffs == NULL, Philox4x32-10(seed, stream + b, i, j) uniform in [0, p) (speed mode).
+ * secret == NULL shares zero (gen_zero_shares, S/masks.py:93-96). ids: host, <= 16. */
+int ssn_gen(const uint64_t *secret, uint64_t secret_bstride, const uint64_t *coeffs, uint64_t coeff_bstride,
+            uint64_t seed, uint64_t stream, int km1, const uint64_t *ids, int nids, uint64_t *out,
+            uint64_t out_bstride, uint64_t out_tstride, uint64_t n, int nbatch, uint64_t p, void *strm);
+
+/* Lagrange reconstruction, SssScheme.rec (S/sss.py:172-194):
+ * out[b][i] = sum_{j<m} w[j] * pts[b][j][i] mod p.  w: host Lagrange weights (S/sss.py:151-170). */
+int ssn_rec(const uint64_t *pts, uint64_t pts_bstride, uint64_t pts_jstride, const uint64_t *w, int m,
+            uint64_t *out, uint64_t out_bstride, uint64_t n, int nbatch, uint64_t p, void *strm);
+
+/* Reshare step 2, reshare_degree_reduce (S/protocol.py:165-185): for front rank b,
+ * out[b][t][i] = sum_{j<m} rt[t*m + j] * pts[b][j][i] mod p, rt = R^T[:nout] (host). */
+int ssn_reduce_apply(const uint64_t *pts, uint64_t pts_bstride, uint64_t pts_jstride, int m, const uint64_t *rt,
+                     int nout, uint64_t *out, uint64_t out_bstride, uint64_t out_tstride, uint64_t n, int nbatch,
+                     uint64_t p, void *strm);
+
+/* Reshare step 3 + rerand + bias (+ truncation front mask), fused:
+ * out[b][i] = sum_{j<k} w[j]*pts[b][j][i] + zero[b][i] + bias[b][(i/bias_div)%bias_mod] + alpha[b][i].
+ * zero/bias/alpha may be NULL.  Replaces S/protocol.py:187-198 (rec of RESHARE_BACK points),
+ * rerand (S/protocol.py:260-265), the bias add (S/layers.py:261-267) and, when the next op is
+ * a truncation, `share_add(x, alpha)` (S/layers.py:293). */
+int ssn_reshare_finish(const uint64_t *pts, uint64_t pts_bstride, uint64_t pts_jstride, const uint64_t *w, int k,
+                       const uint64_t *zero, uint64_t zero_bstride, const uint64_t *bias, uint64_t bias_bstride,
+                       uint64_t bias_div, uint64_t bias_mod, const uint64_t *alpha, uint64_t alpha_bstride,
+                       uint64_t *out, uint64_t out_bstride, uint64_t n, int nbatch, uint64_t p, void *strm);
+
+/* Elite side of the masked truncation, sss_truncation (S/layers.py:295-315):
+ * v = rec(pts[0..k)); optional Reed-Solomon check of pts[k..npts) against the Lagrange
+ * extrapolation ext[(e-k)*k + j] (failures added to *fail, device counter, may be NULL);
+ * shifted = ((v - lo) mod p) + lo with lo = -value_bound + r*d (S/layers.py:231-233,288);
+ * t = floor(shifted / r); if d > 1 t = round_half_away(t, d) (S/model.py:44-50);
+ * then fresh (k,n) shares of t mod p at ids written to out[t_idx*out_tstride + i]
+ * (nids == 0: out[i] = t mod p).  Coefficients as in ssn_gen. */
+int ssn_trunc_elite(const uint64_t *pts, uint64_t pts_jstride, int npts, int k, const uint64_t *w,
+                    const uint64_t *ext, int64_t value_bound, int64_t r, int64_t d, const uint64_t *coeffs,
+                    uint64_t seed, uint64_t stream, int km1, const uint64_t *ids, int nids, uint64_t *out,
+                    uint64_t out_tstride, unsigned long long *fail, uint64_t n, uint64_t p, void *strm);
+
+/* Elite side of the masked nonlinearity, sss_nonlinear (S/layers.py:345-364):
+ * v = rec over m = 2k-1 product shares, decode_signed (S/field.py:130-134), ReLU, window
+ * max (pool_kind 1) / sum (2) over non-overlapping kh x kw windows of nb x (c,h,wd) images
+ * (pool_blocks, S/model.py:374-377), encode_signed.  pool_kind 0: kh = kw = 1. */
+int ssn_nonlin_elite(const uint64_t *pts, uint64_t pts_jstride, int m, const uint64_t *w, int relu, int pool_kind,
+                     int nb, int c, int h, int wd, int kh, int kw, uint64_t *plain, uint64_t p, void *strm);
+
+/* Signed embedding (S/field.py:120-134). encode counts |x| > (p-1)/2 into *overflow. */
+int ssn_encode_signed(const int64_t *x, uint64_t *out, uint64_t n, unsigned long long *overflow, uint64_t p,
+                      void *strm);
+int ssn_decode_signed(const uint64_t *v, int64_t *out, uint64_t n, uint64_t p, void *strm);
+
+/* Multiplicative inverse (Fermat), PrimeField.inv (S/field.py:101-116); 0 -> 0. */
+int ssn_inv(const uint64_t *a, uint64_t *out, uint64_t n, uint64_t p, void *strm);
+
+/* out[i] = lo + Philox uniform in [0, range) (device speed-mode randomness). */
+int ssn_rand(uint64_t *out, uint64_t n, uint64_t lo, uint64_t range, uint64_t seed, uint64_t stream, void *strm);
+
+/* Trusted source, additive mask (gen_additive_mask, S/masks.py:39-54): e = 1 + U[0, emax),
+ * alpha = e*step, comp = -e, both shared at ids: alpha[t][i], comp[t][i]. */
+int ssn_mask_trunc(uint64_t n, uint64_t step, uint64_t emax, uint64_t seed, uint64_t stream, int km1,
+                   const uint64_t *ids, int nids, uint64_t *alpha, uint64_t *comp, uint64_t out_tstride, uint64_t p,
+                   void *strm);
+
+/* Trusted source, multiplicative mask (gen_multiplicative_mask, S/masks.py:67-90): beta
+ * constant per kh x kw window in [1, bmax], shared per input element; beta^-1 shared per
+ * window. Uses Philox streams `stream` and `stream + 1`. */
+int ssn_mask_beta(int nb, int c, int h, int wd, int kh, int kw, uint64_t bmax, uint64_t seed, uint64_t stream,
+                  int km1, const uint64_t *ids, int nids, uint64_t *beta, uint64_t beta_tstride, uint64_t *binv,
+                  uint64_t binv_tstride, uint64_t p, void *strm);
+
+/* Repeat a (nb, c, h/kh, wd/kw) block over windows (np.repeat twice, S/masks.py:84). */
+int ssn_pool_expand(const uint64_t *blk, uint64_t *out, int nb, int c, int h, int wd, int kh, int kw, void *strm);
+
+/* Local share product of sss_linear (S/layers.py:245-255), exact mod p on CUDA cores:
+ * conv  W[party][O][C*kh*kw] x im2col(x[party][img][C][H][W]) -> out[party][img][O][OH*OW]
+ * dense W[party][O][K] x x[party][img][K] -> out[party][img][O]. */
+int ssn_conv_simt(const uint64_t *w, uint64_t w_pstride, const uint64_t *x, uint64_t x_pstride, uint64_t *out,
+                  uint64_t out_pstride, int nparty, int nimg, int O, int C, int H, int W, int kh, int kw, int stride,
+                  int pad, uint64_t p, void *strm);
+int ssn_dense_simt(const uint64_t *w, uint64_t w_pstride, const uint64_t *x, uint64_t x_pstride, uint64_t *out,
+                   uint64_t out_pstride, int nparty, int nimg, int O, int K, uint64_t p, void *strm);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSN_H */

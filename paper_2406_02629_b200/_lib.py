@@ -1,0 +1,120 @@
+"""ctypes binding of libssn_b200.so (the C ABI declared in include/ssn.h).
+
+The product path has NO CPU fallback: if the CUDA library is missing or no CUDA device
+is present, every compute call raises SsnUnavailable.  `build()` compiles the library
+in-tree with nvcc for sm_100a.
+"""
+
+import ctypes
+import os
+import subprocess
+
+import torch
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB_PATH = os.path.join(HERE, "libssn_b200.so")
+CSRC = os.path.join(HERE, "csrc")
+SOURCES = ["ssn_elementwise.cu", "ssn_gemm_simt.cu"]
+NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
+              "-Xcompiler", "-fPIC", "-shared"]
+
+SSN_ERR_ARG, SSN_ERR_CUDA, SSN_ERR_UNSUPPORTED = -1, -2, -3
+
+
+class SsnUnavailable(RuntimeError):
+    """The CUDA extension (or a CUDA device) is missing; there is no CPU fallback."""
+
+
+class SsnKernelError(RuntimeError):
+    pass
+
+
+def build(force=False, verbose=False):
+    srcs = [os.path.join(CSRC, s) for s in SOURCES if os.path.exists(os.path.join(CSRC, s))]
+    deps = srcs + [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h"))]
+    deps.append(os.path.join(ROOT, "include", "ssn.h"))
+    if (not force and os.path.exists(LIB_PATH)
+            and os.path.getmtime(LIB_PATH) >= max(os.path.getmtime(d) for d in deps)):
+        return LIB_PATH
+    cmd = ["nvcc", *NVCC_FLAGS, "-I" + os.path.join(ROOT, "include"), "-I" + CSRC, *srcs,
+           "-lcuda", "-o", LIB_PATH]
+    if verbose:
+        print(" ".join(cmd))
+    subprocess.check_call(cmd)
+    return LIB_PATH
+
+
+_U64, _I64, _I32, _P = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
+
+_SIGS = {
+    "ssn_version": [],
+    "ssn_ewise": [_I32, _P, _P, _P, _U64, _U64, _U64, _U64, _U64, _U64, _P],
+    "ssn_gen": [_P, _U64, _P, _U64, _U64, _U64, _I32, _P, _I32, _P, _U64, _U64, _U64, _I32, _U64, _P],
+    "ssn_rec": [_P, _U64, _U64, _P, _I32, _P, _U64, _U64, _I32, _U64, _P],
+    "ssn_reduce_apply": [_P, _U64, _U64, _I32, _P, _I32, _P, _U64, _U64, _U64, _I32, _U64, _P],
+    "ssn_reshare_finish": [_P, _U64, _U64, _P, _I32, _P, _U64, _P, _U64, _U64, _U64, _P, _U64, _P, _U64,
+                           _U64, _I32, _U64, _P],
+    "ssn_trunc_elite": [_P, _U64, _I32, _I32, _P, _P, _I64, _I64, _I64, _P, _U64, _U64, _I32, _P, _I32, _P,
+                        _U64, _P, _U64, _U64, _P],
+    "ssn_nonlin_elite": [_P, _U64, _I32, _P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _U64, _P],
+    "ssn_encode_signed": [_P, _P, _U64, _P, _U64, _P],
+    "ssn_decode_signed": [_P, _P, _U64, _U64, _P],
+    "ssn_inv": [_P, _P, _U64, _U64, _P],
+    "ssn_rand": [_P, _U64, _U64, _U64, _U64, _U64, _P],
+    "ssn_mask_trunc": [_U64, _U64, _U64, _U64, _U64, _I32, _P, _I32, _P, _P, _U64, _U64, _P],
+    "ssn_mask_beta": [_I32, _I32, _I32, _I32, _I32, _I32, _U64, _U64, _U64, _I32, _P, _I32, _P, _U64, _P,
+                      _U64, _U64, _P],
+    "ssn_pool_expand": [_P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P],
+    "ssn_conv_simt": [_P, _U64, _P, _U64, _P, _U64, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
+                      _I32, _U64, _P],
+    "ssn_dense_simt": [_P, _U64, _P, _U64, _P, _U64, _I32, _I32, _I32, _I32, _U64, _P],
+}
+
+_lib = None
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def load(require_cuda=True):
+    """Load the library (no device needed).  Raises SsnUnavailable if it is missing."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise SsnUnavailable(f"{LIB_PATH} is missing: run __graft_entry__.build() "
+                                 "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        for name, args in _SIGS.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = ctypes.c_int
+        _lib = L
+    if require_cuda and not torch.cuda.is_available():
+        raise SsnUnavailable("no CUDA device: the SSNet B200 path has no CPU fallback")
+    return _lib
+
+
+def call(name, *args):
+    rc = getattr(load(), name)(*args)
+    if rc != 0:
+        if rc == SSN_ERR_ARG:
+            raise ValueError(f"{name}: invalid arguments")
+        raise SsnKernelError(f"{name} failed with code {rc}")
+
+
+def stream_ptr():
+    return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def ptr(t):
+    """Device pointer of a tensor (None -> NULL)."""
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def u64_array(vals):
+    arr = (ctypes.c_uint64 * max(1, len(vals)))(*[int(v) for v in vals])
+    return arr
