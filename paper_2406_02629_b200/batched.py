@@ -1,0 +1,334 @@
+"""Batched lockstep engine: every party and a batch of images per kernel launch.
+
+This is the throughput path (bench.py).  It runs the same protocol as engine.py -- the same
+messages are produced and consumed in HBM, one kernel boundary per protocol hop -- but with
+all n co-resident parties in one launch and a batch of B images folded into the element
+dimension.  Tensors are party-major: value[t] for rank t+1, each (B, *shape) contiguous.
+
+Per op (reference in parentheses, paths relative to /root/reference/pkg/src/ssnet):
+  linear      GEMM for the 2k-1 participants (S/layers.py:245-255)      field GEMM kernel
+              reshare step 1: sub-shares to the front  (S/protocol.py:154-163)   ssn_gen, nbatch = 2k-1
+              step 2: R^T at the k front ranks          (S/protocol.py:165-185)   ssn_reduce_apply, nbatch = k
+              step 3: rec + zero + bias [+ alpha of the next truncation]           ssn_reshare_finish
+  truncation  elite rec / window-decode / floor / round / re-share [+RS check]     ssn_trunc_elite
+              (S/layers.py:277-323); every rank + comp                              ssn_ewise
+  nonlinear   x * beta at the participants (S/layers.py:338-342)                   ssn_ewise
+              elite rec / decode / ReLU / pool / encode (S/layers.py:345-364)      ssn_nonlin_elite
+              plain * beta^-1 at the receivers (S/layers.py:379-380)                ssn_ewise (broadcast)
+  add         local share add (residual, S/sss.py:238)                             ssn_ewise
+  output      rec at the elite + decode (S/protocol.py:289-305)                    ssn_rec, ssn_decode_signed
+Masks come from a device-side trusted source, generated per op just before use
+(S/protocol.py:354-388, S/masks.py): ssn_gen (zero), ssn_mask_trunc, ssn_mask_beta.
+Randomness is device Philox (rng_mode="device"); decoded outputs are RNG-independent, so
+they equal the reference / plaintext exactly (tests/test_gpu_batched.py).
+"""
+
+import time
+
+import numpy as np
+import torch
+
+from . import _lib
+from .gemm import field_conv, field_dense
+from .layers import comm_estimate, consumers, plan_schedule
+from .masks import additive_mask_bound, multiplicative_mask_bound
+from .protocol import VerificationError, extrapolation_coeffs
+from .rng import DeviceRng
+
+
+def _count(shape):
+    n = 1
+    for d in shape:
+        n *= int(d)
+    return n
+
+
+class BatchedEngine:
+    def __init__(self, model, scheme, batch, seed=7, rng_mode="device", verify=False, ordering="ltn",
+                 profile=False):
+        if rng_mode != "device":
+            raise ValueError("the batched engine draws its randomness on the device (rng_mode='device'); "
+                             "use simulate_inference for reference-stream parity runs")
+        self.model = model
+        self.scheme = scheme
+        self.batch = int(batch)
+        self.seed = seed
+        self.verify = verify
+        self.profile = profile
+        self.p = scheme.field.p
+        self.ops, self.digest = plan_schedule(model, scheme, ordering, verify=verify)
+        self.cons = consumers(self.ops)
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        k, n = scheme.k, scheme.n
+        self.k, self.n, self.m = k, n, 2 * k - 1
+        self.w_front = scheme.lagrange_weights(scheme.front_ids)
+        self.w_part = scheme.lagrange_weights(scheme.party_ids[:self.m])
+        R = scheme.reducing_matrix()
+        self.rt = {nout: [R[i][t] for t in range(nout) for i in range(self.m)] for nout in (k, n)}
+        self.ext = [v for row in extrapolation_coeffs(scheme, scheme.front_ids, scheme.party_ids[k:]) for v in row]
+        self.ids_all = _lib.u64_array(scheme.party_ids)
+        self.ids_front = _lib.u64_array(scheme.front_ids)
+        self.runs = 0
+        self.fail = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self._deal_weights()
+        self.kernel_launches = 0
+        self.fault = None
+
+    # ------------------------------------------------------------------ setup
+    def _deal_weights(self):
+        """Weight shares dealt once from lane 1 and reused across runs (S/engine.py:40-49)."""
+        rng = DeviceRng(self.seed, 1)
+        values = self.model.weight_values() if hasattr(self.model, "weight_values") else \
+            {name: qt.values for name, qt in self.model.weights.items()}
+        self.W = {}
+        for name in sorted(values):
+            v = torch.as_tensor(np.asarray(values[name], dtype=np.int64), device=self.dev).contiguous()
+            enc = self._encode(v)
+            out = torch.empty((self.n,) + tuple(v.shape), dtype=torch.int64, device=self.dev)
+            nel = v.numel()
+            _lib.call("ssn_gen", _lib.ptr(enc), 0, None, 0, rng.seed, rng.next_stream(), self.k - 1, self.ids_all,
+                      self.n, _lib.ptr(out), 0, nel, nel, 1, self.p, _lib.stream_ptr())
+            self.W[name] = out
+
+    def _encode(self, v):
+        out = torch.empty_like(v)
+        ovf = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        _lib.call("ssn_encode_signed", _lib.ptr(v), _lib.ptr(out), v.numel(), _lib.ptr(ovf), self.p,
+                  _lib.stream_ptr())
+        return out
+
+    # ------------------------------------------------------------------ helpers
+    def _ew(self, op, a, b, out, n, b_mod=None):
+        """out[:n] = a OP b; b broadcast cyclically with period b_mod (default: full)."""
+        bm = n if b_mod is None else b_mod
+        _lib.call("ssn_ewise", op, _lib.ptr(a), _lib.ptr(b), _lib.ptr(out), n, 1, bm, 1 << 62, 0, self.p,
+                  _lib.stream_ptr())
+        self.kernel_launches += 1
+
+    def comm_per_image(self):
+        """Online elements exchanged per image (reference closed forms, S/layers.py:193-225)."""
+        est = comm_estimate(self.ops, self.scheme, verify=self.verify)
+        online = sum(r["elements"] for r in est if r["kind"] != "offline")
+        offline = next(r["elements"] for r in est if r["kind"] == "offline")
+        return online, offline
+
+    # ------------------------------------------------------------------ run
+    def run(self, x_int, timings=None):
+        """One secure inference of a batch.  x_int: int64 (B, *input_shape), numpy or device.
+        Returns the decoded int64 outputs (numpy, shape (B, *out))."""
+        out = self.run_device(x_int, timings)
+        return out.cpu().numpy()
+
+    def _reveal(self, Y, shape):
+        """Test helper: reconstruct an op output from the front ranks' shares (decoded int64)."""
+        N = self.batch * _count(shape)
+        v = torch.empty(N, dtype=torch.int64, device=self.dev)
+        _lib.call("ssn_rec", _lib.ptr(Y), 0, N, _lib.u64_array(self.w_front), self.k, _lib.ptr(v), 0, N, 1,
+                  self.p, _lib.stream_ptr())
+        out = torch.empty_like(v)
+        _lib.call("ssn_decode_signed", _lib.ptr(v), _lib.ptr(out), N, self.p, _lib.stream_ptr())
+        return out.reshape((self.batch,) + tuple(shape)).cpu().numpy()
+
+    def run_device(self, x_int, timings=None, capture=None):
+        B, n, k, m, p = self.batch, self.n, self.k, self.m, self.p
+        run_id = self.runs
+        self.runs += 1
+        src_rng = DeviceRng(self.seed, 4, run_id)          # trusted source lane
+        party_rng = DeviceRng(self.seed, 5, run_id)        # online protocol lane
+        if isinstance(x_int, torch.Tensor):
+            x = x_int.to(device=self.dev, dtype=torch.int64).contiguous()
+        else:
+            x = torch.as_tensor(np.asarray(x_int, dtype=np.int64), device=self.dev).contiguous()
+        if x.shape[0] != B:
+            raise ValueError(f"batch {x.shape[0]} != engine batch {B}")
+        ev = [] if timings is not None else None
+
+        def mark(label):
+            if ev is not None:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record()
+                ev.append((label, e))
+
+        mark("start")
+        # input dealing (S/engine.py:52-54), lane 3
+        enc = self._encode(x)
+        X = torch.empty((n,) + tuple(x.shape), dtype=torch.int64, device=self.dev)
+        irng = DeviceRng(self.seed, 3, run_id)
+        nel = x.numel()
+        _lib.call("ssn_gen", _lib.ptr(enc), 0, None, 0, irng.seed, irng.next_stream(), k - 1, self.ids_all, n,
+                  _lib.ptr(X), 0, nel, nel, 1, p, _lib.stream_ptr())
+        vals = {-1: X}
+        masked_for = {}          # linear idx -> True when its output already carries alpha
+        remaining = {i: len(c) for i, c in self.cons.items()}
+        result = None
+        for idx, op in enumerate(self.ops):
+            src = idx - 1 if op.src is None else op.src
+            xin = vals.get(src)
+            if op.kind == "linear":
+                y = self._linear(idx, op, xin, src_rng, party_rng)
+                masked_for[idx] = getattr(self, "_fused_alpha", False)
+            elif op.kind == "truncation":
+                y = self._truncation(idx, op, xin, masked_for.get(src, False), src_rng, party_rng)
+            elif op.kind == "nonlinear":
+                y = self._nonlinear(idx, op, xin, src_rng)
+            elif op.kind == "add":
+                other = vals[op.src2]
+                nn = _count(op.out_shape) * B
+                y = torch.empty((n, B) + tuple(op.out_shape), dtype=torch.int64, device=self.dev)
+                self._ew(0, xin, other, y, n * nn)
+            elif op.kind == "output":
+                result = self._output(op, xin)
+                y = None
+            else:
+                raise ValueError(op.kind)
+            vals[idx] = y
+            if self.fault is not None and self.fault[0] == idx and y is not None:
+                y[self.fault[1]].view(-1)[0] += 1              # test hook: corrupt one share
+            if capture is not None and y is not None and op.kind != "linear":
+                capture[idx] = self._reveal(y, op.out_shape)
+            mark(op.kind)
+            # release inputs no longer needed
+            for s in ([src] + ([op.src2] if op.kind == "add" else [])):
+                remaining[s] -= 1
+                if remaining[s] <= 0 and s in vals:
+                    del vals[s]
+        if timings is not None:
+            torch.cuda.synchronize()
+            for (lab0, e0), (lab1, e1) in zip(ev[:-1], ev[1:]):
+                timings[lab1] = timings.get(lab1, 0.0) + e0.elapsed_time(e1)
+        return result
+
+    # ------------------------------------------------------------------ ops
+    def _linear(self, idx, op, X, src_rng, party_rng):
+        B, n, k, m, p = self.batch, self.n, self.k, self.m, self.p
+        w = self.W[op.weight + ".w"]
+        b = self.W[op.weight + ".b"]
+        O = op.out_shape[0]
+        conv = w.dim() == 5
+        if conv:
+            C, H, Wd = op.in_shape
+            acc = field_conv(w[:m], X[:m].reshape(m, B, C, H, Wd), op.stride, op.padding, p, nimg=B, nparty=m)
+            ohw = _count(op.out_shape[1:])
+        else:
+            acc = field_dense(w[:m], X[:m].reshape(m, B, -1), p, nimg=B, nparty=m)
+            ohw = 1
+        N = B * O * ohw
+        nout = n if op.passive_out else k
+        # source: zero shares for every rank (gen_zero_shares)
+        Z = torch.empty((n, N), dtype=torch.int64, device=self.dev)
+        _lib.call("ssn_gen", None, 0, None, 0, src_rng.seed, src_rng.next_stream(), k - 1, self.ids_all, n,
+                  _lib.ptr(Z), 0, N, N, 1, p, _lib.stream_ptr())
+        # fuse the next truncation's alpha into step 3 when the truncation is the sole consumer
+        nxt = self.cons[idx]
+        alpha = None
+        self._fused_alpha = False
+        if len(nxt) == 1 and self.ops[nxt[0]].kind == "truncation":
+            alpha = self._trunc_masks(nxt[0], self.ops[nxt[0]], src_rng)
+            self._fused_alpha = True
+        # step 1 (RESHARE_OUT): participant i -> front j
+        SUB = torch.empty((m, k, N), dtype=torch.int64, device=self.dev)
+        _lib.call("ssn_gen", _lib.ptr(acc), N, None, 0, party_rng.seed, party_rng.next_stream(m), k - 1,
+                  self.ids_front, k, _lib.ptr(SUB), k * N, N, N, m, p, _lib.stream_ptr())
+        # step 2 (RESHARE_BACK): front j applies R^T to its m sub-shares
+        BACK = torch.empty((k, nout, N), dtype=torch.int64, device=self.dev)
+        _lib.call("ssn_reduce_apply", _lib.ptr(SUB), N, k * N, m, _lib.u64_array(self.rt[nout]), nout,
+                  _lib.ptr(BACK), nout * N, N, N, k, p, _lib.stream_ptr())
+        del SUB
+        # step 3: out rank t reconstructs from the k fronts, + zero + bias (+ alpha)
+        Y = torch.empty((n, B) + tuple(op.out_shape), dtype=torch.int64, device=self.dev)
+        _lib.call("ssn_reshare_finish", _lib.ptr(BACK), N, nout * N, _lib.u64_array(self.w_front), k,
+                  _lib.ptr(Z), N, _lib.ptr(b), O, ohw, O, _lib.ptr(alpha[0] if alpha is not None else None), N,
+                  _lib.ptr(Y), N, N, nout, p, _lib.stream_ptr())
+        self.kernel_launches += 5
+        return Y
+
+    def _trunc_masks(self, idx, op, src_rng):
+        """Source: alpha / comp shares for truncation idx (gen_additive_mask), cached."""
+        if not hasattr(self, "_mask_cache"):
+            self._mask_cache = {}
+        got = self._mask_cache.get(idx)
+        if got is not None:
+            return got
+        B, n, p = self.batch, self.n, self.p
+        N = B * _count(op.in_shape)
+        step = op.r * op.divisor
+        emax = additive_mask_bound(self.scheme.field, step, op.value_bound)
+        A = torch.empty((n, N), dtype=torch.int64, device=self.dev)
+        Cm = torch.empty((n, N), dtype=torch.int64, device=self.dev)
+        _lib.call("ssn_mask_trunc", N, step, emax, src_rng.seed, src_rng.next_stream(), self.k - 1, self.ids_all, n,
+                  _lib.ptr(A), _lib.ptr(Cm), N, p, _lib.stream_ptr())
+        self.kernel_launches += 1
+        self._mask_cache[idx] = (A, Cm)
+        return A, Cm
+
+    def _truncation(self, idx, op, X, fused, src_rng, party_rng):
+        B, n, k, p = self.batch, self.n, self.k, self.p
+        N = B * _count(op.in_shape)
+        A, Cm = self._trunc_masks(idx, op, src_rng)
+        self._mask_cache.pop(idx, None)
+        senders = n if self.verify else k
+        if fused:
+            masked = X
+        else:
+            masked = torch.empty((senders, N), dtype=torch.int64, device=self.dev)
+            self._ew(0, X, A, masked, senders * N)
+        FR = torch.empty((n, N), dtype=torch.int64, device=self.dev)
+        _lib.call("ssn_trunc_elite", _lib.ptr(masked), N, senders, k, _lib.u64_array(self.w_front),
+                  _lib.u64_array(self.ext), op.value_bound, op.r, op.divisor, None, party_rng.seed,
+                  party_rng.next_stream(), k - 1, self.ids_all, n, _lib.ptr(FR), N,
+                  _lib.ptr(self.fail) if self.verify else None, N, p, _lib.stream_ptr())
+        Y = torch.empty((n, B) + tuple(op.out_shape), dtype=torch.int64, device=self.dev)
+        self._ew(0, FR, Cm, Y, n * N)
+        self.kernel_launches += 1
+        return Y
+
+    def _nonlinear(self, idx, op, X, src_rng):
+        B, n, k, m, p = self.batch, self.n, self.k, self.m, self.p
+        n_in, n_out = B * _count(op.in_shape), B * _count(op.out_shape)
+        if op.pool_kind is not None:
+            c, h, w = op.in_shape
+            kh, kw = op.pool
+            kind = 1 if op.pool_kind == "max" else 2
+        elif len(op.in_shape) == 3:
+            (c, h, w), kh, kw, kind = op.in_shape, 1, 1, 0
+        else:
+            c, h, w, kh, kw, kind = _count(op.in_shape), 1, 1, 1, 1, 0
+        bmax = multiplicative_mask_bound(self.scheme.field, op.value_bound)
+        BETA = torch.empty((n, n_in), dtype=torch.int64, device=self.dev)
+        BINV = torch.empty((n, n_out), dtype=torch.int64, device=self.dev)
+        _lib.call("ssn_mask_beta", B, c, h, w, kh, kw, bmax, src_rng.seed, src_rng.next_stream(2), k - 1,
+                  self.ids_all, n, _lib.ptr(BETA), n_in, _lib.ptr(BINV), n_out, p, _lib.stream_ptr())
+        MASKED = torch.empty((m, n_in), dtype=torch.int64, device=self.dev)
+        self._ew(2, X, BETA, MASKED, m * n_in)
+        plain = torch.empty(n_out, dtype=torch.int64, device=self.dev)
+        _lib.call("ssn_nonlin_elite", _lib.ptr(MASKED), n_in, m, _lib.u64_array(self.w_part), int(bool(op.relu)),
+                  kind, B, c, h, w, kh, kw, _lib.ptr(plain), p, _lib.stream_ptr())
+        fan = n if op.passive_out else k
+        Y = torch.empty((n, B) + tuple(op.out_shape), dtype=torch.int64, device=self.dev)
+        self._ew(2, BINV, plain, Y, fan * n_out, b_mod=n_out)
+        self.kernel_launches += 2
+        return Y
+
+    def _output(self, op, X):
+        B, n, k, p = self.batch, self.n, self.k, self.p
+        N = B * _count(op.out_shape)
+        if self.verify:
+            scratch = torch.empty(N, dtype=torch.int64, device=self.dev)
+            _lib.call("ssn_trunc_elite", _lib.ptr(X), N, n, k, _lib.u64_array(self.w_front),
+                      _lib.u64_array(self.ext), 0, 1, 1, None, 0, 0, 0, None, 0, _lib.ptr(scratch), 0,
+                      _lib.ptr(self.fail), N, p, _lib.stream_ptr())
+        v = torch.empty(N, dtype=torch.int64, device=self.dev)
+        _lib.call("ssn_rec", _lib.ptr(X), 0, N, _lib.u64_array(self.w_front), k, _lib.ptr(v), 0, N, 1, p,
+                  _lib.stream_ptr())
+        out = torch.empty_like(v)
+        _lib.call("ssn_decode_signed", _lib.ptr(v), _lib.ptr(out), N, p, _lib.stream_ptr())
+        self.kernel_launches += 2
+        if self.verify:
+            self._check_failures()
+        return out.reshape((B,) + tuple(op.out_shape))
+
+    def _check_failures(self):
+        bad = int(self.fail.item())
+        if bad:
+            self.fail.zero_()
+            raise VerificationError(f"{bad} share(s) failed the Reed-Solomon check")

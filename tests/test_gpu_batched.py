@@ -1,0 +1,105 @@
+"""The batched lockstep engine (the bench path) against the oracle: decoded outputs
+(parity tier T1) and every op's reconstructed value (tier T2) equal the integer plaintext;
+verification detects a corrupted share.  GPU only."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import sim
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ssn():
+    import paper_2406_02629_b200 as pkg
+    pkg._lib.load()
+    return pkg
+
+
+def _plain_batch(ops, xb, weights):
+    outs, inter = [], []
+    for i in range(xb.shape[0]):
+        o, vals = sim.plaintext(ops, xb[i], weights)
+        outs.append(o)
+        inter.append(vals)
+    return np.stack(outs), inter
+
+
+def test_reference_model_batched_matches_plaintext(ssn):
+    from paper_2406_02629_b200.batched import BatchedEngine
+    model, _ = ssn.build_reference_model(7, pool="max")
+    weights = {name: qt.values for name, qt in model.weights.items()}
+    F = ssn.PrimeField()
+    for k, n in ((2, 3), (3, 5)):
+        scheme = ssn.SssScheme(F, k, n)
+        B = 8
+        xb = np.stack([ssn.random_input(7, model, index=i)[0] for i in range(B)])
+        eng = BatchedEngine(model, scheme, batch=B, seed=9)
+        ops = [op.meta() for op in eng.ops]
+        want, _ = _plain_batch(ops, xb, weights)
+        for _ in range(2):                       # second run uses fresh randomness
+            assert np.array_equal(eng.run(xb), want)
+
+
+def test_avg_pool_chain_model(ssn):
+    from paper_2406_02629_b200.batched import BatchedEngine
+    model, _ = ssn.build_reference_model(7, pool="avg")
+    weights = {name: qt.values for name, qt in model.weights.items()}
+    scheme = ssn.SssScheme(ssn.PrimeField(), 2, 3)
+    xb = np.stack([ssn.random_input(8, model, index=i)[0] for i in range(4)])
+    eng = BatchedEngine(model, scheme, batch=4, seed=2)
+    want = np.stack([ssn.plaintext_infer(model, xb[i]) for i in range(4)])
+    assert np.array_equal(eng.run(xb), want)
+
+
+@pytest.mark.parametrize("k,n", [(2, 3), (3, 5)])
+def test_tiny_resnet_every_op_reconstructs_to_plaintext(ssn, k, n):
+    from paper_2406_02629_b200 import resnet
+    from paper_2406_02629_b200.batched import BatchedEngine
+    net = resnet.tiny_resnet(seed=3)
+    scheme = ssn.SssScheme(ssn.PrimeField(), k, n)
+    B = 3
+    xb = net.random_inputs(seed=5, batch=B)
+    eng = BatchedEngine(net, scheme, batch=B, seed=11)
+    ops = [op.meta() for op in eng.ops]
+    want, inter = _plain_batch(ops, xb, net.weight_values())
+    cap = {}
+    out = eng.run_device(xb, capture=cap).cpu().numpy()
+    assert np.array_equal(out, want)
+    for idx, got in cap.items():
+        ref = np.stack([inter[b][idx] for b in range(B)])
+        assert np.array_equal(got, ref.reshape(got.shape)), (idx, eng.ops[idx].name)
+    # independent checker: float64 exact plaintext of the DAG
+    pf, _ = resnet.plaintext_forward(net, xb)
+    assert np.array_equal(out, pf)
+
+
+def test_cifar_resnet18_batched_matches_plaintext(ssn):
+    from paper_2406_02629_b200 import resnet
+    from paper_2406_02629_b200.batched import BatchedEngine
+    net = resnet.cifar_resnet18(seed=7)
+    scheme = ssn.SssScheme(ssn.PrimeField(), 2, 3)
+    xb = net.random_inputs(seed=1, batch=2)
+    eng = BatchedEngine(net, scheme, batch=2, seed=3)
+    want, _ = resnet.plaintext_forward(net, xb)
+    assert np.array_equal(eng.run(xb), want)
+
+
+def test_verification_detects_corruption(ssn):
+    from paper_2406_02629_b200 import resnet
+    from paper_2406_02629_b200.batched import BatchedEngine
+    from paper_2406_02629_b200.protocol import VerificationError
+    net = resnet.tiny_resnet(seed=3)
+    scheme = ssn.SssScheme(ssn.PrimeField(), 3, 5)
+    xb = net.random_inputs(seed=6, batch=2)
+    eng = BatchedEngine(net, scheme, batch=2, seed=4, verify=True)
+    want, _ = resnet.plaintext_forward(net, xb)
+    assert np.array_equal(eng.run(xb), want)
+    first_linear = next(i for i, op in enumerate(eng.ops) if op.kind == "linear")
+    eng.fault = (first_linear, 4)            # a passive rank's share of a linear output
+    with pytest.raises(VerificationError):
+        eng.run(xb)
+    eng.fault = None
+    assert np.array_equal(eng.run(xb), want)
