@@ -132,8 +132,8 @@ def multiplicative_mask_bound(p, value_bound):
 
 
 def _inv_vec(x, p):
-    flat = [pow(int(v), p - 2, p) for v in np.asarray(x).ravel()]
-    return np.array(flat, dtype=np.uint64).reshape(np.shape(x))
+    from . import inv_vec
+    return inv_vec(np.asarray(x, dtype=np.uint64), p).reshape(np.shape(x))
 
 
 def source_masks(ops, sch, rng, record_plain=False):
@@ -156,7 +156,7 @@ def source_masks(ops, sch, rng, record_plain=False):
             step = op["r"] * op["divisor"]
             emax = additive_mask_bound(p, step, op["value_bound"])
             e = rng.integers(1, emax + 1, size=tuple(op["in_shape"]), dtype=np.int64)
-            alpha = (e.astype(object) * step % p).astype(np.uint64)
+            alpha = ((e * step) % p).astype(np.uint64)      # e*step < 2^52: exact in int64
             comp = ((-e) % p).astype(np.uint64)
             spread(idx, "alpha", sch.share(alpha, rng))
             spread(idx, "comp", sch.share(comp, rng))

@@ -62,6 +62,9 @@ u64 ssn_o_inv(u64 a, u64 p) {
 /* Elementwise add/sub/mul with optional scalar broadcast of b (b_len==1).
  * share_add/share_sub/share_mul (S/sss.py:238-276), PrimeField.add/sub/mul (S/field.py:89-99). */
 void ssn_o_ewise(int op, const u64 *a, const u64 *b, size_t b_len, u64 *out, size_t n, u64 p) {
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) if (n > 4096)
+#endif
     for (size_t i = 0; i < n; i++) {
         u64 x = a[i], y = b[b_len == 1 ? 0 : i];
         out[i] = op == 0 ? addmod(x, y, p) : op == 1 ? submod(x, y, p) : mulmod(x, y, p);
@@ -75,6 +78,9 @@ void ssn_o_gen(const u64 *secret, const u64 *coeffs, int km1, const u64 *ids, in
                u64 *out, size_t n, u64 p) {
     for (int t = 0; t < nids; t++) {
         u64 pid = ids[t] % p;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) if (n > 4096)
+#endif
         for (size_t i = 0; i < n; i++) {
             u64 acc = secret[i], pw = 1;
             for (int j = 0; j < km1; j++) {
@@ -89,6 +95,9 @@ void ssn_o_gen(const u64 *secret, const u64 *coeffs, int km1, const u64 *ids, in
 /* SssScheme.rec (S/sss.py:172-194): sum_i w_i * s_i over the first m shares.
  * shares: (m, n); weights: m Lagrange weights for the shares' party ids. */
 void ssn_o_rec(const u64 *shares, const u64 *w, int m, u64 *out, size_t n, u64 p) {
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) if (n > 4096)
+#endif
     for (size_t i = 0; i < n; i++) {
         u64 acc = 0;
         for (int j = 0; j < m; j++) acc = addmod(acc, mulmod(shares[(size_t)j * n + i], w[j], p), p);
@@ -100,6 +109,9 @@ void ssn_o_rec(const u64 *shares, const u64 *w, int m, u64 *out, size_t n, u64 p
  * stack: (m, n) sub-shares ascending by source rank; Rt: (nout, m) = R^T rows; out: (nout, n). */
 void ssn_o_reduce_apply(const u64 *stack, const u64 *Rt, int m, int nout, u64 *out, size_t n, u64 p) {
     for (int t = 0; t < nout; t++)
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) if (n > 4096)
+#endif
         for (size_t i = 0; i < n; i++) {
             u128 acc = 0;
             for (int j = 0; j < m; j++) acc += (u128)Rt[t * m + j] * stack[(size_t)j * n + i];
@@ -165,6 +177,9 @@ void ssn_o_round_half_away(const i64 *v, i64 d, i64 *out, size_t n) {
 void ssn_o_trunc_elite(const u64 *masked, const u64 *w, int k, i64 value_bound, i64 r, i64 d,
                        u64 *t_out, size_t n, u64 p) {
     i64 lo = -value_bound + r * d;
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static) if (n > 4096)
+#endif
     for (size_t i = 0; i < n; i++) {
         u64 v = 0;
         for (int j = 0; j < k; j++) v = addmod(v, mulmod(masked[(size_t)j * n + i], w[j], p), p);
@@ -240,4 +255,12 @@ void ssn_o_plain_trunc(const i64 *x, i64 r, i64 d, i64 *out, size_t n) {
         i64 t = floordiv(x[i], r);
         out[i] = d > 1 ? round_half_away1(t, d) : t;
     }
+}
+
+/* Vectorised PrimeField.inv (S/field.py:101-116) for the trusted-source beta^-1. */
+void ssn_o_inv_vec(const u64 *a, u64 *out, size_t n, u64 p) {
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
+    for (size_t i = 0; i < n; i++) out[i] = ssn_o_inv(a[i], p);
 }

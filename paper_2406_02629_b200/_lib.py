@@ -96,7 +96,16 @@ def load(require_cuda=True):
     return _lib
 
 
+_launches = [0]
+
+
+def launch_count():
+    """Number of kernel-launching C-ABI calls made by this process (one kernel each)."""
+    return _launches[0]
+
+
 def call(name, *args):
+    _launches[0] += 1
     rc = getattr(load(), name)(*args)
     if rc != 0:
         if rc == SSN_ERR_ARG:

@@ -105,6 +105,38 @@ class BatchedEngine:
                   _lib.stream_ptr())
         self.kernel_launches += 1
 
+    # ------------------------------------------------------------------ instrumentation
+    _gemm_prof = None
+
+    def enable_gemm_profiling(self):
+        """Record CUDA events around every share-GEMM launch (bench roofline)."""
+        self._gemm_prof = []
+        return self._gemm_prof
+
+    def disable_gemm_profiling(self):
+        self._gemm_prof = None
+
+    def gemm_profile_summary(self, steps):
+        prof = self._gemm_prof or []
+        torch.cuda.synchronize()
+        ms = [a.elapsed_time(b) for a, b, _, _ in prof]
+        macs = [mac for _, _, mac, _ in prof]
+        kernels = sorted({kname for _, _, _, kname in prof})
+        nl = len(prof)
+        L = self.limb_products()
+        return {"launches": nl // max(steps, 1), "ms_total": sum(ms) / max(steps, 1),
+                "ms_per_launch": (sum(ms) / nl) if nl else 0.0,
+                "field_ops_per_launch": (2.0 * sum(macs) / nl) if nl else 0.0,
+                "int8_ops_per_launch": (2.0 * L * sum(macs) / nl) if nl else 0.0,
+                "limb_products": L, "kernel": ",".join(kernels)}
+
+    def limb_products(self):
+        L = (self.p.bit_length() + 7) // 8
+        return L * L
+
+    def out_shape(self):
+        return tuple(self.ops[-1].out_shape)
+
     def comm_per_image(self):
         """Online elements exchanged per image (reference closed forms, S/layers.py:193-225)."""
         est = comm_estimate(self.ops, self.scheme, verify=self.verify)
@@ -205,13 +237,23 @@ class BatchedEngine:
         b = self.W[op.weight + ".b"]
         O = op.out_shape[0]
         conv = w.dim() == 5
+        prof = self._gemm_prof
+        if prof is not None:
+            g0 = torch.cuda.Event(enable_timing=True)
+            g0.record()
         if conv:
             C, H, Wd = op.in_shape
             acc = field_conv(w[:m], X[:m].reshape(m, B, C, H, Wd), op.stride, op.padding, p, nimg=B, nparty=m)
             ohw = _count(op.out_shape[1:])
+            K = C * w.shape[-1] * w.shape[-2]
         else:
             acc = field_dense(w[:m], X[:m].reshape(m, B, -1), p, nimg=B, nparty=m)
             ohw = 1
+            K = w.shape[-1]
+        if prof is not None:
+            g1 = torch.cuda.Event(enable_timing=True)
+            g1.record()
+            prof.append((g0, g1, m * B * ohw * O * K, "ssn_conv_simt" if conv else "ssn_dense_simt"))
         N = B * O * ohw
         nout = n if op.passive_out else k
         # source: zero shares for every rank (gen_zero_shares)
