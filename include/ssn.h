@@ -129,6 +129,22 @@ int ssn_conv_simt(const uint64_t *w, uint64_t w_pstride, const uint64_t *x, uint
 int ssn_dense_simt(const uint64_t *w, uint64_t w_pstride, const uint64_t *x, uint64_t x_pstride, uint64_t *out,
                    uint64_t out_pstride, int nparty, int nimg, int O, int K, uint64_t p, void *strm);
 
+/* Tensor-core field GEMM (tcgen05.mma kind::i8, TMEM accumulators, TMA-fed), the same
+ * contraction as ssn_conv_simt/ssn_dense_simt (S/layers.py:252,254):
+ *  - ssn_limb_split: x[party][rows][K] u64 -> planes[party][L][rows][Kpad] u8 (little-endian
+ *    limbs, zero padded to Kpad % 16 == 0);  used for weights (once) and dense activations.
+ *  - ssn_im2col_limbs: conv unfold (S/model.py:354-371) fused with the limb split:
+ *    x[party][img][C][H][W] -> planes[party][L][img*OH*OW][Kpad], k = (c, i, j).
+ *  - ssn_gemm_tc: out[party][img][O][ohw] (row = img*ohw + pix) = A . B^T mod p with
+ *    A planes [party][L][M][Kpad], B planes [party][L][O][Kpad]; L in {6,7,8};
+ *    requires L * Kpad * 255^2 < 2^32. */
+int ssn_limb_split(const uint64_t *x, uint64_t rows, uint64_t K, uint64_t Kpad, int L, uint8_t *planes,
+                   uint64_t x_pstride, int nparty, void *stream);
+int ssn_im2col_limbs(const uint64_t *x, int nparty, int nimg, int C, int H, int W, int kh, int kw, int stride,
+                     int pad, int L, uint8_t *planes, uint64_t Kpad, uint64_t x_pstride, void *stream);
+int ssn_gemm_tc(const uint8_t *a_planes, const uint8_t *b_planes, int nparty, int L, int M, int O, uint64_t Kpad,
+                uint64_t ohw, uint64_t *out, uint64_t out_pstride, uint64_t p, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "libssn_b200.so")
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["ssn_elementwise.cu", "ssn_gemm_simt.cu"]
+SOURCES = ["ssn_elementwise.cu", "ssn_gemm_simt.cu", "ssn_gemm_tc.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
 
@@ -69,6 +69,9 @@ _SIGS = {
     "ssn_conv_simt": [_P, _U64, _P, _U64, _P, _U64, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
                       _I32, _U64, _P],
     "ssn_dense_simt": [_P, _U64, _P, _U64, _P, _U64, _I32, _I32, _I32, _I32, _U64, _P],
+    "ssn_limb_split": [_P, _U64, _U64, _U64, _I32, _P, _U64, _I32, _P],
+    "ssn_im2col_limbs": [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _U64, _U64, _P],
+    "ssn_gemm_tc": [_P, _P, _I32, _I32, _I32, _I32, _U64, _U64, _P, _U64, _U64, _P],
 }
 
 _lib = None

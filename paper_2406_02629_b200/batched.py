@@ -29,6 +29,7 @@ import numpy as np
 import torch
 
 from . import _lib
+from . import gemm as gemm_mod
 from .gemm import field_conv, field_dense
 from .layers import comm_estimate, consumers, plan_schedule
 from .masks import additive_mask_bound, multiplicative_mask_bound
@@ -70,6 +71,7 @@ class BatchedEngine:
         self.ids_front = _lib.u64_array(scheme.front_ids)
         self.runs = 0
         self.fail = torch.zeros(1, dtype=torch.int64, device=self.dev)
+        self._planes = {}
         self._deal_weights()
         self.kernel_launches = 0
         self.fault = None
@@ -241,19 +243,26 @@ class BatchedEngine:
         if prof is not None:
             g0 = torch.cuda.Event(enable_timing=True)
             g0.record()
+        K = _count(w.shape[2:])
+        ohw = _count(op.out_shape[1:]) if conv else 1
+        tc = gemm_mod.use_tc(p, B * ohw, K, O)
+        planes = None
+        if tc:
+            planes = self._planes.get(op.weight)
+            if planes is None:
+                planes = self._planes[op.weight] = gemm_mod.weight_planes(w[:m].reshape(m, O, K), p, m)
         if conv:
             C, H, Wd = op.in_shape
-            acc = field_conv(w[:m], X[:m].reshape(m, B, C, H, Wd), op.stride, op.padding, p, nimg=B, nparty=m)
-            ohw = _count(op.out_shape[1:])
-            K = C * w.shape[-1] * w.shape[-2]
+            acc = field_conv(w[:m], X[:m].reshape(m, B, C, H, Wd), op.stride, op.padding, p, nimg=B, nparty=m,
+                             planes=planes, force="tc" if tc else "simt")
         else:
-            acc = field_dense(w[:m], X[:m].reshape(m, B, -1), p, nimg=B, nparty=m)
-            ohw = 1
-            K = w.shape[-1]
+            acc = field_dense(w[:m], X[:m].reshape(m, B, -1), p, nimg=B, nparty=m, planes=planes,
+                              force="tc" if tc else "simt")
         if prof is not None:
             g1 = torch.cuda.Event(enable_timing=True)
             g1.record()
-            prof.append((g0, g1, m * B * ohw * O * K, "ssn_conv_simt" if conv else "ssn_dense_simt"))
+            kname = "ssn_gemm_tc" if tc else ("ssn_conv_simt" if conv else "ssn_dense_simt")
+            prof.append((g0, g1, m * B * ohw * O * K, kname))
         N = B * O * ohw
         nout = n if op.passive_out else k
         # source: zero shares for every rank (gen_zero_shares)

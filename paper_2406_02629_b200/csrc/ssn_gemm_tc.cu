@@ -1,0 +1,380 @@
+// ssn_gemm_tc.cu -- exact mod-p share GEMM on the 5th-gen tensor cores (tcgen05, kind::i8).
+//
+// Replaces the object-dtype contraction of sss_linear (S/layers.py:252 conv, :254 dense).
+// Field elements (< 2^(8L)) are split into L little-endian u8 limbs.  For a tile of
+// 128 output rows (activation pixels) x 32 output columns (channels) the CTA keeps 2L-1
+// int32 accumulators in TMEM, one per limb diagonal d = i + j:
+//       D_d = sum_{i+j=d} A_i(128 x K) . B_j(32 x K)^T          (exact: <= L*K*255^2 < 2^32)
+// fed by TMA (4-D tensor maps over [party][limb][row][K], 64-byte swizzle) through a
+// 3-stage mbarrier pipeline; one elected thread issues the L^2 tcgen05.mma per 32-wide K
+// slice.  The epilogue reads TMEM (tcgen05.ld), recombines sum_d D_d * (2^(8d) mod p) in
+// 128-bit registers and reduces mod p (Barrett), writing canonical u64 shares straight into
+// the [party][img][O][OH*OW] layout the protocol kernels consume.
+//
+// Operand preparation (also here): ssn_limb_split (row-major u64 -> K-major u8 limb planes:
+// weights once per model, dense activations) and ssn_im2col_limbs (implicit conv unfold
+// S/model.py:354-371 fused with the limb split, shared-memory transposed so both the gather
+// and the plane writes are coalesced).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include "ssn_field.cuh"
+#include "ssn.h"
+
+namespace {
+
+constexpr int BM = 128;        // UMMA_M: rows per tile
+constexpr int BN = 32;         // UMMA_N: output channels per tile
+constexpr int BK = 64;         // bytes of K per pipeline stage (= one 64B swizzle atom row)
+constexpr int UK = 32;         // K per tcgen05.mma.kind::i8
+constexpr int STAGES = 3;
+constexpr int MAXL = 8;
+
+struct CdTable { u64 c[2 * MAXL - 1]; };
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)), "r"(parity));
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                            int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+
+// UMMA shared-memory descriptor: K-major, 64-byte swizzle, 8-row core groups 512 B apart.
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
+    d |= (uint64_t)0 << 16;                          // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(512 >> 4) << 32;                 // SBO
+    d |= (uint64_t)1 << 46;                          // version (sm_100)
+    d |= (uint64_t)4 << 61;                          // SWIZZLE_64B
+    return d;
+}
+
+// instruction descriptor: D=S32, A=B=U8, K-major both, N=BN, M=BM
+constexpr uint32_t kIdesc = (2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int L>
+__global__ void __launch_bounds__(128, 1)
+k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, u64 *__restrict__ out,
+          u64 out_pstride, u64 ohw, int O, int M, int nkb, SsnField f, u64 r64, CdTable cd) {
+    constexpr int ND = 2 * L - 1;
+    constexpr int A_BYTES = L * BM * BK;
+    constexpr int B_BYTES = L * BN * BK;
+    constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *full = reinterpret_cast<uint64_t *>(base + STAGES * STAGE_BYTES);
+    uint64_t *empty = full + STAGES;
+    uint64_t *done = empty + STAGES;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, party = blockIdx.z;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ---- TMA producer ----
+        for (int kb = 0; kb < nkb; kb++) {
+            const int s = kb % STAGES;
+            const uint32_t ph = (kb / STAGES) & 1;
+            mbar_wait(&empty[s], ph ^ 1);
+            mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+            uint8_t *sa = base + s * STAGE_BYTES;
+            tma_load_4d(sa, &tmA, &full[s], kb * BK, m0, 0, party);
+            tma_load_4d(sa + A_BYTES, &tmB, &full[s], kb * BK, n0, 0, party);
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---- MMA issuer: L^2 limb products per 32-wide K slice into 2L-1 diagonal accumulators ----
+        for (int kb = 0; kb < nkb; kb++) {
+            const int s = kb % STAGES;
+            const uint32_t ph = (kb / STAGES) & 1;
+            mbar_wait(&full[s], ph);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t sa = smem_u32(base + s * STAGE_BYTES);
+            const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < BK / UK; kk++) {
+#pragma unroll
+                for (int i = 0; i < L; i++) {
+                    const uint64_t adesc = umma_desc_sw64(sa + i * BM * BK + kk * UK);
+#pragma unroll
+                    for (int j = 0; j < L; j++) {
+                        const uint64_t bdesc = umma_desc_sw64(sb + j * BN * BK + kk * UK);
+                        const uint32_t first = (kb == 0 && kk == 0 && (i == 0 || j == L - 1));
+                        mma_i8(tmem + (uint32_t)((i + j) * BN), adesc, bdesc, first ? 0u : 1u);
+                    }
+                }
+            }
+            mma_commit(&empty[s]);
+        }
+        mma_commit(done);
+    }
+    __syncwarp();
+
+    // ---- epilogue: all 4 warps; warp w owns TMEM lanes 32w..32w+31 (tile rows) ----
+    mbar_wait(done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int row = m0 + warp * 32 + lane;
+    const bool row_ok = row < M;
+    const u64 img = row_ok ? (u64)row / ohw : 0;
+    const u64 pix = row_ok ? (u64)row - img * ohw : 0;
+    u64 *obase = out + (u64)party * out_pstride + img * (u64)O * ohw + pix;
+    const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+        u64 lo[16], hi[16];
+#pragma unroll
+        for (int c = 0; c < 16; c++) lo[c] = hi[c] = 0;
+#pragma unroll
+        for (int d = 0; d < ND; d++) {
+            uint32_t r[16];
+            tmem_ld16(lane_addr + (uint32_t)(d * BN + c0), r);
+            const u64 w = cd.c[d];
+#pragma unroll
+            for (int c = 0; c < 16; c++) {
+                const u64 plo = (u64)r[c] * w, phi = __umul64hi((u64)r[c], w);
+                lo[c] += plo;
+                hi[c] += phi + (lo[c] < plo);
+            }
+        }
+        if (row_ok) {
+#pragma unroll
+            for (int c = 0; c < 16; c++) {
+                const int col = n0 + c0 + c;
+                if (col < O) obase[(u64)col * ohw] = ssn_reduce128(u128s{lo[c], hi[c]}, f, r64);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void *p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+int make_map(CUtensorMap *map, const uint8_t *planes, int Kpad, int rows, int L, int P, int box_rows) {
+    auto enc = get_encode();
+    if (!enc) return SSN_ERR_CUDA;
+    cuuint64_t dims[4] = {(cuuint64_t)Kpad, (cuuint64_t)rows, (cuuint64_t)L, (cuuint64_t)P};
+    cuuint64_t strides[3] = {(cuuint64_t)Kpad, (cuuint64_t)Kpad * rows, (cuuint64_t)Kpad * rows * L};
+    cuuint32_t box[4] = {(cuuint32_t)BK, (cuuint32_t)box_rows, (cuuint32_t)L, 1};
+    cuuint32_t estr[4] = {1, 1, 1, 1};
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t *>(planes), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? 0 : SSN_ERR_CUDA;
+}
+
+template <int L>
+int launch_tc(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int Kpad, u64 *out, u64 out_pstride,
+              u64 ohw, u64 p, cudaStream_t st) {
+    CUtensorMap ma, mb;
+    if (make_map(&ma, a, Kpad, M, L, nparty, BM) || make_map(&mb, b, Kpad, O, L, nparty, BN)) return SSN_ERR_CUDA;
+    constexpr int smem = STAGES * (L * BM * BK + L * BN * BK) + 1024 + 256;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_gemm_tc<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+            return SSN_ERR_CUDA;
+        attr = true;
+    }
+    CdTable cd = {};
+    unsigned __int128 w = 1;
+    for (int d = 0; d < 2 * L - 1; d++) {
+        cd.c[d] = (u64)(w % p);
+        w = (w % p) << 8;
+    }
+    SsnField f = ssn_make_field(p);
+    u64 r64 = (u64)((((unsigned __int128)1) << 64) % p);
+    dim3 grid((O + BN - 1) / BN, (M + BM - 1) / BM, nparty);
+    k_gemm_tc<L><<<grid, 128, smem, st>>>(ma, mb, out, out_pstride, ohw, O, M, (Kpad + BK - 1) / BK, f, r64, cd);
+    return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
+}
+
+// ---------------------------------------------------------------- operand preparation
+// x: [P][rows][K] u64 (row-major) -> planes [P][L][rows][Kpad] u8, zero padded in K.
+__global__ void k_limb_split(const u64 *__restrict__ x, u64 rows, u64 K, u64 Kpad, int L, uint8_t *__restrict__ planes,
+                             u64 x_pstride, u64 total_chunks) {
+    const u64 chunks_per_row = Kpad / 8;
+    for (u64 g = blockIdx.x * (u64)blockDim.x + threadIdx.x; g < total_chunks; g += (u64)gridDim.x * blockDim.x) {
+        const u64 per_party = rows * chunks_per_row;
+        const u64 party = g / per_party;
+        const u64 rem = g - party * per_party;
+        const u64 r = rem / chunks_per_row, kc = (rem - r * chunks_per_row) * 8;
+        const u64 *src = x + party * x_pstride + r * K;
+        u64 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; q++) v[q] = (kc + q < K) ? src[kc + q] : 0;
+        uint8_t *dst = planes + party * (u64)L * rows * Kpad + r * Kpad + kc;
+        for (int l = 0; l < L; l++) {
+            u64 packed = 0;
+#pragma unroll
+            for (int q = 0; q < 8; q++) packed |= ((v[q] >> (8 * l)) & 0xFF) << (8 * q);
+            *reinterpret_cast<u64 *>(dst + (u64)l * rows * Kpad) = packed;
+        }
+    }
+}
+
+// conv: x [P][img][C][H][W] -> planes [P][L][img*OH*OW][Kpad], k = (c, i, j) like im2col.
+// Block: 32 rows x 64 k; gather coalesced along rows, transpose in shared memory, write
+// 8-byte limb packs along k.
+__global__ void __launch_bounds__(256) k_im2col_limbs(const u64 *__restrict__ x, int C, int H, int W, int kh, int kw,
+                                                       int stride, int pad, int OH, int OW, int L, u64 rows, int K,
+                                                       int Kpad, uint8_t *__restrict__ planes, u64 x_pstride) {
+    __shared__ u64 sv[32][65];
+    const int party = blockIdx.z;
+    const u64 r0 = (u64)blockIdx.y * 32;
+    const int k0 = blockIdx.x * 64;
+    const int t = threadIdx.x;
+    const u64 *xp = x + (u64)party * x_pstride;
+    const int ohw = OH * OW;
+    {
+        const int rr = t & 31;
+        const u64 r = r0 + rr;
+        u64 img = 0;
+        int oy = 0, ox = 0;
+        const bool rok = r < rows;
+        if (rok) {
+            img = r / ohw;
+            int pix = (int)(r - img * ohw);
+            oy = pix / OW;
+            ox = pix - oy * OW;
+        }
+        for (int kk = t >> 5; kk < 64; kk += 8) {
+            const int k = k0 + kk;
+            u64 v = 0;
+            if (rok && k < K) {
+                const int c = k / (kh * kw);
+                const int rem = k - c * kh * kw;
+                const int i = rem / kw, j = rem - i * kw;
+                const int sy = oy * stride + i - pad, sx = ox * stride + j - pad;
+                if (sy >= 0 && sy < H && sx >= 0 && sx < W) v = xp[((img * C + c) * H + sy) * (u64)W + sx];
+            }
+            sv[rr][kk] = v;
+        }
+    }
+    __syncthreads();
+    {
+        const int rr = t >> 3, kc = (t & 7) * 8;
+        const u64 r = r0 + rr;
+        if (r < rows && k0 + kc < Kpad) {
+            uint8_t *dst = planes + (u64)party * L * rows * Kpad + r * Kpad + k0 + kc;
+            for (int l = 0; l < L; l++) {
+                u64 packed = 0;
+#pragma unroll
+                for (int q = 0; q < 8; q++) packed |= ((sv[rr][kc + q] >> (8 * l)) & 0xFF) << (8 * q);
+                *reinterpret_cast<u64 *>(dst + (u64)l * rows * Kpad) = packed;
+            }
+        }
+    }
+}
+
+}  // namespace
+
+extern "C" int ssn_limb_split(const u64 *x, u64 rows, u64 K, u64 Kpad, int L, uint8_t *planes, u64 x_pstride,
+                              int nparty, void *stream) {
+    if (L < 1 || L > MAXL || Kpad % 16 || Kpad < K || nparty < 1) return SSN_ERR_ARG;
+    u64 total = (u64)nparty * rows * (Kpad / 8);
+    if (total == 0) return 0;
+    u64 blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_limb_split<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, rows, K, Kpad, L, planes, x_pstride, total);
+    return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
+}
+
+extern "C" int ssn_im2col_limbs(const u64 *x, int nparty, int nimg, int C, int H, int W, int kh, int kw, int stride,
+                                int pad, int L, uint8_t *planes, u64 Kpad, u64 x_pstride, void *stream) {
+    if (L < 1 || L > MAXL || Kpad % 16 || nparty < 1 || nimg < 1) return SSN_ERR_ARG;
+    const int OH = (H + 2 * pad - kh) / stride + 1, OW = (W + 2 * pad - kw) / stride + 1;
+    const int K = C * kh * kw;
+    if ((u64)K > Kpad || OH < 1 || OW < 1) return SSN_ERR_ARG;
+    const u64 rows = (u64)nimg * OH * OW;
+    dim3 grid((unsigned)((Kpad + 63) / 64), (unsigned)((rows + 31) / 32), (unsigned)nparty);
+    k_im2col_limbs<<<grid, 256, 0, (cudaStream_t)stream>>>(x, C, H, W, kh, kw, stride, pad, OH, OW, L, rows, K,
+                                                           (int)Kpad, planes, x_pstride);
+    return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
+}
+
+// planes A [P][L][M][Kpad] (rows = activation pixels), B [P][L][O][Kpad] (weights);
+// out [P] at out_pstride: element (row, col) -> out[(row / ohw) * O * ohw + col * ohw + row % ohw].
+// Exactness requires L * K * 255^2 < 2^32 (host splits K otherwise).
+extern "C" int ssn_gemm_tc(const uint8_t *a_planes, const uint8_t *b_planes, int nparty, int L, int M, int O,
+                           u64 Kpad, u64 ohw, u64 *out, u64 out_pstride, u64 p, void *stream) {
+    if (L < 1 || L > MAXL || Kpad % 16 || M < 1 || O < 1 || nparty < 1 || ohw < 1) return SSN_ERR_ARG;
+    if ((unsigned __int128)L * Kpad * 65025 >= ((unsigned __int128)1 << 32)) return SSN_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (L) {
+        case 6: return launch_tc<6>(a_planes, b_planes, nparty, M, O, (int)Kpad, out, out_pstride, ohw, p, st);
+        case 7: return launch_tc<7>(a_planes, b_planes, nparty, M, O, (int)Kpad, out, out_pstride, ohw, p, st);
+        case 8: return launch_tc<8>(a_planes, b_planes, nparty, M, O, (int)Kpad, out, out_pstride, ohw, p, st);
+        default: return SSN_ERR_UNSUPPORTED;
+    }
+}

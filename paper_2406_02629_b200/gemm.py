@@ -1,37 +1,93 @@
 """Field GEMM / conv dispatch: the local share product of sss_linear (S/layers.py:245-255).
 
-All paths are exact mod p.  Large conv/dense tiles go to the tcgen05 int8 limb GEMM
-(csrc/ssn_gemm_tc.cu) once it is available for the shape; everything else to the CUDA-core
-kernel (csrc/ssn_gemm_simt.cu).
+All paths are exact mod p.
+* tensor-core path (csrc/ssn_gemm_tc.cu): u8 limb planes, tcgen05.mma kind::i8 with the
+  2L-1 limb-diagonal accumulators in TMEM, TMA-fed; used whenever the shape fills a
+  128-row tile and the prime has 6..8 limbs (the default p = 2^45 - 55 has L = 6).
+* CUDA-core path (csrc/ssn_gemm_simt.cu): 64-bit multiply, 128-bit accumulate; small or
+  odd shapes and tiny test primes.
 """
 
 import torch
 
 from . import _lib
 
+TC_MIN_ROWS = 128
 
-def field_conv(w, x, stride, padding, p, nimg=1, nparty=1):
-    """w: (O, C, kh, kw) [per party], x: (C, H, W) [per party/image] -> (O, OH, OW)."""
+
+def limbs(p):
+    return (p.bit_length() + 7) // 8
+
+
+def kpad(K):
+    return (K + 15) // 16 * 16
+
+
+def tc_supported(p, K):
+    L = limbs(p)
+    return 6 <= L <= 8 and L * kpad(K) * 65025 < (1 << 32)
+
+
+def weight_planes(w, p, nparty=1):
+    """(nparty, O, K) u64 field weights -> (nparty, L, O, Kpad) u8 limb planes."""
+    w2 = w.reshape(nparty, w.shape[-2], w.shape[-1]).contiguous()
+    O, K = w2.shape[-2:]
+    L, Kp = limbs(p), kpad(K)
+    planes = torch.empty((nparty, L, O, Kp), dtype=torch.uint8, device=w.device)
+    _lib.call("ssn_limb_split", _lib.ptr(w2), O, K, Kp, L, _lib.ptr(planes), O * K, nparty, _lib.stream_ptr())
+    return planes
+
+
+def use_tc(p, rows, K, O):
+    return rows >= TC_MIN_ROWS and O >= 16 and K >= 32 and tc_supported(p, K)
+
+
+def field_conv(w, x, stride, padding, p, nimg=1, nparty=1, planes=None, force=None):
+    """w: (nparty, O, C, kh, kw), x: (nparty, nimg, C, H, W) -> (nparty, nimg, O, OH, OW)
+    (leading unit dims squeezed when nparty == nimg == 1)."""
     O, C, kh, kw = w.shape[-4:]
     H, W = x.shape[-2:]
     OH = (H + 2 * padding - kh) // stride + 1
     OW = (W + 2 * padding - kw) // stride + 1
-    w = w.contiguous()
+    K = C * kh * kw
     x = x.contiguous()
     out = torch.empty((nparty, nimg, O, OH, OW) if (nparty > 1 or nimg > 1) else (O, OH, OW),
                       dtype=torch.int64, device=x.device)
+    rows = nimg * OH * OW
+    tc = use_tc(p, rows, K, O) if force is None else force == "tc"
+    if tc:
+        L, Kp = limbs(p), kpad(K)
+        if planes is None:
+            planes = weight_planes(w.reshape(nparty, O, K), p, nparty)
+        a = torch.empty((nparty, L, rows, Kp), dtype=torch.uint8, device=x.device)
+        _lib.call("ssn_im2col_limbs", _lib.ptr(x), nparty, nimg, C, H, W, kh, kw, stride, padding, L, _lib.ptr(a),
+                  Kp, nimg * C * H * W, _lib.stream_ptr())
+        _lib.call("ssn_gemm_tc", _lib.ptr(a), _lib.ptr(planes), nparty, L, rows, O, Kp, OH * OW, _lib.ptr(out),
+                  nimg * O * OH * OW, p, _lib.stream_ptr())
+        return out
+    w = w.contiguous()
     _lib.call("ssn_conv_simt", _lib.ptr(w), O * C * kh * kw, _lib.ptr(x), nimg * C * H * W, _lib.ptr(out),
               nimg * O * OH * OW, nparty, nimg, O, C, H, W, kh, kw, stride, padding, p, _lib.stream_ptr())
     return out
 
 
-def field_dense(w, x, p, nimg=1, nparty=1):
-    """w: (O, K), x: (K,) -> (O,)."""
+def field_dense(w, x, p, nimg=1, nparty=1, planes=None, force=None):
+    """w: (nparty, O, K), x: (nparty, nimg, K) -> (nparty, nimg, O) (squeezed for 1 x 1)."""
     O, K = w.shape[-2:]
-    w = w.contiguous()
     x = x.contiguous()
     out = torch.empty((nparty, nimg, O) if (nparty > 1 or nimg > 1) else (O,), dtype=torch.int64,
                       device=x.device)
+    tc = use_tc(p, nimg, K, O) if force is None else force == "tc"
+    if tc:
+        L, Kp = limbs(p), kpad(K)
+        if planes is None:
+            planes = weight_planes(w.reshape(nparty, O, K), p, nparty)
+        a = torch.empty((nparty, L, nimg, Kp), dtype=torch.uint8, device=x.device)
+        _lib.call("ssn_limb_split", _lib.ptr(x), nimg, K, Kp, L, _lib.ptr(a), nimg * K, nparty, _lib.stream_ptr())
+        _lib.call("ssn_gemm_tc", _lib.ptr(a), _lib.ptr(planes), nparty, L, nimg, O, Kp, 1, _lib.ptr(out), nimg * O,
+                  p, _lib.stream_ptr())
+        return out
+    w = w.contiguous()
     _lib.call("ssn_dense_simt", _lib.ptr(w), O * K, _lib.ptr(x), nimg * K, _lib.ptr(out), nimg * O, nparty,
               nimg, O, K, p, _lib.stream_ptr())
     return out

@@ -1,0 +1,86 @@
+"""tcgen05 limb GEMM (csrc/ssn_gemm_tc.cu) against the CUDA-core kernel and the CPU oracle.
+Structured cases first so a layout bug shows up as a readable failure.  GPU only."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+P = oracle.DEFAULT_PRIME
+
+
+@pytest.fixture(scope="module")
+def g():
+    import paper_2406_02629_b200 as pkg
+    from paper_2406_02629_b200 import gemm
+    pkg._lib.load()
+    return gemm
+
+
+def dev(a):
+    return torch.as_tensor(np.asarray(a, dtype=np.uint64).astype(np.int64), device="cuda")
+
+
+def host(t):
+    return t.cpu().numpy().astype(np.uint64)
+
+
+def _dense_both(g, w, x, nimg):
+    tc = host(g.field_dense(dev(w), dev(x), P, nimg=nimg, force="tc"))
+    simt = host(g.field_dense(dev(w), dev(x), P, nimg=nimg, force="simt"))
+    return tc, simt
+
+
+@pytest.mark.parametrize("case", ["limb0", "limb5", "ones", "maxval"])
+def test_structured_dense(g, case):
+    rows, O, K = 128, 32, 64
+    if case == "limb0":
+        w = np.arange(O * K, dtype=np.uint64).reshape(O, K) % 7
+        x = np.arange(rows * K, dtype=np.uint64).reshape(rows, K) % 5
+    elif case == "limb5":
+        w = (np.arange(O * K, dtype=np.uint64).reshape(O, K) % 7) << np.uint64(40)
+        x = (np.arange(rows * K, dtype=np.uint64).reshape(rows, K) % 5) << np.uint64(40)
+    elif case == "ones":
+        w = np.ones((O, K), dtype=np.uint64)
+        x = np.ones((rows, K), dtype=np.uint64)
+    else:
+        w = np.full((O, K), P - 1, dtype=np.uint64)
+        x = np.full((rows, K), P - 1, dtype=np.uint64)
+    tc, simt = _dense_both(g, w, x, rows)
+    want = oracle.gemm(x, w.T)                     # (rows, O)
+    assert np.array_equal(simt.reshape(rows, O), want)
+    assert np.array_equal(tc.reshape(rows, O), want), (case, tc.reshape(rows, O)[:2, :4], want[:2, :4])
+
+
+@pytest.mark.parametrize("rows,O,K", [(128, 32, 64), (300, 48, 200), (1000, 64, 576), (257, 1000, 2048),
+                                      (640, 96, 4608)])
+def test_random_dense_shapes(g, rows, O, K):
+    rng = np.random.default_rng(rows + O + K)
+    w = rng.integers(0, P, size=(O, K), dtype=np.uint64)
+    x = rng.integers(0, P, size=(rows, K), dtype=np.uint64)
+    tc, simt = _dense_both(g, w, x, rows)
+    assert np.array_equal(tc, simt)
+    if rows * O * K <= 64 * 1024 * 1024:
+        assert np.array_equal(tc.reshape(rows, O), oracle.gemm(x, w.T))
+
+
+@pytest.mark.parametrize("C,H,W,O,k,s,pad,nimg,nparty", [
+    (3, 32, 32, 64, 3, 1, 1, 2, 1),
+    (64, 14, 14, 64, 1, 1, 0, 3, 2),
+    (16, 15, 17, 48, 3, 2, 1, 2, 3),
+    (3, 56, 56, 64, 7, 2, 3, 1, 1),
+    (256, 7, 7, 128, 3, 1, 1, 4, 5),
+])
+def test_conv_tc_vs_simt(g, C, H, W, O, k, s, pad, nimg, nparty):
+    rng = np.random.default_rng(C * H + O)
+    w = rng.integers(0, P, size=(nparty, O, C, k, k), dtype=np.uint64)
+    x = rng.integers(0, P, size=(nparty, nimg, C, H, W), dtype=np.uint64)
+    tc = g.field_conv(dev(w), dev(x), s, pad, P, nimg=nimg, nparty=nparty, force="tc")
+    simt = g.field_conv(dev(w), dev(x), s, pad, P, nimg=nimg, nparty=nparty, force="simt")
+    assert np.array_equal(host(tc), host(simt))
+    # one party/image against the oracle's im2col GEMM
+    want = oracle.gemm(w[0].reshape(O, -1), oracle.im2col(x[0, 0], k, k, s, pad))
+    got = host(tc).reshape(nparty, nimg, O, -1)[0, 0] if (nparty > 1 or nimg > 1) else host(tc).reshape(O, -1)
+    assert np.array_equal(got, want)
