@@ -1,0 +1,26 @@
+"""Run one warm step of the batched engine inside a cudaProfilerStart/Stop range (for ncu
+--profile-from-start off).  Usage: python tools/profile_step.py [workload] [batch]"""
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2406_02629_b200.batched import BatchedEngine  # noqa: E402
+from paper_2406_02629_b200.field import PrimeField  # noqa: E402
+from paper_2406_02629_b200.sss import SssScheme  # noqa: E402
+
+wl = sys.argv[1] if len(sys.argv) > 1 else "resnet152-5pc"
+B = int(sys.argv[2]) if len(sys.argv) > 2 else 16
+kind, k, n, verify, _ = bench.WORKLOADS[wl]
+model = bench.build_model(kind)
+eng = BatchedEngine(model, SssScheme(PrimeField(), k, n), batch=B, seed=7, verify=verify)
+x = torch.as_tensor(model.random_inputs(seed=1, batch=B), device="cuda")
+eng.run_device(x)
+torch.cuda.synchronize()
+torch.cuda.profiler.start()
+eng.run_device(x)
+torch.cuda.synchronize()
+torch.cuda.profiler.stop()
+print("profiled one step:", wl, "batch", B)
