@@ -1,22 +1,25 @@
 // ssn_elementwise.cu -- HBM-bound field kernels of the SSNet hot path (sm_100a) + C-ABI.
 //
-// Every kernel is a grid-stride loop over elements with one thread per element per
-// iteration (coalesced u64 loads/stores); multi-party operands are addressed as strided
-// 2-D views base + b*stride_b + j*stride_j so one launch covers all co-resident parties.
+// Every kernel is a grid-stride loop with one thread per element per iteration (coalesced
+// u64 loads/stores); multi-party operands are strided 2-D views base + b*stride_b + j*stride_j
+// so one launch covers all co-resident parties.  Loops over parties / points / coefficients
+// are fully unrolled against compile-time maxima with runtime guards, so every per-element
+// temporary lives in registers (no local-memory stack).
 // Reference functions restated (paths relative to /root/reference/pkg/src/ssnet):
-//   ssn_ewise            share_add/sub/mul, PrimeField.add/sub/mul   S/sss.py:238-276, S/field.py:89-99
-//   ssn_gen              SssScheme.gen (Horner over party ids)      S/sss.py:118-147
-//   ssn_rec              SssScheme.rec (Lagrange weighted sum)       S/sss.py:172-194
-//   ssn_reduce_apply     reshare step 2, R^T @ stack                 S/protocol.py:165-185
-//   ssn_reshare_finish   reshare step 3 + rerand + bias (+ trunc mask) S/protocol.py:187-198, S/layers.py:260-267,290-293
+//   ssn_ewise            share_add/sub/mul, PrimeField.add/sub/mul     S/sss.py:238-276, S/field.py:89-99
+//   ssn_gen              SssScheme.gen (Horner over party ids)         S/sss.py:118-147
+//   ssn_rec              SssScheme.rec (Lagrange weighted sum)          S/sss.py:172-194
+//   ssn_reduce_apply     reshare step 2, R^T @ stack                    S/protocol.py:165-185
+//   ssn_reshare_finish   reshare step 3 + rerand + bias (+ trunc mask)  S/protocol.py:187-198, S/layers.py:260-267,290-293
 //   ssn_trunc_elite      masked truncation at the elite (+ fresh shares, + RS check)  S/layers.py:295-315
-//   ssn_nonlin_elite     masked ReLU / max / sum pool at the elite   S/layers.py:345-364
-//   ssn_mask_*           trusted-source masks                        S/masks.py:39-96, S/protocol.py:354-388
+//   ssn_nonlin_elite     masked ReLU / max / sum pool at the elite      S/layers.py:345-364
+//   ssn_mask_*           trusted-source masks                           S/masks.py:39-96, S/protocol.py:354-388
 #include "ssn_field.cuh"
 #include "ssn.h"
 
-#define SSN_MAXJ 16
-#define SSN_MAXK 8
+#define SSN_MAXJ 16      // parties / share ids
+#define SSN_MAXP 9       // points of one reconstruction (2k-1 <= 9)
+#define SSN_MAXK 8       // polynomial coefficients k-1
 
 static int ssn_blocks(u64 n, int threads = 256) {
     u64 b = (n + threads - 1) / threads;
@@ -31,30 +34,180 @@ static inline int ssn_check_launch() {
     return e == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
 
-struct PowTable {            // pw[t][j] = ids[t]^(j+1) mod p
-    u64 pw[SSN_MAXJ][SSN_MAXK];
+// ---------------------------------------------------------------- small linear combinations
+// Every constant linear combination on the protocol path -- Lagrange weights at 0 (rec),
+// the reducing matrix R (reshare step 2), RS extrapolation rows and party-id powers (gen) --
+// is a ratio of small integers for the default party ids 1..n (e.g. rec over ids 1..5 at 0
+// has weights 5,-10,10,-5,1).  The host finds N_j / D with |N_j| < 2^13 by rational
+// reconstruction; the device then evaluates D^-1 * sum N_j x_j with 32-bit multiplies and a
+// single reduction instead of one full 64x64 mulmod per term.  Any other constant set falls
+// back to full mulmods (flag ok = 0).
+struct LinRow {
+    u64 w[SSN_MAXJ];        // full field constants (fallback)
+    int32_t n[SSN_MAXJ];    // small signed numerators
+    u64 dinv;               // D^-1 mod p
+    int one;                // D == 1
 };
+
+static int ratrec(u64 w, u64 p, long long &a, long long &b) {
+    // a/b == w (mod p) with |a|, |b| <= 2^15 (half extended Euclid)
+    const long long A = 1 << 15;
+    __int128 r0 = p, r1 = w % p, t0 = 0, t1 = 1;
+    while (r1 > A) {
+        __int128 q = r0 / r1, r2 = r0 - q * r1, t2 = t0 - q * t1;
+        r0 = r1; r1 = r2; t0 = t1; t1 = t2;
+    }
+    a = (long long)r1;
+    b = (long long)t1;
+    if (b < 0) { a = -a; b = -b; }
+    return b > 0 && b <= A;
+}
+
+static long long gcdll(long long x, long long y) {
+    if (x < 0) x = -x;
+    while (y) { long long t = x % y; x = y; y = t; }
+    return x;
+}
+
+static u64 inv_host(u64 a, u64 p) {
+    __int128 lm = 1, hm = 0, low = a % p, high = p;
+    while (low > 1) {
+        __int128 r = high / low, nm = hm - lm * r, nw = high - low * r;
+        hm = lm; high = low; lm = nm; low = nw;
+    }
+    __int128 v = lm % (__int128)p;
+    if (v < 0) v += p;
+    return (u64)v;
+}
+
+// returns 1 if the row has a small representation
+static int make_row(LinRow &r, const u64 *w, int m, u64 p) {
+    long long a[SSN_MAXJ], b[SSN_MAXJ], D = 1;
+    for (int j = 0; j < SSN_MAXJ; j++) { r.w[j] = 0; r.n[j] = 0; }
+    for (int j = 0; j < m; j++) r.w[j] = w[j] % p;
+    r.dinv = 1;
+    r.one = 1;
+    // 16 terms of x * |N| with x < p < 2^47 and |N| < 2^13 stay below 2^64
+    int ok = p > (1ull << 32) && p < (1ull << 47);
+    for (int j = 0; j < m && ok; j++) {
+        ok = ratrec(r.w[j], p, a[j], b[j]);
+        if (ok) {
+            D = D / gcdll(D, b[j]) * b[j];
+            ok = D < (1 << 15);
+        }
+    }
+    for (int j = 0; j < m && ok; j++) {
+        long long nj = a[j] * (D / b[j]);
+        ok = nj > -(1 << 13) && nj < (1 << 13);
+        r.n[j] = (int32_t)nj;
+    }
+    if (ok) {
+        r.dinv = inv_host((u64)D, p);
+        r.one = D == 1;
+    }
+    return ok;
+}
+
+struct Weights { LinRow r; int small; };
+struct RTable { LinRow r[SSN_MAXJ]; int small; };
+struct ExtTable { LinRow r[SSN_MAXP]; int small; };
+struct PowTable {            // row t: ids[t]^(j+1) mod p, j < km1
+    LinRow r[SSN_MAXJ];
+    int small;
+};
+
+static Weights make_weights(const u64 *w, int m, u64 p) {
+    Weights W;
+    W.small = make_row(W.r, w, m, p);
+    return W;
+}
 
 static PowTable make_pows(const u64 *ids, int nids, int km1, u64 p) {
     PowTable t;
-    for (int a = 0; a < nids; a++) {
+    t.small = 1;
+    for (int a = 0; a < SSN_MAXJ; a++) {
+        u64 row[SSN_MAXK] = {0};
         unsigned __int128 acc = 1;
-        for (int j = 0; j < km1; j++) {
-            acc = acc * (ids[a] % p) % p;
-            t.pw[a][j] = (u64)acc;
+        if (a < nids)
+            for (int j = 0; j < km1; j++) {
+                acc = acc * (ids[a] % p) % p;
+                row[j] = (u64)acc;
+            }
+        int ok = make_row(t.r[a], row, km1, p);
+        if (a < nids) {
+            // gen accumulates only positive terms: require D == 1 and non-negative numerators
+            for (int j = 0; j < km1; j++) ok = ok && t.r[a].n[j] >= 0;
+            t.small = t.small && ok && t.r[a].one;
         }
     }
     return t;
 }
 
-struct Weights { u64 w[SSN_MAXJ]; };
+__device__ __forceinline__ u64 mul_small(u64 x, uint32_t c) {
+    // x < 2^62, c < 2^13: (xh*c << 32) + xl*c with two 32x32 products
+    return ((u64)(uint32_t)(x >> 32) * c << 32) + (u64)(uint32_t)x * c;
+}
+
+// sum_j coef_j * x_j over j < m (coefficients of row r)
+template <int MAXM>
+__device__ __forceinline__ u64 lincomb(const u64 (&x)[MAXM], const LinRow &r, int small, int m,
+                                       const SsnField &f) {
+    if (small) {
+        u64 pos = 0, neg = 0;
+#pragma unroll
+        for (int j = 0; j < MAXM; j++)
+            if (j < m) {
+                const int32_t c = r.n[j];
+                if (c >= 0) pos += mul_small(x[j], (uint32_t)c);
+                else neg += mul_small(x[j], (uint32_t)(-c));
+            }
+        const u64 v = ssn_submod(ssn_reduce64(pos, f), ssn_reduce64(neg, f), f.p);
+        return r.one ? v : ssn_mulmod(v, r.dinv, f);
+    }
+    u64 acc = 0;
+#pragma unroll
+    for (int j = 0; j < MAXM; j++)
+        if (j < m) acc = ssn_addmod(acc, ssn_mulmod(x[j], r.w[j], f), f.p);
+    return acc;
+}
+
+// Polynomial coefficients c_0..c_{km1-1} for element i: host-fed or Philox pairs.
+__device__ __forceinline__ void load_coeffs(u64 (&c)[SSN_MAXK], const u64 *__restrict__ coeffs, u64 n, u64 i,
+                                            int km1, u64 seed, u64 stream, const SsnField &f) {
+    if (coeffs) {
+#pragma unroll
+        for (int j = 0; j < SSN_MAXK; j++)
+            if (j < km1) c[j] = coeffs[(u64)j * n + i];
+    } else {
+#pragma unroll
+        for (int jp = 0; jp < SSN_MAXK / 2; jp++)
+            if (2 * jp < km1) ssn_rand_field2(seed, stream, i, jp, f, c[2 * jp], c[2 * jp + 1]);
+    }
+}
+
+// share at id t: s + sum_j c_j * ids[t]^(j+1)
+__device__ __forceinline__ u64 horner_at(u64 s, const u64 (&c)[SSN_MAXK], const PowTable &pw, int t, int km1,
+                                         const SsnField &f) {
+    if (pw.small) {
+        u64 acc = s;
+#pragma unroll
+        for (int j = 0; j < SSN_MAXK; j++)
+            if (j < km1) acc += mul_small(c[j], (uint32_t)pw.r[t].n[j]);
+        return ssn_reduce64(acc, f);
+    }
+    u64 acc = s;
+#pragma unroll
+    for (int j = 0; j < SSN_MAXK; j++)
+        if (j < km1) acc = ssn_addmod(acc, ssn_mulmod(c[j], pw.r[t].w[j], f), f.p);
+    return acc;
+}
 
 // ------------------------------------------------------------------ ewise
 __global__ void k_ewise(int op, const u64 *__restrict__ a, const u64 *__restrict__ b, u64 *__restrict__ out,
                         u64 n, u64 b_div, u64 b_mod, u64 b_div2, u64 b_mul2, SsnField f) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
         u64 x = a[i];
-        u64 y = op == 3 ? 0 : b[(i / b_div) % b_mod + (i / b_div2) * b_mul2];
+        u64 y = op == 3 ? 0 : b[(b_div == 1 ? i : i / b_div) % b_mod + (i / b_div2) * b_mul2];
         u64 r;
         if (op == 0) r = ssn_addmod(x, y, f.p);
         else if (op == 1) r = ssn_submod(x, y, f.p);
@@ -75,27 +228,18 @@ extern "C" int ssn_ewise(int op, const u64 *a, const u64 *b, u64 *out, u64 n, u6
 
 // ------------------------------------------------------------------ gen
 // out[b][t][i] = secret[b][i] + sum_j c_j[b][i] * ids[t]^(j+1)
-// coeffs[b][j][i] when host-fed, else Philox(seed, stream + b, i, j).
 __global__ void k_gen(const u64 *__restrict__ secret, u64 s_b, const u64 *__restrict__ coeffs, u64 c_b, u64 seed,
                       u64 stream, int km1, PowTable pw, int nids, u64 *__restrict__ out, u64 o_b, u64 o_t, u64 n,
                       int nb, SsnField f) {
-    u64 total = n * (u64)nb;
+    const u64 total = n * (u64)nb;
     for (u64 g = blockIdx.x * (u64)blockDim.x + threadIdx.x; g < total; g += (u64)gridDim.x * blockDim.x) {
-        u64 b = g / n, i = g - b * n;
-        u64 s = secret ? secret[b * s_b + i] : 0;
+        const u64 b = nb == 1 ? 0 : g / n, i = g - b * n;
+        const u64 s = secret ? secret[b * s_b + i] : 0;
         u64 c[SSN_MAXK];
+        load_coeffs(c, coeffs ? coeffs + b * c_b : nullptr, n, i, km1, seed, stream + b, f);
 #pragma unroll
-        for (int j = 0; j < SSN_MAXK; j++) {
-            if (j < km1)
-                c[j] = coeffs ? coeffs[b * c_b + (u64)j * n + i] : ssn_rand_range(seed, stream + b, i, j, f.p);
-        }
-        for (int t = 0; t < nids; t++) {
-            u64 acc = s;
-#pragma unroll
-            for (int j = 0; j < SSN_MAXK; j++)
-                if (j < km1) acc = ssn_addmod(acc, ssn_mulmod(c[j], pw.pw[t][j], f), f.p);
-            out[b * o_b + t * o_t + i] = acc;
-        }
+        for (int t = 0; t < SSN_MAXJ; t++)
+            if (t < nids) out[b * o_b + t * o_t + i] = horner_at(s, c, pw, t, km1, f);
     }
 }
 
@@ -112,16 +256,17 @@ extern "C" int ssn_gen(const u64 *secret, u64 secret_bstride, const u64 *coeffs,
 }
 
 // ------------------------------------------------------------------ rec
-// out[b][i] = sum_j w[j] * pts[b][j][i]
 __global__ void k_rec(const u64 *__restrict__ pts, u64 p_b, u64 p_j, Weights w, int m, u64 *__restrict__ out,
                       u64 o_b, u64 n, int nb, SsnField f) {
-    u64 total = n * (u64)nb;
+    const u64 total = n * (u64)nb;
     for (u64 g = blockIdx.x * (u64)blockDim.x + threadIdx.x; g < total; g += (u64)gridDim.x * blockDim.x) {
-        u64 b = g / n, i = g - b * n;
+        const u64 b = nb == 1 ? 0 : g / n, i = g - b * n;
         const u64 *base = pts + b * p_b + i;
-        u64 acc = 0;
-        for (int j = 0; j < m; j++) acc = ssn_addmod(acc, ssn_mulmod(base[j * p_j], w.w[j], f), f.p);
-        out[b * o_b + i] = acc;
+        u64 x[SSN_MAXJ];
+#pragma unroll
+        for (int j = 0; j < SSN_MAXJ; j++)
+            if (j < m) x[j] = base[j * p_j];
+        out[b * o_b + i] = lincomb<SSN_MAXJ>(x, w.r, w.small, m, f);
     }
 }
 
@@ -129,8 +274,7 @@ extern "C" int ssn_rec(const u64 *pts, u64 pts_bstride, u64 pts_jstride, const u
                        u64 out_bstride, u64 n, int nbatch, u64 p, void *strm) {
     if (m < 1 || m > SSN_MAXJ || nbatch < 1) return SSN_ERR_ARG;
     if (n == 0) return 0;
-    Weights W;
-    for (int j = 0; j < m; j++) W.w[j] = w[j] % p;
+    Weights W = make_weights(w, m, p);
     k_rec<<<ssn_blocks(n * nbatch), 256, 0, (cudaStream_t)strm>>>(pts, pts_bstride, pts_jstride, W, m, out,
                                                                   out_bstride, n, nbatch, ssn_make_field(p));
     return ssn_check_launch();
@@ -138,51 +282,55 @@ extern "C" int ssn_rec(const u64 *pts, u64 pts_bstride, u64 pts_jstride, const u
 
 // ------------------------------------------------------------------ reduce apply (reshare step 2)
 // out[b][t][i] = sum_j Rt[t][j] * pts[b][j][i]  -- b = front rank, j = sub-share source, t = out rank
-struct RTable { u64 r[SSN_MAXJ][SSN_MAXJ]; };
-
 __global__ void k_reduce_apply(const u64 *__restrict__ pts, u64 p_b, u64 p_j, RTable R, int m, int nout,
-                               u64 *__restrict__ out, u64 o_b, u64 o_t, u64 n, int nb, SsnField f, u64 r64) {
-    u64 total = n * (u64)nb;
+                               u64 *__restrict__ out, u64 o_b, u64 o_t, u64 n, int nb, SsnField f) {
+    const u64 total = n * (u64)nb;
     for (u64 g = blockIdx.x * (u64)blockDim.x + threadIdx.x; g < total; g += (u64)gridDim.x * blockDim.x) {
-        u64 b = g / n, i = g - b * n;
+        const u64 b = nb == 1 ? 0 : g / n, i = g - b * n;
         const u64 *base = pts + b * p_b + i;
-        u64 v[SSN_MAXJ];
-        for (int j = 0; j < m; j++) v[j] = base[j * p_j];
-        for (int t = 0; t < nout; t++) {
-            u128s acc = {0, 0};
-            for (int j = 0; j < m; j++) ssn_mac(acc, v[j], R.r[t][j]);
-            out[b * o_b + t * o_t + i] = ssn_reduce128(acc, f, r64);
-        }
+        u64 v[SSN_MAXP];
+#pragma unroll
+        for (int j = 0; j < SSN_MAXP; j++)
+            if (j < m) v[j] = base[j * p_j];
+#pragma unroll
+        for (int t = 0; t < SSN_MAXJ; t++)
+            if (t < nout) out[b * o_b + t * o_t + i] = lincomb<SSN_MAXP>(v, R.r[t], R.small, m, f);
     }
 }
 
-static u64 r64_of(u64 p) { return (u64)((((unsigned __int128)1) << 64) % p); }
-
 extern "C" int ssn_reduce_apply(const u64 *pts, u64 pts_bstride, u64 pts_jstride, int m, const u64 *rt, int nout,
                                 u64 *out, u64 out_bstride, u64 out_tstride, u64 n, int nbatch, u64 p, void *strm) {
-    if (m < 1 || m > SSN_MAXJ || nout < 1 || nout > SSN_MAXJ || nbatch < 1) return SSN_ERR_ARG;
+    if (m < 1 || m > SSN_MAXP || nout < 1 || nout > SSN_MAXJ || nbatch < 1) return SSN_ERR_ARG;
     if (n == 0) return 0;
     RTable R;
-    for (int t = 0; t < nout; t++)
-        for (int j = 0; j < m; j++) R.r[t][j] = rt[t * m + j] % p;
+    R.small = 1;
+    for (int t = 0; t < SSN_MAXJ; t++) {
+        u64 row[SSN_MAXJ] = {0};
+        if (t < nout)
+            for (int j = 0; j < m; j++) row[j] = rt[t * m + j];
+        int ok = make_row(R.r[t], row, m, p);
+        if (t < nout) R.small = R.small && ok;
+    }
     k_reduce_apply<<<ssn_blocks(n * nbatch), 256, 0, (cudaStream_t)strm>>>(pts, pts_bstride, pts_jstride, R, m, nout,
                                                                            out, out_bstride, out_tstride, n, nbatch,
-                                                                           ssn_make_field(p), r64_of(p));
+                                                                           ssn_make_field(p));
     return ssn_check_launch();
 }
 
 // ------------------------------------------------------------------ reshare step 3 (+rerand, +bias, +alpha)
-// out[b][i] = sum_j w[j]*pts[b][j][i] + zero[b][i] + bias[b][(i / bias_div) % bias_mod] (+ alpha[b][i])
 __global__ void k_reshare_finish(const u64 *__restrict__ pts, u64 p_b, u64 p_j, Weights w, int k,
                                  const u64 *__restrict__ zero, u64 z_b, const u64 *__restrict__ bias, u64 bi_b,
                                  u64 bias_div, u64 bias_mod, const u64 *__restrict__ alpha, u64 a_b,
                                  u64 *__restrict__ out, u64 o_b, u64 n, int nb, SsnField f) {
-    u64 total = n * (u64)nb;
+    const u64 total = n * (u64)nb;
     for (u64 g = blockIdx.x * (u64)blockDim.x + threadIdx.x; g < total; g += (u64)gridDim.x * blockDim.x) {
-        u64 b = g / n, i = g - b * n;
+        const u64 b = nb == 1 ? 0 : g / n, i = g - b * n;
         const u64 *base = pts + b * p_b + i;
-        u64 acc = 0;
-        for (int j = 0; j < k; j++) acc = ssn_addmod(acc, ssn_mulmod(base[j * p_j], w.w[j], f), f.p);
+        u64 x[SSN_MAXP];
+#pragma unroll
+        for (int j = 0; j < SSN_MAXP; j++)
+            if (j < k) x[j] = base[j * p_j];
+        u64 acc = lincomb<SSN_MAXP>(x, w.r, w.small, k, f);
         if (zero) acc = ssn_addmod(acc, zero[b * z_b + i], f.p);
         if (bias) acc = ssn_addmod(acc, bias[b * bi_b + (i / bias_div) % bias_mod], f.p);
         if (alpha) acc = ssn_addmod(acc, alpha[b * a_b + i], f.p);
@@ -194,10 +342,9 @@ extern "C" int ssn_reshare_finish(const u64 *pts, u64 pts_bstride, u64 pts_jstri
                                   const u64 *zero, u64 zero_bstride, const u64 *bias, u64 bias_bstride,
                                   u64 bias_div, u64 bias_mod, const u64 *alpha, u64 alpha_bstride, u64 *out,
                                   u64 out_bstride, u64 n, int nbatch, u64 p, void *strm) {
-    if (k < 1 || k > SSN_MAXJ || nbatch < 1 || bias_div == 0 || bias_mod == 0) return SSN_ERR_ARG;
+    if (k < 1 || k > SSN_MAXP || nbatch < 1 || bias_div == 0 || bias_mod == 0) return SSN_ERR_ARG;
     if (n == 0) return 0;
-    Weights W;
-    for (int j = 0; j < k; j++) W.w[j] = w[j] % p;
+    Weights W = make_weights(w, k, p);
     k_reshare_finish<<<ssn_blocks(n * nbatch), 256, 0, (cudaStream_t)strm>>>(
         pts, pts_bstride, pts_jstride, W, k, zero, zero_bstride, bias, bias_bstride, bias_div, bias_mod, alpha,
         alpha_bstride, out, out_bstride, n, nbatch, ssn_make_field(p));
@@ -205,11 +352,6 @@ extern "C" int ssn_reshare_finish(const u64 *pts, u64 pts_bstride, u64 pts_jstri
 }
 
 // ------------------------------------------------------------------ truncation elite
-// v = sum_{j<k} w[j]*pts[j][i]; RS check of pts[k..npts) against Lagrange extrapolation;
-// shifted = ((v - lo) mod p) + lo, lo = -value_bound + r*d; t = floor(shifted / r);
-// d > 1: t = round_half_away(t, d); then fresh shares out[tt][i] = gen(t mod p) at ids.
-struct ExtTable { u64 e[SSN_MAXJ][SSN_MAXK]; };
-
 __device__ __forceinline__ i64 ssn_floordiv(i64 a, i64 b) {
     i64 q = a / b;
     if ((a % b != 0) && ((a < 0) != (b < 0))) q -= 1;
@@ -217,46 +359,39 @@ __device__ __forceinline__ i64 ssn_floordiv(i64 a, i64 b) {
 }
 
 __global__ void k_trunc_elite(const u64 *__restrict__ pts, u64 p_j, int npts, int k, Weights w, ExtTable ext,
-                              i64 lo, i64 r, i64 d, const u64 *__restrict__ coeffs, u64 seed, u64 stream, int km1,
-                              PowTable pw, int nids, u64 *__restrict__ out, u64 o_t,
+                              i64 lo, u64 neglo_mod, i64 r, int rshift, i64 d, const u64 *__restrict__ coeffs,
+                              u64 seed, u64 stream, int km1, PowTable pw, int nids, u64 *__restrict__ out, u64 o_t,
                               unsigned long long *__restrict__ fail, u64 n, SsnField f) {
     unsigned long long bad_local = 0;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-        u64 s[SSN_MAXJ];
-        for (int j = 0; j < npts; j++) s[j] = pts[j * p_j + i];
-        u64 v = 0;
-        for (int j = 0; j < k; j++) v = ssn_addmod(v, ssn_mulmod(s[j], w.w[j], f), f.p);
-        for (int e = k; e < npts; e++) {
-            u64 pred = 0;
-            for (int j = 0; j < k; j++) pred = ssn_addmod(pred, ssn_mulmod(s[j], ext.e[e - k][j], f), f.p);
-            bad_local += (pred != s[e]);
+        u64 s[SSN_MAXP];
+#pragma unroll
+        for (int j = 0; j < SSN_MAXP; j++)
+            if (j < npts) s[j] = pts[j * p_j + i];
+        const u64 v = lincomb<SSN_MAXP>(s, w.r, w.small, k, f);
+#pragma unroll
+        for (int q = 1; q < SSN_MAXP; q++) {                       // RS checks of points k..npts-1
+            if (q >= k && q < npts) bad_local += (lincomb<SSN_MAXP>(s, ext.r[q - k], ext.small, k, f) != s[q]);
         }
-        // window decode: u = (v - lo) mod p with -lo >= 0 (lo may be negative or positive)
-        u64 neglo_mod = lo <= 0 ? ssn_reduce64((u64)(-lo), f) : (f.p - ssn_reduce64((u64)lo, f)) % f.p;
-        u64 u = ssn_addmod(v, neglo_mod, f.p);
-        i64 shifted = (i64)u + lo;
-        i64 t = ssn_floordiv(shifted, r);
+        // window decode into [lo, lo + p), floor division by r, round half away by d
+        const u64 u = ssn_addmod(v, neglo_mod, f.p);
+        const i64 shifted = (i64)u + lo;
+        i64 t = rshift >= 0 ? (shifted >> rshift) : ssn_floordiv(shifted, r);   // arithmetic shift == floor
         if (d > 1) {
-            i64 a = t < 0 ? -t : t;
-            i64 q = ssn_floordiv(2 * a + d, 2 * d);
-            t = t < 0 ? -q : q;
+            const i64 a = t < 0 ? -t : t;
+            const i64 qd = (2 * a + d) / (2 * d);
+            t = t < 0 ? -qd : qd;
         }
-        u64 tm = t >= 0 ? ssn_reduce64((u64)t, f) : (f.p - ssn_reduce64((u64)(-t), f)) % f.p;
+        const u64 tm = t >= 0 ? ssn_reduce64((u64)t, f) : (f.p - ssn_reduce64((u64)(-t), f)) % f.p;
         if (nids == 0) {
             out[i] = tm;
             continue;
         }
         u64 c[SSN_MAXK];
+        load_coeffs(c, coeffs, n, i, km1, seed, stream, f);
 #pragma unroll
-        for (int j = 0; j < SSN_MAXK; j++)
-            if (j < km1) c[j] = coeffs ? coeffs[(u64)j * n + i] : ssn_rand_range(seed, stream, i, j, f.p);
-        for (int tt = 0; tt < nids; tt++) {
-            u64 acc = tm;
-#pragma unroll
-            for (int j = 0; j < SSN_MAXK; j++)
-                if (j < km1) acc = ssn_addmod(acc, ssn_mulmod(c[j], pw.pw[tt][j], f), f.p);
-            out[tt * o_t + i] = acc;
-        }
+        for (int tt = 0; tt < SSN_MAXJ; tt++)
+            if (tt < nids) out[tt * o_t + i] = horner_at(tm, c, pw, tt, km1, f);
     }
     if (fail && bad_local) atomicAdd(fail, bad_local);
 }
@@ -265,21 +400,31 @@ extern "C" int ssn_trunc_elite(const u64 *pts, u64 pts_jstride, int npts, int k,
                                i64 value_bound, i64 r, i64 d, const u64 *coeffs, u64 seed, u64 stream, int km1,
                                const u64 *ids, int nids, u64 *out, u64 out_tstride, unsigned long long *fail, u64 n,
                                u64 p, void *strm) {
-    if (k < 1 || npts < k || npts > SSN_MAXJ || npts - k > SSN_MAXJ || r < 1 || d < 1 || km1 < 0 ||
-        km1 > SSN_MAXK || nids < 0 || nids > SSN_MAXJ)
+    if (k < 1 || k > SSN_MAXP || npts < k || npts > SSN_MAXP || r < 1 || d < 1 || km1 < 0 || km1 > SSN_MAXK ||
+        nids < 0 || nids > SSN_MAXJ)
         return SSN_ERR_ARG;
     if (n == 0) return 0;
-    Weights W;
-    for (int j = 0; j < k; j++) W.w[j] = w[j] % p;
-    ExtTable E = {};
-    if (npts > k && ext)
-        for (int e = 0; e < npts - k; e++)
-            for (int j = 0; j < k; j++) E.e[e][j] = ext[e * k + j] % p;
-    PowTable pw = nids ? make_pows(ids, nids, km1, p) : PowTable{};
-    i64 lo = -value_bound + r * d;
-    k_trunc_elite<<<ssn_blocks(n), 256, 0, (cudaStream_t)strm>>>(pts, pts_jstride, npts, k, W, E, lo, r, d, coeffs,
-                                                                 seed, stream, km1, pw, nids, out, out_tstride, fail,
-                                                                 n, ssn_make_field(p));
+    Weights W = make_weights(w, k, p);
+    ExtTable E;
+    E.small = 1;
+    for (int e = 0; e < SSN_MAXP; e++) {
+        u64 row[SSN_MAXJ] = {0};
+        if (e < npts - k && ext)
+            for (int j = 0; j < k; j++) row[j] = ext[e * k + j];
+        int ok = make_row(E.r[e], row, k, p);
+        if (e < npts - k) E.small = E.small && ok;
+    }
+    PowTable pw = make_pows(ids, nids, km1, p);
+    const i64 lo = -value_bound + r * d;
+    const u64 neglo_mod = lo <= 0 ? (u64)(-lo) % p : (p - (u64)lo % p) % p;
+    int rshift = -1;
+    if ((r & (r - 1)) == 0) {
+        rshift = 0;
+        while ((1ll << rshift) < r) rshift++;
+    }
+    k_trunc_elite<<<ssn_blocks(n), 256, 0, (cudaStream_t)strm>>>(pts, pts_jstride, npts, k, W, E, lo, neglo_mod, r,
+                                                                 rshift, d, coeffs, seed, stream, km1, pw, nids, out,
+                                                                 out_tstride, fail, n, ssn_make_field(p));
     return ssn_check_launch();
 }
 
@@ -291,17 +436,26 @@ __global__ void k_nonlin_elite(const u64 *__restrict__ pts, u64 p_j, int m, Weig
                                SsnField f) {
     const int oh = h / kh, ow = wd / kw;
     for (u64 o = blockIdx.x * (u64)blockDim.x + threadIdx.x; o < n_out; o += (u64)gridDim.x * blockDim.x) {
-        u64 img = o / ((u64)c * oh * ow);
-        u64 rem = o - img * ((u64)c * oh * ow);
-        int ci = (int)(rem / ((u64)oh * ow));
-        int rr = (int)(rem % ((u64)oh * ow));
-        int y = rr / ow, x = rr % ow;
+        u64 base_in;
+        if (pool_kind == 0) {
+            base_in = o;
+        } else {
+            const u64 img = o / ((u64)c * oh * ow);
+            const u64 rem = o - img * ((u64)c * oh * ow);
+            const int ci = (int)(rem / ((u64)oh * ow));
+            const int rr = (int)(rem % ((u64)oh * ow));
+            const int y = rr / ow, x = rr % ow;
+            base_in = ((img * c + ci) * (u64)h + (u64)(y * kh)) * wd + (u64)(x * kw);
+        }
         i64 acc = pool_kind == 1 ? INT64_MIN : 0;
         for (int a = 0; a < kh; a++)
             for (int bq = 0; bq < kw; bq++) {
-                u64 i = ((img * c + ci) * (u64)h + (u64)(y * kh + a)) * wd + (u64)(x * kw + bq);
-                u64 v = 0;
-                for (int j = 0; j < m; j++) v = ssn_addmod(v, ssn_mulmod(pts[j * p_j + i], w.w[j], f), f.p);
+                const u64 i = base_in + (u64)a * wd + bq;
+                u64 x[SSN_MAXP];
+#pragma unroll
+                for (int j = 0; j < SSN_MAXP; j++)
+                    if (j < m) x[j] = pts[j * p_j + i];
+                const u64 v = lincomb<SSN_MAXP>(x, w.r, w.small, m, f);
                 i64 sv = v > f.half ? (i64)v - (i64)f.p : (i64)v;
                 if (relu && sv <= 0) sv = 0;
                 if (pool_kind == 1) acc = sv > acc ? sv : acc;
@@ -313,12 +467,11 @@ __global__ void k_nonlin_elite(const u64 *__restrict__ pts, u64 p_j, int m, Weig
 
 extern "C" int ssn_nonlin_elite(const u64 *pts, u64 pts_jstride, int m, const u64 *w, int relu, int pool_kind,
                                 int nb, int c, int h, int wd, int kh, int kw, u64 *plain, u64 p, void *strm) {
-    if (m < 1 || m > SSN_MAXJ || pool_kind < 0 || pool_kind > 2 || kh < 1 || kw < 1 || h % kh || wd % kw)
+    if (m < 1 || m > SSN_MAXP || pool_kind < 0 || pool_kind > 2 || kh < 1 || kw < 1 || h % kh || wd % kw)
         return SSN_ERR_ARG;
     if (pool_kind == 0 && (kh != 1 || kw != 1)) return SSN_ERR_ARG;
-    Weights W;
-    for (int j = 0; j < m; j++) W.w[j] = w[j] % p;
-    u64 n_out = (u64)nb * c * (h / kh) * (wd / kw);
+    Weights W = make_weights(w, m, p);
+    const u64 n_out = (u64)nb * c * (h / kh) * (wd / kw);
     if (n_out == 0) return 0;
     k_nonlin_elite<<<ssn_blocks(n_out), 256, 0, (cudaStream_t)strm>>>(pts, pts_jstride, m, W, relu, pool_kind, c, h,
                                                                       wd, kh, kw, plain, n_out, ssn_make_field(p));
@@ -329,8 +482,8 @@ extern "C" int ssn_nonlin_elite(const u64 *pts, u64 pts_jstride, int m, const u6
 __global__ void k_encode(const i64 *__restrict__ x, u64 *__restrict__ out, u64 n, SsnField f,
                          unsigned long long *overflow) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-        i64 v = x[i];
-        u64 mag = v < 0 ? (u64)(-v) : (u64)v;
+        const i64 v = x[i];
+        const u64 mag = v < 0 ? (u64)(-v) : (u64)v;
         if (mag > f.half && overflow) atomicAdd(overflow, 1ull);
         out[i] = v < 0 ? f.p - mag : mag;
     }
@@ -343,7 +496,7 @@ extern "C" int ssn_encode_signed(const i64 *x, u64 *out, u64 n, unsigned long lo
 
 __global__ void k_decode(const u64 *__restrict__ v, i64 *__restrict__ out, u64 n, SsnField f) {
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-        u64 x = v[i];
+        const u64 x = v[i];
         out[i] = x > f.half ? (i64)x - (i64)f.p : (i64)x;
     }
 }
@@ -375,37 +528,25 @@ extern "C" int ssn_rand(u64 *out, u64 n, u64 lo, u64 range, u64 seed, u64 stream
 }
 
 // ------------------------------------------------------------------ trusted source (device speed mode)
-// Zero shares: out[t][i] = sum_j c_j(i) id_t^(j+1)   (gen_zero_shares, S/masks.py:93-96)
-// is ssn_gen with secret = NULL.
-//
-// Additive mask (S/masks.py:39-54): e = 1 + U[0, emax); alpha = e*step; comp = -e;
-// alpha/comp shared over all ids.  Philox draw j = 0 is e, 1..km1 alpha coeffs,
-// km1+1..2km1 comp coeffs.
+// Additive mask (S/masks.py:39-54): e = 1 + U[0, emax); alpha = e*step; comp = -e; both shared.
+// Philox draw j = 0 is e; alpha / comp coefficients come from streams stream+1 / stream+2.
 __global__ void k_mask_trunc(u64 n, u64 step, u64 emax, u64 seed, u64 stream, int km1, PowTable pw, int nids,
                              u64 *__restrict__ alpha, u64 *__restrict__ comp, u64 o_t, SsnField f) {
+    const u64 stepm = ssn_reduce64(step, f);
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-        u64 e = 1 + ssn_rand_range(seed, stream, i, 0, emax);
-        u64 a = ssn_mulmod(ssn_reduce64(e, f), ssn_reduce64(step, f), f);
-        u64 cm = ssn_reduce64(e, f);
-        cm = cm ? f.p - cm : 0;
+        const u64 e = 1 + ssn_rand_range(seed, stream, i, 0, emax);
+        const u64 em = ssn_reduce64(e, f);
+        const u64 a = ssn_mulmod(em, stepm, f);
+        const u64 cm = em ? f.p - em : 0;
         u64 ca[SSN_MAXK], cc[SSN_MAXK];
+        load_coeffs(ca, nullptr, n, i, km1, seed, stream + 1, f);
+        load_coeffs(cc, nullptr, n, i, km1, seed, stream + 2, f);
 #pragma unroll
-        for (int j = 0; j < SSN_MAXK; j++)
-            if (j < km1) {
-                ca[j] = ssn_rand_range(seed, stream, i, 1 + j, f.p);
-                cc[j] = ssn_rand_range(seed, stream, i, 1 + km1 + j, f.p);
+        for (int t = 0; t < SSN_MAXJ; t++)
+            if (t < nids) {
+                alpha[t * o_t + i] = horner_at(a, ca, pw, t, km1, f);
+                comp[t * o_t + i] = horner_at(cm, cc, pw, t, km1, f);
             }
-        for (int t = 0; t < nids; t++) {
-            u64 x = a, y = cm;
-#pragma unroll
-            for (int j = 0; j < SSN_MAXK; j++)
-                if (j < km1) {
-                    x = ssn_addmod(x, ssn_mulmod(ca[j], pw.pw[t][j], f), f.p);
-                    y = ssn_addmod(y, ssn_mulmod(cc[j], pw.pw[t][j], f), f.p);
-                }
-            alpha[t * o_t + i] = x;
-            comp[t * o_t + i] = y;
-        }
     }
 }
 
@@ -419,49 +560,64 @@ extern "C" int ssn_mask_trunc(u64 n, u64 step, u64 emax, u64 seed, u64 stream, i
     return ssn_check_launch();
 }
 
-// Multiplicative mask (S/masks.py:67-90): one thread per window (output element): beta =
-// 1 + U[0, bmax) constant over the kh x kw window, beta^-1 by Fermat, beta shared at every
-// input element of the window (own coefficients per element), beta^-1 shared at the window.
-// Philox: stream s draws: window o: j=0 beta, 1..km1 beta_inv coeffs; stream s+1 input
-// element i: j=0..km1-1 beta coeffs.
-__global__ void k_mask_beta(int c, int h, int wd, int kh, int kw, u64 n_out, u64 bmax, u64 seed, u64 stream,
-                            int km1, PowTable pw, int nids, u64 *__restrict__ beta, u64 b_t,
-                            u64 *__restrict__ binv, u64 bi_t, SsnField f) {
+// Multiplicative mask (S/masks.py:67-90).  Each thread owns WPT windows spaced a grid
+// apart (coalesced); beta = 1 + U[0, bmax) per window, the WPT inverses by Montgomery's
+// batch trick (one Fermat exponentiation per thread instead of per window), beta shared per
+// input element of the window (streams stream+1), beta^-1 shared per window (stream+2).
+#define SSN_WPT 8
+__global__ void __launch_bounds__(256, 1) k_mask_beta(int c, int h, int wd, int kh, int kw, u64 n_out, u64 bmax,
+                                                   u64 seed, u64 stream, int km1, PowTable pw, int nids,
+                                                   u64 *__restrict__ beta, u64 b_t, u64 *__restrict__ binv,
+                                                   u64 bi_t, SsnField f) {
     const int oh = h / kh, ow = wd / kw;
-    for (u64 o = blockIdx.x * (u64)blockDim.x + threadIdx.x; o < n_out; o += (u64)gridDim.x * blockDim.x) {
-        u64 bt = 1 + ssn_rand_range(seed, stream, o, 0, bmax);
-        u64 bi = ssn_powmod(bt, f.p - 2, f);
-        u64 cc[SSN_MAXK];
+    const u64 T = (u64)gridDim.x * blockDim.x;
+    for (u64 o0 = blockIdx.x * (u64)blockDim.x + threadIdx.x; o0 < n_out; o0 += T * SSN_WPT) {
+        u64 bt[SSN_WPT], pre[SSN_WPT];
+        u64 run = 1;
 #pragma unroll
-        for (int j = 0; j < SSN_MAXK; j++)
-            if (j < km1) cc[j] = ssn_rand_range(seed, stream, o, 1 + j, f.p);
-        for (int t = 0; t < nids; t++) {
-            u64 y = bi;
-#pragma unroll
-            for (int j = 0; j < SSN_MAXK; j++)
-                if (j < km1) y = ssn_addmod(y, ssn_mulmod(cc[j], pw.pw[t][j], f), f.p);
-            binv[t * bi_t + o] = y;
+        for (int q = 0; q < SSN_WPT; q++) {
+            const u64 o = o0 + (u64)q * T;
+            bt[q] = o < n_out ? 1 + ssn_rand_range(seed, stream, o, 0, bmax) : 1;
+            run = ssn_mulmod(run, bt[q], f);
+            pre[q] = run;
         }
-        u64 img = o / ((u64)c * oh * ow);
-        u64 rem = o - img * ((u64)c * oh * ow);
-        int ci = (int)(rem / ((u64)oh * ow));
-        int rr = (int)(rem % ((u64)oh * ow));
-        int y0 = rr / ow, x0 = rr % ow;
-        for (int a = 0; a < kh; a++)
-            for (int b = 0; b < kw; b++) {
-                u64 i = ((img * c + ci) * (u64)h + (u64)(y0 * kh + a)) * wd + (u64)(x0 * kw + b);
-                u64 ca[SSN_MAXK];
+        u64 inv = ssn_powmod(run, f.p - 2, f);
 #pragma unroll
-                for (int j = 0; j < SSN_MAXK; j++)
-                    if (j < km1) ca[j] = ssn_rand_range(seed, stream + 1, i, j, f.p);
-                for (int t = 0; t < nids; t++) {
-                    u64 x = bt;
+        for (int q = SSN_WPT - 1; q >= 0; q--) {
+            const u64 bi = q ? ssn_mulmod(inv, pre[q - 1], f) : inv;
+            inv = ssn_mulmod(inv, bt[q], f);
+            pre[q] = bi;                                    // reuse: beta^-1 of window q
+        }
 #pragma unroll
-                    for (int j = 0; j < SSN_MAXK; j++)
-                        if (j < km1) x = ssn_addmod(x, ssn_mulmod(ca[j], pw.pw[t][j], f), f.p);
-                    beta[t * b_t + i] = x;
-                }
+        for (int q = 0; q < SSN_WPT; q++) {
+            const u64 o = o0 + (u64)q * T;
+            if (o >= n_out) continue;
+            u64 cc[SSN_MAXK];
+            load_coeffs(cc, nullptr, n_out, o, km1, seed, stream + 2, f);
+#pragma unroll
+            for (int t = 0; t < SSN_MAXJ; t++)
+                if (t < nids) binv[t * bi_t + o] = horner_at(pre[q], cc, pw, t, km1, f);
+            u64 base_in;
+            if (kh == 1 && kw == 1) {
+                base_in = o;
+            } else {
+                const u64 img = o / ((u64)c * oh * ow);
+                const u64 rem = o - img * ((u64)c * oh * ow);
+                const int ci = (int)(rem / ((u64)oh * ow));
+                const int rr = (int)(rem % ((u64)oh * ow));
+                const int y0 = rr / ow, x0 = rr % ow;
+                base_in = ((img * c + ci) * (u64)h + (u64)(y0 * kh)) * wd + (u64)(x0 * kw);
             }
+            for (int a = 0; a < kh; a++)
+                for (int b = 0; b < kw; b++) {
+                    const u64 i = base_in + (u64)a * wd + b;
+                    u64 ca[SSN_MAXK];
+                    load_coeffs(ca, nullptr, 0, i, km1, seed, stream + 1, f);
+#pragma unroll
+                    for (int t = 0; t < SSN_MAXJ; t++)
+                        if (t < nids) beta[t * b_t + i] = horner_at(bt[q], ca, pw, t, km1, f);
+                }
+        }
     }
 }
 
@@ -471,12 +627,15 @@ extern "C" int ssn_mask_beta(int nb, int c, int h, int wd, int kh, int kw, u64 b
     if (bmax < 1 || kh < 1 || kw < 1 || h % kh || wd % kw || km1 < 0 || km1 > SSN_MAXK || nids < 1 ||
         nids > SSN_MAXJ)
         return SSN_ERR_ARG;
-    u64 n_out = (u64)nb * c * (h / kh) * (wd / kw);
+    const u64 n_out = (u64)nb * c * (h / kh) * (wd / kw);
     if (n_out == 0) return 0;
     PowTable pw = make_pows(ids, nids, km1, p);
-    k_mask_beta<<<ssn_blocks(n_out), 256, 0, (cudaStream_t)strm>>>(c, h, wd, kh, kw, n_out, bmax, seed, stream, km1,
-                                                                   pw, nids, beta, beta_tstride, binv, binv_tstride,
-                                                                   ssn_make_field(p));
+    u64 blocks = (n_out + 256 * SSN_WPT - 1) / (256 * SSN_WPT);
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
+    k_mask_beta<<<(unsigned)blocks, 256, 0, (cudaStream_t)strm>>>(c, h, wd, kh, kw, n_out, bmax, seed, stream, km1,
+                                                                  pw, nids, beta, beta_tstride, binv, binv_tstride,
+                                                                  ssn_make_field(p));
     return ssn_check_launch();
 }
 
@@ -485,13 +644,13 @@ __global__ void k_pool_expand(const u64 *__restrict__ blk, u64 *__restrict__ out
                               int kw, u64 n) {
     const int oh = h / kh, ow = wd / kw;
     for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
-        u64 x = i % wd, y = (i / wd) % h, rest = i / ((u64)wd * h);   // rest = img*c + ci
+        const u64 x = i % wd, y = (i / wd) % h, rest = i / ((u64)wd * h);   // rest = img*c + ci
         out[i] = blk[(rest * oh + y / kh) * ow + x / kw];
     }
 }
 extern "C" int ssn_pool_expand(const u64 *blk, u64 *out, int nb, int c, int h, int wd, int kh, int kw, void *strm) {
     if (kh < 1 || kw < 1 || h % kh || wd % kw) return SSN_ERR_ARG;
-    u64 n = (u64)nb * c * h * wd;
+    const u64 n = (u64)nb * c * h * wd;
     if (n == 0) return 0;
     k_pool_expand<<<ssn_blocks(n), 256, 0, (cudaStream_t)strm>>>(blk, out, c, h, wd, kh, kw, n);
     return ssn_check_launch();

@@ -1,9 +1,11 @@
 // ssn_field.cuh -- prime-field arithmetic and counter-based randomness on sm_100a.
 //
 // Field elements are canonical uint64 in [0, p), p < 2^62 (the reference caps p at 57
-// bits, S/field.py:64-75).  mulmod is an exact Barrett reduction of the 128-bit product
-// (any p), so the same kernels serve the default p = 2^45 - 55 (S/field.py:21) and the
-// F_11 worked examples of the reference tests.
+// bits, S/field.py:64-75).  Two exact reductions of the 128-bit product:
+//   * pseudo-Mersenne fold for p = 2^s - c with small c and s <= 50 (the default
+//     p = 2^45 - 55, S/field.py:21): x = q*2^s + r == q*c + r, folded twice;
+//   * Barrett for any other p (e.g. the F_11 worked examples of the reference tests).
+// The choice is a warp-uniform branch on SsnField::pm.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -14,16 +16,14 @@ typedef uint32_t u32;
 
 struct SsnField {
     u64 p;      // modulus
-    u64 mu;     // floor(2^(2s) / p)
-    int s;      // bit length of p
+    u64 mu;     // floor(2^(2s) / p)            (Barrett)
+    u64 c;      // 2^s - p                        (pseudo-Mersenne)
+    u64 mask;   // 2^s - 1
     u64 half;   // (p-1)/2, signed decode threshold (S/field.py:74)
+    int s;      // bit length of p
+    int pm;     // 1: use the pseudo-Mersenne fold
+    int near;   // 1: 2^s - p < 2^(s-24): uniform draws by masking (stat. distance < 2^-24)
 };
-
-#ifdef __CUDACC__
-#define SSN_HD __host__ __device__ __forceinline__
-#else
-#define SSN_HD inline
-#endif
 
 static inline SsnField ssn_make_field(u64 p) {
     SsnField f;
@@ -33,7 +33,11 @@ static inline SsnField ssn_make_field(u64 p) {
     f.s = s;
     unsigned __int128 num = ((unsigned __int128)1) << (2 * s);
     f.mu = (u64)(num / p);
+    f.mask = (s >= 64) ? ~0ull : ((1ull << s) - 1);
+    f.c = f.mask + 1 - p;
     f.half = (p - 1) / 2;
+    f.pm = (s >= 24 && s <= 50 && f.c < (1ull << 12)) ? 1 : 0;
+    f.near = (s >= 32 && f.c < (1ull << (s - 24))) ? 1 : 0;
     return f;
 }
 
@@ -58,8 +62,21 @@ __device__ __forceinline__ u64 ssn_barrett(u64 hi, u64 lo, const SsnField &f) {
     return r;
 }
 
+// Pseudo-Mersenne fold of x = hi*2^64 + lo < 2^(2s), s <= 50, c < 2^12.
+__device__ __forceinline__ u64 ssn_pmfold(u64 hi, u64 lo, const SsnField &f) {
+    const int s = f.s;
+    u64 q = (hi << (64 - s)) | (lo >> s);                  // < 2^s
+    u64 t = q * f.c + (lo & f.mask);                       // < 2^(s+12) + 2^s
+    t = (t >> s) * f.c + (t & f.mask);                     // < 2^s + 2^25
+    return t >= f.p ? t - f.p : t;
+}
+
+__device__ __forceinline__ u64 ssn_reduce_wide(u64 hi, u64 lo, const SsnField &f) {
+    return f.pm ? ssn_pmfold(hi, lo, f) : ssn_barrett(hi, lo, f);
+}
+
 __device__ __forceinline__ u64 ssn_mulmod(u64 a, u64 b, const SsnField &f) {
-    return ssn_barrett(__umul64hi(a, b), a * b, f);
+    return ssn_reduce_wide(__umul64hi(a, b), a * b, f);
 }
 
 // 128-bit accumulator helpers
@@ -69,13 +86,13 @@ __device__ __forceinline__ void ssn_mac(u128s &acc, u64 a, u64 b) {
     acc.lo += lo;
     acc.hi += hi + (acc.lo < lo);
 }
-// reduce any 64-bit value mod p (Barrett is exact for x < 2^(2s), i.e. all x when s >= 32)
+// reduce any 64-bit value mod p (exact for all x when s >= 32)
 __device__ __forceinline__ u64 ssn_reduce64(u64 x, const SsnField &f) {
-    return f.s >= 32 ? ssn_barrett(0, x, f) : x % f.p;
+    return f.s >= 32 ? ssn_reduce_wide(0, x, f) : x % f.p;
 }
-// reduce an arbitrary 128-bit value mod p: x = hi*2^64 + lo == (hi mod p)*r64 + lo (mod p),
-// r64 = 2^64 mod p.
+// reduce an arbitrary 128-bit value mod p: hi*2^64 + lo == (hi mod p)*r64 + lo (mod p).
 __device__ __forceinline__ u64 ssn_reduce128(u128s x, const SsnField &f, u64 r64) {
+    if (f.s >= 32 && x.hi < (1ull << (2 * f.s - 64))) return ssn_reduce_wide(x.hi, x.lo, f);
     u64 t = ssn_mulmod(ssn_reduce64(x.hi, f), r64, f);
     return ssn_addmod(t, ssn_reduce64(x.lo, f), f.p);
 }
@@ -104,6 +121,11 @@ __device__ __forceinline__ ssn_u4 ssn_philox(u32 c0, u32 c1, u32 c2, u32 c3, u32
     return ssn_u4{c0, c1, c2, c3};
 }
 
+__device__ __forceinline__ ssn_u4 ssn_philox_at(u64 seed, u64 stream, u64 i, u32 j) {
+    return ssn_philox((u32)i, (u32)(i >> 32) ^ (j << 20), (u32)stream, (u32)(stream >> 32), (u32)seed,
+                      (u32)(seed >> 32));
+}
+
 // floor(r96 * range / 2^96) for r96 = (r64 << 32) | r32: uniform in [0, range),
 // statistical distance from uniform < range / 2^96.
 __device__ __forceinline__ u64 ssn_bounded(u64 r64, u32 r32, u64 range) {
@@ -115,10 +137,26 @@ __device__ __forceinline__ u64 ssn_bounded(u64 r64, u32 r32, u64 range) {
     return hi1 + ((a1 + uhi + carry1) >> 32);
 }
 
-// Draw number `j` for element `i` of stream `stream` under key `seed`.
+// Draw number `j` for element `i` of stream `stream`: uniform in [0, range) (one Philox call).
 __device__ __forceinline__ u64 ssn_rand_range(u64 seed, u64 stream, u64 i, u32 j, u64 range) {
-    ssn_u4 r = ssn_philox((u32)i, (u32)(i >> 32) ^ (j << 20), (u32)stream, (u32)(stream >> 32),
-                          (u32)seed, (u32)(seed >> 32));
+    ssn_u4 r = ssn_philox_at(seed, stream, i, j);
     return ssn_bounded(((u64)r.x << 32) | r.y, r.z, range);
+}
+
+// Two uniform field elements (coefficients 2*jp and 2*jp+1) from one Philox call when p is
+// within 2^-24 of a power of two (masked 64-bit words; the default prime is 2^-39 close);
+// otherwise the bounded 96-bit method, one call each.
+__device__ __forceinline__ void ssn_rand_field2(u64 seed, u64 stream, u64 i, u32 jp, const SsnField &f, u64 &x0,
+                                                u64 &x1) {
+    if (f.near) {
+        ssn_u4 r = ssn_philox_at(seed, stream, i, 0x800u | jp);
+        x0 = (((u64)r.x << 32) | r.y) & f.mask;
+        x1 = (((u64)r.z << 32) | r.w) & f.mask;
+        if (x0 >= f.p) x0 -= f.p;
+        if (x1 >= f.p) x1 -= f.p;
+    } else {
+        x0 = ssn_rand_range(seed, stream, i, 2 * jp, f.p);
+        x1 = ssn_rand_range(seed, stream, i, 2 * jp + 1, f.p);
+    }
 }
 #endif

@@ -96,6 +96,20 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// (hi*2^64 + lo) mod p for p >= 2^40 (L >= 6): hi < 2^40 <= p, so hi*r64 is one mulmod.
+// Not inlined: keeps the epilogue's SASS small enough to stay in the instruction cache.
+__device__ __noinline__ u64 epi_reduce(u64 lo, u64 hi, SsnField f, u64 r64) {
+    const u64 t = ssn_mulmod(hi, r64, f);
+    return ssn_addmod(t, ssn_reduce_wide(0, lo, f), f.p);
+}
+
 template <int L>
 __global__ void __launch_bounds__(128, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, u64 *__restrict__ out,
@@ -151,9 +165,9 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t sa = smem_u32(base + s * STAGE_BYTES);
             const uint32_t sb = sa + A_BYTES;
-#pragma unroll
+#pragma unroll 1
             for (int kk = 0; kk < BK / UK; kk++) {
-#pragma unroll
+#pragma unroll 1
                 for (int i = 0; i < L; i++) {
                     const uint64_t adesc = umma_desc_sw64(sa + i * BM * BK + kk * UK);
 #pragma unroll
@@ -179,28 +193,39 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     const u64 pix = row_ok ? (u64)row - img * ohw : 0;
     u64 *obase = out + (u64)party * out_pstride + img * (u64)O * ohw + pix;
     const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+    // Kept as rolled loops: a fully unrolled epilogue is ~80 KB of SASS that each CTA runs
+    // once, which made the kernel instruction-fetch bound (ncu: stalled_no_instruction).
+    // sum_d D_d * w_d with w = wh*2^32 + wl:  S0 = sum D*wl (128-bit via carry count),
+    // S1 = sum D*wh (< 2^61), total = S0 + S1*2^32.
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 8) {
+        u64 s0[8], s1[8];
+        uint32_t cy[8];
 #pragma unroll
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-        u64 lo[16], hi[16];
-#pragma unroll
-        for (int c = 0; c < 16; c++) lo[c] = hi[c] = 0;
-#pragma unroll
+        for (int c = 0; c < 8; c++) {
+            s0[c] = s1[c] = 0;
+            cy[c] = 0;
+        }
+#pragma unroll 1
         for (int d = 0; d < ND; d++) {
-            uint32_t r[16];
-            tmem_ld16(lane_addr + (uint32_t)(d * BN + c0), r);
-            const u64 w = cd.c[d];
+            uint32_t r[8];
+            tmem_ld8(lane_addr + (uint32_t)(d * BN + c0), r);
+            const uint32_t wl = (uint32_t)cd.c[d], wh = (uint32_t)(cd.c[d] >> 32);
 #pragma unroll
-            for (int c = 0; c < 16; c++) {
-                const u64 plo = (u64)r[c] * w, phi = __umul64hi((u64)r[c], w);
-                lo[c] += plo;
-                hi[c] += phi + (lo[c] < plo);
+            for (int c = 0; c < 8; c++) {
+                const u64 t0 = (u64)r[c] * wl;
+                s0[c] += t0;
+                cy[c] += (s0[c] < t0);
+                s1[c] += (u64)r[c] * wh;
             }
         }
         if (row_ok) {
 #pragma unroll
-            for (int c = 0; c < 16; c++) {
+            for (int c = 0; c < 8; c++) {
                 const int col = n0 + c0 + c;
-                if (col < O) obase[(u64)col * ohw] = ssn_reduce128(u128s{lo[c], hi[c]}, f, r64);
+                const u64 lo = s0[c] + (s1[c] << 32);
+                const u64 hi = (u64)cy[c] + (s1[c] >> 32) + (lo < s0[c]);
+                if (col < O) obase[(u64)col * ohw] = epi_reduce(lo, hi, f, r64);
             }
         }
     }
