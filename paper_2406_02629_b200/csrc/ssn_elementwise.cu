@@ -29,6 +29,16 @@ static int ssn_blocks(u64 n, int threads = 256) {
     return (int)b;
 }
 
+// 2-D grid: y = batch (party / front rank), x = grid-stride over the n elements of one batch
+static dim3 ssn_grid2(u64 n, int nb) {
+    u64 x = (n + 255) / 256;
+    u64 cap = (148ull * 16) / (u64)nb;
+    if (cap < 1) cap = 1;
+    if (x > cap) x = cap;
+    if (x < 1) x = 1;
+    return dim3((unsigned)x, (unsigned)nb);
+}
+
 static inline int ssn_check_launch() {
     cudaError_t e = cudaGetLastError();
     return e == cudaSuccess ? 0 : SSN_ERR_CUDA;
@@ -203,11 +213,18 @@ __device__ __forceinline__ u64 horner_at(u64 s, const u64 (&c)[SSN_MAXK], const 
 }
 
 // ------------------------------------------------------------------ ewise
-__global__ void k_ewise(int op, const u64 *__restrict__ a, const u64 *__restrict__ b, u64 *__restrict__ out,
-                        u64 n, u64 b_div, u64 b_mod, u64 b_div2, u64 b_mul2, SsnField f) {
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+__global__ void k_ewise(int op, int mode, const u64 *__restrict__ a, const u64 *__restrict__ b,
+                        u64 *__restrict__ out, u64 n, u64 b_div, u64 b_mod, u64 b_div2, u64 b_mul2, SsnField f) {
+    const u64 row0 = mode == 2 ? (u64)blockIdx.y * b_mod : 0;     // cyclic mode: one row per grid.y
+    const u64 lim = mode == 2 ? row0 + b_mod : n;
+    for (u64 i = row0 + blockIdx.x * (u64)blockDim.x + threadIdx.x; i < lim; i += (u64)gridDim.x * blockDim.x) {
         u64 x = a[i];
-        u64 y = op == 3 ? 0 : b[(b_div == 1 ? i : i / b_div) % b_mod + (i / b_div2) * b_mul2];
+        u64 y;
+        if (mode == 0) y = b[i];                                   // full
+        else if (mode == 1) y = b[0];                              // scalar
+        else if (mode == 2) y = b[i - row0];                       // cyclic: row blockIdx.y
+        else if (mode == 3) y = 0;                                 // neg
+        else y = b[(i / b_div) % b_mod + (i / b_div2) * b_mul2];   // general strided broadcast
         u64 r;
         if (op == 0) r = ssn_addmod(x, y, f.p);
         else if (op == 1) r = ssn_submod(x, y, f.p);
@@ -221,8 +238,14 @@ extern "C" int ssn_ewise(int op, const u64 *a, const u64 *b, u64 *out, u64 n, u6
                          u64 b_div2, u64 b_mul2, u64 p, void *stream) {
     if (op < 0 || op > 3 || b_div == 0 || b_mod == 0 || b_div2 == 0) return SSN_ERR_ARG;
     if (n == 0) return 0;
-    k_ewise<<<ssn_blocks(n), 256, 0, (cudaStream_t)stream>>>(op, a, b, out, n, b_div, b_mod, b_div2, b_mul2,
-                                                            ssn_make_field(p));
+    int mode = 4;
+    if (op == 3) mode = 3;
+    else if (b_mul2 == 0 && b_div == 1 && b_mod >= n) mode = 0;
+    else if (b_mul2 == 0 && b_mod == 1) mode = 1;
+    else if (b_mul2 == 0 && b_div == 1 && n % b_mod == 0 && n / b_mod <= 65535) mode = 2;
+    dim3 grid = mode == 2 ? ssn_grid2(b_mod, (int)(n / b_mod)) : dim3(ssn_blocks(n));
+    k_ewise<<<grid, 256, 0, (cudaStream_t)stream>>>(op, mode, a, b, out, n, b_div, b_mod, b_div2, b_mul2,
+                                                    ssn_make_field(p));
     return ssn_check_launch();
 }
 
@@ -231,9 +254,8 @@ extern "C" int ssn_ewise(int op, const u64 *a, const u64 *b, u64 *out, u64 n, u6
 __global__ void k_gen(const u64 *__restrict__ secret, u64 s_b, const u64 *__restrict__ coeffs, u64 c_b, u64 seed,
                       u64 stream, int km1, PowTable pw, int nids, u64 *__restrict__ out, u64 o_b, u64 o_t, u64 n,
                       int nb, SsnField f) {
-    const u64 total = n * (u64)nb;
-    for (u64 g = blockIdx.x * (u64)blockDim.x + threadIdx.x; g < total; g += (u64)gridDim.x * blockDim.x) {
-        const u64 b = nb == 1 ? 0 : g / n, i = g - b * n;
+    const u64 b = blockIdx.y;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
         const u64 s = secret ? secret[b * s_b + i] : 0;
         u64 c[SSN_MAXK];
         load_coeffs(c, coeffs ? coeffs + b * c_b : nullptr, n, i, km1, seed, stream + b, f);
@@ -249,7 +271,7 @@ extern "C" int ssn_gen(const u64 *secret, u64 secret_bstride, const u64 *coeffs,
     if (km1 < 0 || km1 > SSN_MAXK || nids < 1 || nids > SSN_MAXJ || nbatch < 1) return SSN_ERR_ARG;
     if (n == 0) return 0;
     PowTable pw = make_pows(ids, nids, km1, p);
-    k_gen<<<ssn_blocks(n * nbatch), 256, 0, (cudaStream_t)strm>>>(secret, secret_bstride, coeffs, coeff_bstride,
+    k_gen<<<ssn_grid2(n, nbatch), 256, 0, (cudaStream_t)strm>>>(secret, secret_bstride, coeffs, coeff_bstride,
                                                                   seed, stream, km1, pw, nids, out, out_bstride,
                                                                   out_tstride, n, nbatch, ssn_make_field(p));
     return ssn_check_launch();
@@ -258,9 +280,8 @@ extern "C" int ssn_gen(const u64 *secret, u64 secret_bstride, const u64 *coeffs,
 // ------------------------------------------------------------------ rec
 __global__ void k_rec(const u64 *__restrict__ pts, u64 p_b, u64 p_j, Weights w, int m, u64 *__restrict__ out,
                       u64 o_b, u64 n, int nb, SsnField f) {
-    const u64 total = n * (u64)nb;
-    for (u64 g = blockIdx.x * (u64)blockDim.x + threadIdx.x; g < total; g += (u64)gridDim.x * blockDim.x) {
-        const u64 b = nb == 1 ? 0 : g / n, i = g - b * n;
+    const u64 b = blockIdx.y;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
         const u64 *base = pts + b * p_b + i;
         u64 x[SSN_MAXJ];
 #pragma unroll
@@ -275,7 +296,7 @@ extern "C" int ssn_rec(const u64 *pts, u64 pts_bstride, u64 pts_jstride, const u
     if (m < 1 || m > SSN_MAXJ || nbatch < 1) return SSN_ERR_ARG;
     if (n == 0) return 0;
     Weights W = make_weights(w, m, p);
-    k_rec<<<ssn_blocks(n * nbatch), 256, 0, (cudaStream_t)strm>>>(pts, pts_bstride, pts_jstride, W, m, out,
+    k_rec<<<ssn_grid2(n, nbatch), 256, 0, (cudaStream_t)strm>>>(pts, pts_bstride, pts_jstride, W, m, out,
                                                                   out_bstride, n, nbatch, ssn_make_field(p));
     return ssn_check_launch();
 }
@@ -284,9 +305,8 @@ extern "C" int ssn_rec(const u64 *pts, u64 pts_bstride, u64 pts_jstride, const u
 // out[b][t][i] = sum_j Rt[t][j] * pts[b][j][i]  -- b = front rank, j = sub-share source, t = out rank
 __global__ void k_reduce_apply(const u64 *__restrict__ pts, u64 p_b, u64 p_j, RTable R, int m, int nout,
                                u64 *__restrict__ out, u64 o_b, u64 o_t, u64 n, int nb, SsnField f) {
-    const u64 total = n * (u64)nb;
-    for (u64 g = blockIdx.x * (u64)blockDim.x + threadIdx.x; g < total; g += (u64)gridDim.x * blockDim.x) {
-        const u64 b = nb == 1 ? 0 : g / n, i = g - b * n;
+    const u64 b = blockIdx.y;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
         const u64 *base = pts + b * p_b + i;
         u64 v[SSN_MAXP];
 #pragma unroll
@@ -311,7 +331,7 @@ extern "C" int ssn_reduce_apply(const u64 *pts, u64 pts_bstride, u64 pts_jstride
         int ok = make_row(R.r[t], row, m, p);
         if (t < nout) R.small = R.small && ok;
     }
-    k_reduce_apply<<<ssn_blocks(n * nbatch), 256, 0, (cudaStream_t)strm>>>(pts, pts_bstride, pts_jstride, R, m, nout,
+    k_reduce_apply<<<ssn_grid2(n, nbatch), 256, 0, (cudaStream_t)strm>>>(pts, pts_bstride, pts_jstride, R, m, nout,
                                                                            out, out_bstride, out_tstride, n, nbatch,
                                                                            ssn_make_field(p));
     return ssn_check_launch();
@@ -322,9 +342,8 @@ __global__ void k_reshare_finish(const u64 *__restrict__ pts, u64 p_b, u64 p_j, 
                                  const u64 *__restrict__ zero, u64 z_b, const u64 *__restrict__ bias, u64 bi_b,
                                  u64 bias_div, u64 bias_mod, const u64 *__restrict__ alpha, u64 a_b,
                                  u64 *__restrict__ out, u64 o_b, u64 n, int nb, SsnField f) {
-    const u64 total = n * (u64)nb;
-    for (u64 g = blockIdx.x * (u64)blockDim.x + threadIdx.x; g < total; g += (u64)gridDim.x * blockDim.x) {
-        const u64 b = nb == 1 ? 0 : g / n, i = g - b * n;
+    const u64 b = blockIdx.y;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
         const u64 *base = pts + b * p_b + i;
         u64 x[SSN_MAXP];
 #pragma unroll
@@ -332,7 +351,11 @@ __global__ void k_reshare_finish(const u64 *__restrict__ pts, u64 p_b, u64 p_j, 
             if (j < k) x[j] = base[j * p_j];
         u64 acc = lincomb<SSN_MAXP>(x, w.r, w.small, k, f);
         if (zero) acc = ssn_addmod(acc, zero[b * z_b + i], f.p);
-        if (bias) acc = ssn_addmod(acc, bias[b * bi_b + (i / bias_div) % bias_mod], f.p);
+        if (bias) {
+            const u64 ch = n < (1ull << 32) ? (u64)(((uint32_t)i / (uint32_t)bias_div) % (uint32_t)bias_mod)
+                                            : (i / bias_div) % bias_mod;
+            acc = ssn_addmod(acc, bias[b * bi_b + ch], f.p);
+        }
         if (alpha) acc = ssn_addmod(acc, alpha[b * a_b + i], f.p);
         out[b * o_b + i] = acc;
     }
@@ -345,7 +368,7 @@ extern "C" int ssn_reshare_finish(const u64 *pts, u64 pts_bstride, u64 pts_jstri
     if (k < 1 || k > SSN_MAXP || nbatch < 1 || bias_div == 0 || bias_mod == 0) return SSN_ERR_ARG;
     if (n == 0) return 0;
     Weights W = make_weights(w, k, p);
-    k_reshare_finish<<<ssn_blocks(n * nbatch), 256, 0, (cudaStream_t)strm>>>(
+    k_reshare_finish<<<ssn_grid2(n, nbatch), 256, 0, (cudaStream_t)strm>>>(
         pts, pts_bstride, pts_jstride, W, k, zero, zero_bstride, bias, bias_bstride, bias_div, bias_mod, alpha,
         alpha_bstride, out, out_bstride, n, nbatch, ssn_make_field(p));
     return ssn_check_launch();
@@ -382,7 +405,13 @@ __global__ void k_trunc_elite(const u64 *__restrict__ pts, u64 p_j, int npts, in
             const i64 qd = (2 * a + d) / (2 * d);
             t = t < 0 ? -qd : qd;
         }
-        const u64 tm = t >= 0 ? ssn_reduce64((u64)t, f) : (f.p - ssn_reduce64((u64)(-t), f)) % f.p;
+        u64 tm;
+        if (t >= 0) {
+            tm = ssn_reduce64((u64)t, f);
+        } else {
+            const u64 mneg = ssn_reduce64((u64)(-t), f);
+            tm = mneg ? f.p - mneg : 0;
+        }
         if (nids == 0) {
             out[i] = tm;
             continue;
@@ -440,12 +469,11 @@ __global__ void k_nonlin_elite(const u64 *__restrict__ pts, u64 p_j, int m, Weig
         if (pool_kind == 0) {
             base_in = o;
         } else {
-            const u64 img = o / ((u64)c * oh * ow);
-            const u64 rem = o - img * ((u64)c * oh * ow);
-            const int ci = (int)(rem / ((u64)oh * ow));
-            const int rr = (int)(rem % ((u64)oh * ow));
-            const int y = rr / ow, x = rr % ow;
-            base_in = ((img * c + ci) * (u64)h + (u64)(y * kh)) * wd + (u64)(x * kw);
+            const uint32_t o32 = (uint32_t)o, chw = (uint32_t)(c * oh * ow), hw = (uint32_t)(oh * ow);
+            const uint32_t img = o32 / chw, rem = o32 - img * chw;
+            const uint32_t ci = rem / hw, rr = rem - ci * hw;
+            const uint32_t y = rr / (uint32_t)ow, x = rr - y * (uint32_t)ow;
+            base_in = (((u64)img * c + ci) * (u64)h + (u64)(y * kh)) * wd + (u64)(x * kw);
         }
         i64 acc = pool_kind == 1 ? INT64_MIN : 0;
         for (int a = 0; a < kh; a++)
@@ -473,6 +501,7 @@ extern "C" int ssn_nonlin_elite(const u64 *pts, u64 pts_jstride, int m, const u6
     Weights W = make_weights(w, m, p);
     const u64 n_out = (u64)nb * c * (h / kh) * (wd / kw);
     if (n_out == 0) return 0;
+    if (n_out >= (1ull << 32)) return SSN_ERR_UNSUPPORTED;
     k_nonlin_elite<<<ssn_blocks(n_out), 256, 0, (cudaStream_t)strm>>>(pts, pts_jstride, m, W, relu, pool_kind, c, h,
                                                                       wd, kh, kw, plain, n_out, ssn_make_field(p));
     return ssn_check_launch();
@@ -601,12 +630,11 @@ __global__ void __launch_bounds__(256, 1) k_mask_beta(int c, int h, int wd, int 
             if (kh == 1 && kw == 1) {
                 base_in = o;
             } else {
-                const u64 img = o / ((u64)c * oh * ow);
-                const u64 rem = o - img * ((u64)c * oh * ow);
-                const int ci = (int)(rem / ((u64)oh * ow));
-                const int rr = (int)(rem % ((u64)oh * ow));
-                const int y0 = rr / ow, x0 = rr % ow;
-                base_in = ((img * c + ci) * (u64)h + (u64)(y0 * kh)) * wd + (u64)(x0 * kw);
+                const uint32_t o32 = (uint32_t)o, chw = (uint32_t)(c * oh * ow), hw = (uint32_t)(oh * ow);
+                const uint32_t img = o32 / chw, rem = o32 - img * chw;
+                const uint32_t ci = rem / hw, rr = rem - ci * hw;
+                const uint32_t y0 = rr / (uint32_t)ow, x0 = rr - y0 * (uint32_t)ow;
+                base_in = (((u64)img * c + ci) * (u64)h + (u64)(y0 * kh)) * wd + (u64)(x0 * kw);
             }
             for (int a = 0; a < kh; a++)
                 for (int b = 0; b < kw; b++) {
@@ -629,6 +657,7 @@ extern "C" int ssn_mask_beta(int nb, int c, int h, int wd, int kh, int kw, u64 b
         return SSN_ERR_ARG;
     const u64 n_out = (u64)nb * c * (h / kh) * (wd / kw);
     if (n_out == 0) return 0;
+    if (n_out >= (1ull << 32)) return SSN_ERR_UNSUPPORTED;
     PowTable pw = make_pows(ids, nids, km1, p);
     u64 blocks = (n_out + 256 * SSN_WPT - 1) / (256 * SSN_WPT);
     if (blocks > 148 * 8) blocks = 148 * 8;
