@@ -145,6 +145,52 @@ int ssn_im2col_limbs(const uint64_t *x, int nparty, int nimg, int C, int H, int 
 int ssn_gemm_tc(const uint8_t *a_planes, const uint8_t *b_planes, int nparty, int L, int M, int O, uint64_t Kpad,
                 uint64_t ohw, uint64_t *out, uint64_t out_pstride, uint64_t p, void *stream);
 
+/* Fused per-layer protocol chain for co-resident parties (one launch per secure layer after
+ * its share GEMM).  Per element i of the linear op's output, for all n parties at once:
+ *   reshare_degree_reduce (S/protocol.py:131-199): participant j (j < m = 2k-1) sub-shares
+ *     acc[j][i] to the k front ranks (RESHARE_OUT), front ranks apply R^T (RESHARE_BACK),
+ *     out rank t (t < nout) reconstructs;  + zero share (rerand, S/protocol.py:260-265)
+ *     + bias share (S/layers.py:260-267);
+ *   sss_truncation (S/layers.py:277-323): + alpha share, elite rec over the k front ranks,
+ *     [verify: Reed-Solomon check of the n-k extra masked shares -> *fail], window decode,
+ *     floor(/r), round_half_away(/d), fresh (k,n) shares (SHARE_DIST), + comp share;
+ *   [other != NULL] share_add of a residual input (S/sss.py:238);
+ *   [nonlin] sss_nonlinear (S/layers.py:326-380): * beta shares (window-constant beta),
+ *     elite rec over m, decode, ReLU, max/sum over kh x kw windows, encode (NONLIN_PLAIN),
+ *     * beta^-1 shares at ranks t < fan.
+ * Masks are the trusted source's (S/masks.py:39-96), drawn from Philox lane (src_seed,
+ * src_stream + 0..6); protocol randomness from (party_seed, party_stream + 0..m).
+ * Layouts: acc [m][nel] at acc_pstride; bias [n][O] at bias_pstride with channel
+ * (i / bias_div) % bias_mod; other [n][nel]; out [n][nel or n_out] at out_pstride.
+ * Host arrays: ids[n] (party ids), rt[n*m] (R^T rows for all n ranks), ext[(n-k)*k]
+ * (Lagrange extrapolation from the front ids to ids[k..n)).  Supported (k, n): (2,3),
+ * (3,5), (4,7). */
+typedef struct ssn_chain_desc {
+    const uint64_t *acc;
+    uint64_t acc_pstride;
+    const uint64_t *bias;
+    uint64_t bias_pstride, bias_div, bias_mod;
+    const uint64_t *other;
+    uint64_t other_pstride;
+    uint64_t *out;
+    uint64_t out_pstride;
+    uint64_t nel;
+    int nout;
+    int64_t value_bound, r, d;
+    uint64_t emax;
+    int verify;
+    unsigned long long *fail;
+    int nonlin, relu, pool_kind, nb, c, h, w, kh, kw, fan;
+    uint64_t bmax;
+    uint64_t party_seed, party_stream, src_seed, src_stream;
+    int k, n;
+    const uint64_t *ids, *rt, *ext;
+    uint64_t p;
+    int fault_rank;   /* test hook: < 0 off; else rank's reshared share of element 0 is corrupted */
+} ssn_chain_desc;
+
+int ssn_layer_chain(const ssn_chain_desc *desc, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

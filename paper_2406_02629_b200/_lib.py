@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "libssn_b200.so")
 CSRC = os.path.join(HERE, "csrc")
-SOURCES = ["ssn_elementwise.cu", "ssn_gemm_simt.cu", "ssn_gemm_tc.cu"]
+SOURCES = ["ssn_elementwise.cu", "ssn_gemm_simt.cu", "ssn_gemm_tc.cu", "ssn_chain.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared"]
 
@@ -72,7 +72,32 @@ _SIGS = {
     "ssn_limb_split": [_P, _U64, _U64, _U64, _I32, _P, _U64, _I32, _P],
     "ssn_im2col_limbs": [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _U64, _U64, _P],
     "ssn_gemm_tc": [_P, _P, _I32, _I32, _I32, _I32, _U64, _U64, _P, _U64, _U64, _P],
+    "ssn_layer_chain": [_P, _P],
 }
+
+
+class ChainDesc(ctypes.Structure):
+    """struct ssn_chain_desc (include/ssn.h)."""
+    _fields_ = [
+        ("acc", _P), ("acc_pstride", _U64),
+        ("bias", _P), ("bias_pstride", _U64), ("bias_div", _U64), ("bias_mod", _U64),
+        ("other", _P), ("other_pstride", _U64),
+        ("out", _P), ("out_pstride", _U64),
+        ("nel", _U64),
+        ("nout", _I32),
+        ("value_bound", _I64), ("r", _I64), ("d", _I64),
+        ("emax", _U64),
+        ("verify", _I32),
+        ("fail", _P),
+        ("nonlin", _I32), ("relu", _I32), ("pool_kind", _I32), ("nb", _I32), ("c", _I32), ("h", _I32),
+        ("w", _I32), ("kh", _I32), ("kw", _I32), ("fan", _I32),
+        ("bmax", _U64),
+        ("party_seed", _U64), ("party_stream", _U64), ("src_seed", _U64), ("src_stream", _U64),
+        ("k", _I32), ("n", _I32),
+        ("ids", _P), ("rt", _P), ("ext", _P),
+        ("p", _U64),
+        ("fault_rank", _I32),
+    ]
 
 _lib = None
 

@@ -23,6 +23,7 @@ Randomness is device Philox (rng_mode="device"); decoded outputs are RNG-indepen
 they equal the reference / plaintext exactly (tests/test_gpu_batched.py).
 """
 
+import ctypes
 import time
 
 import numpy as np
@@ -46,7 +47,7 @@ def _count(shape):
 
 class BatchedEngine:
     def __init__(self, model, scheme, batch, seed=7, rng_mode="device", verify=False, ordering="ltn",
-                 profile=False):
+                 profile=False, fuse=True):
         if rng_mode != "device":
             raise ValueError("the batched engine draws its randomness on the device (rng_mode='device'); "
                              "use simulate_inference for reference-stream parity runs")
@@ -75,6 +76,11 @@ class BatchedEngine:
         self._deal_weights()
         self.kernel_launches = 0
         self.fault = None
+        self.fuse = fuse
+        self.chains = self._plan_chains() if fuse else {}
+        self._chain_member = {i: start for start, ch in self.chains.items() for i in ch[1:]}
+        self._rt_all = _lib.u64_array([R[i][t] for t in range(n) for i in range(self.m)])
+        self._ext_host = _lib.u64_array(self.ext) if self.ext else None
 
     # ------------------------------------------------------------------ setup
     def _deal_weights(self):
@@ -98,6 +104,93 @@ class BatchedEngine:
         _lib.call("ssn_encode_signed", _lib.ptr(v), _lib.ptr(out), v.numel(), _lib.ptr(ovf), self.p,
                   _lib.stream_ptr())
         return out
+
+    # ------------------------------------------------------------------ fused chains
+    CHAIN_SCHEMES = ((2, 3), (3, 5), (4, 7))
+
+    def _srcs(self, idx):
+        op = self.ops[idx]
+        s = [idx - 1 if op.src is None else op.src]
+        if op.kind == "add":
+            s.append(op.src2)
+        return s
+
+    def _plan_chains(self):
+        """Group linear -> truncation [-> add] [-> nonlinear] runs whose intermediates have a
+        single consumer into one fused protocol launch (csrc/ssn_chain.cu)."""
+        if (self.k, self.n) not in self.CHAIN_SCHEMES:
+            return {}
+        ops, cons = self.ops, self.cons
+        chains = {}
+        for idx, op in enumerate(ops):
+            c = cons.get(idx, [])
+            if op.kind != "linear" or len(c) != 1 or ops[c[0]].kind != "truncation":
+                continue
+            chain = [idx, c[0]]
+            cur = c[0]
+            nxt = cons.get(cur, [])
+            if len(nxt) == 1 and ops[nxt[0]].kind == "add":
+                a = nxt[0]
+                others = [s for s in self._srcs(a) if s != cur]
+                if len(others) == 1 and others[0] < idx:
+                    chain.append(a)
+                    cur = a
+                    nxt = cons.get(cur, [])
+            if len(nxt) == 1 and ops[nxt[0]].kind == "nonlinear" and self._srcs(nxt[0]) == [cur]:
+                chain.append(nxt[0])
+            chains[idx] = chain
+        return chains
+
+    def _chain(self, chain, vals, src_rng, party_rng):
+        """One fused launch: reshare + rerand + bias + truncation [+ add] [+ nonlinear]."""
+        B, n, k, m, p = self.batch, self.n, self.k, self.m, self.p
+        lin = self.ops[chain[0]]
+        acc = self._gemm(chain[0], lin, vals[self._srcs(chain[0])[0]])
+        tr = self.ops[chain[1]]
+        add = next((self.ops[i] for i in chain[2:] if self.ops[i].kind == "add"), None)
+        nl = next((self.ops[i] for i in chain[2:] if self.ops[i].kind == "nonlinear"), None)
+        last = self.ops[chain[-1]]
+        O = lin.out_shape[0]
+        ohw = _count(lin.out_shape[1:]) if len(lin.out_shape) > 1 else 1
+        nel = B * _count(lin.out_shape)
+        n_out = B * _count(last.out_shape)
+        Y = torch.empty((n, B) + tuple(last.out_shape), dtype=torch.int64, device=self.dev)
+        d = _lib.ChainDesc()
+        d.acc, d.acc_pstride = acc.data_ptr(), nel
+        bias = self.W[lin.weight + ".b"]
+        d.bias, d.bias_pstride, d.bias_div, d.bias_mod = bias.data_ptr(), O, ohw, O
+        if add is not None:
+            other = [s for s in self._srcs(chain[2]) if s != chain[1]][0]
+            d.other, d.other_pstride = vals[other].data_ptr(), nel
+        d.out, d.out_pstride = Y.data_ptr(), n_out
+        d.nel = nel
+        d.nout = n if lin.passive_out else k
+        d.value_bound, d.r, d.d = tr.value_bound, tr.r, tr.divisor
+        d.emax = additive_mask_bound(self.scheme.field, tr.r * tr.divisor, tr.value_bound)
+        d.verify = int(bool(self.verify))
+        d.fail = self.fail.data_ptr()
+        if nl is not None:
+            if nl.pool_kind is not None:
+                (c, h, w), (kh, kw) = nl.in_shape, nl.pool
+                kind = 1 if nl.pool_kind == "max" else 2
+            elif len(nl.in_shape) == 3:
+                (c, h, w), kh, kw, kind = nl.in_shape, 1, 1, 0
+            else:
+                c, h, w, kh, kw, kind = _count(nl.in_shape), 1, 1, 1, 1, 0
+            d.nonlin, d.relu, d.pool_kind = 1, int(bool(nl.relu)), kind
+            d.nb, d.c, d.h, d.w, d.kh, d.kw = B, c, h, w, kh, kw
+            d.fan = n if nl.passive_out else k
+            d.bmax = multiplicative_mask_bound(self.scheme.field, nl.value_bound)
+        d.party_seed, d.party_stream = party_rng.seed, party_rng.next_stream(m + 1)
+        d.src_seed, d.src_stream = src_rng.seed, src_rng.next_stream(7)
+        d.k, d.n = k, n
+        d.ids, d.rt = ctypes.addressof(self.ids_all), ctypes.addressof(self._rt_all)
+        d.ext = ctypes.addressof(self._ext_host) if self._ext_host is not None else None
+        d.p = p
+        d.fault_rank = self.fault[1] if (self.fault is not None and self.fault[0] == chain[0]) else -1
+        _lib.call("ssn_layer_chain", ctypes.byref(d), _lib.stream_ptr())
+        self.kernel_launches += 1
+        return Y
 
     # ------------------------------------------------------------------ helpers
     def _ew(self, op, a, b, out, n, b_mod=None):
@@ -195,10 +288,17 @@ class BatchedEngine:
         masked_for = {}          # linear idx -> True when its output already carries alpha
         remaining = {i: len(c) for i, c in self.cons.items()}
         result = None
+        pending = {}
         for idx, op in enumerate(self.ops):
             src = idx - 1 if op.src is None else op.src
             xin = vals.get(src)
-            if op.kind == "linear":
+            if idx in self.chains:
+                chain = self.chains[idx]
+                pending[chain[-1]] = self._chain(chain, vals, src_rng, party_rng)
+                y = None
+            elif idx in self._chain_member:
+                y = pending.pop(idx, None)
+            elif op.kind == "linear":
                 y = self._linear(idx, op, xin, src_rng, party_rng)
                 masked_for[idx] = getattr(self, "_fused_alpha", False)
             elif op.kind == "truncation":
@@ -215,12 +315,13 @@ class BatchedEngine:
                 y = None
             else:
                 raise ValueError(op.kind)
-            vals[idx] = y
-            if self.fault is not None and self.fault[0] == idx and y is not None:
+            if y is not None:
+                vals[idx] = y
+            if self.fault is not None and self.fault[0] == idx and y is not None and not self.chains:
                 y[self.fault[1]].view(-1)[0] += 1              # test hook: corrupt one share
-            if capture is not None and y is not None and op.kind != "linear":
+            if capture is not None and y is not None and op.kind != "linear" and idx not in self.chains:
                 capture[idx] = self._reveal(y, op.out_shape)
-            mark(op.kind)
+            mark("chain" if (idx in self.chains or idx in self._chain_member) else op.kind)
             # release inputs no longer needed
             for s in ([src] + ([op.src2] if op.kind == "add" else [])):
                 remaining[s] -= 1
@@ -233,10 +334,10 @@ class BatchedEngine:
         return result
 
     # ------------------------------------------------------------------ ops
-    def _linear(self, idx, op, X, src_rng, party_rng):
-        B, n, k, m, p = self.batch, self.n, self.k, self.m, self.p
+    def _gemm(self, idx, op, X):
+        """Local share products of the m participants (S/layers.py:245-255): acc [m][B][O][ohw]."""
+        B, m, p = self.batch, self.m, self.p
         w = self.W[op.weight + ".w"]
-        b = self.W[op.weight + ".b"]
         O = op.out_shape[0]
         conv = w.dim() == 5
         prof = self._gemm_prof
@@ -263,6 +364,14 @@ class BatchedEngine:
             g1.record()
             kname = "ssn_gemm_tc" if tc else ("ssn_conv_simt" if conv else "ssn_dense_simt")
             prof.append((g0, g1, m * B * ohw * O * K, kname))
+        return acc
+
+    def _linear(self, idx, op, X, src_rng, party_rng):
+        B, n, k, m, p = self.batch, self.n, self.k, self.m, self.p
+        b = self.W[op.weight + ".b"]
+        O = op.out_shape[0]
+        ohw = _count(op.out_shape[1:]) if len(op.out_shape) > 1 else 1
+        acc = self._gemm(idx, op, X)
         N = B * O * ohw
         nout = n if op.passive_out else k
         # source: zero shares for every rank (gen_zero_shares)

@@ -36,11 +36,12 @@ def test_reference_model_batched_matches_plaintext(ssn):
         scheme = ssn.SssScheme(F, k, n)
         B = 8
         xb = np.stack([ssn.random_input(7, model, index=i)[0] for i in range(B)])
-        eng = BatchedEngine(model, scheme, batch=B, seed=9)
-        ops = [op.meta() for op in eng.ops]
-        want, _ = _plain_batch(ops, xb, weights)
-        for _ in range(2):                       # second run uses fresh randomness
-            assert np.array_equal(eng.run(xb), want)
+        for fuse in (False, True):
+            eng = BatchedEngine(model, scheme, batch=B, seed=9, fuse=fuse)
+            ops = [op.meta() for op in eng.ops]
+            want, _ = _plain_batch(ops, xb, weights)
+            for _ in range(2):                       # second run uses fresh randomness
+                assert np.array_equal(eng.run(xb), want)
 
 
 def test_avg_pool_chain_model(ssn):
@@ -49,20 +50,23 @@ def test_avg_pool_chain_model(ssn):
     weights = {name: qt.values for name, qt in model.weights.items()}
     scheme = ssn.SssScheme(ssn.PrimeField(), 2, 3)
     xb = np.stack([ssn.random_input(8, model, index=i)[0] for i in range(4)])
-    eng = BatchedEngine(model, scheme, batch=4, seed=2)
     want = np.stack([ssn.plaintext_infer(model, xb[i]) for i in range(4)])
-    assert np.array_equal(eng.run(xb), want)
+    for fuse in (False, True):
+        eng = BatchedEngine(model, scheme, batch=4, seed=2, fuse=fuse)
+        assert np.array_equal(eng.run(xb), want)
 
 
+@pytest.mark.parametrize("fuse", [False, True])
 @pytest.mark.parametrize("k,n", [(2, 3), (3, 5)])
-def test_tiny_resnet_every_op_reconstructs_to_plaintext(ssn, k, n):
+def test_tiny_resnet_every_op_reconstructs_to_plaintext(ssn, k, n, fuse):
     from paper_2406_02629_b200 import resnet
     from paper_2406_02629_b200.batched import BatchedEngine
     net = resnet.tiny_resnet(seed=3)
     scheme = ssn.SssScheme(ssn.PrimeField(), k, n)
     B = 3
     xb = net.random_inputs(seed=5, batch=B)
-    eng = BatchedEngine(net, scheme, batch=B, seed=11)
+    eng = BatchedEngine(net, scheme, batch=B, seed=11, fuse=fuse)
+    assert bool(eng.chains) == fuse
     ops = [op.meta() for op in eng.ops]
     want, inter = _plain_batch(ops, xb, net.weight_values())
     cap = {}
@@ -87,14 +91,15 @@ def test_cifar_resnet18_batched_matches_plaintext(ssn):
     assert np.array_equal(eng.run(xb), want)
 
 
-def test_verification_detects_corruption(ssn):
+@pytest.mark.parametrize("fuse", [False, True])
+def test_verification_detects_corruption(ssn, fuse):
     from paper_2406_02629_b200 import resnet
     from paper_2406_02629_b200.batched import BatchedEngine
     from paper_2406_02629_b200.protocol import VerificationError
     net = resnet.tiny_resnet(seed=3)
     scheme = ssn.SssScheme(ssn.PrimeField(), 3, 5)
     xb = net.random_inputs(seed=6, batch=2)
-    eng = BatchedEngine(net, scheme, batch=2, seed=4, verify=True)
+    eng = BatchedEngine(net, scheme, batch=2, seed=4, verify=True, fuse=fuse)
     want, _ = resnet.plaintext_forward(net, xb)
     assert np.array_equal(eng.run(xb), want)
     first_linear = next(i for i, op in enumerate(eng.ops) if op.kind == "linear")
