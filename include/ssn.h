@@ -190,6 +190,9 @@ typedef struct ssn_chain_desc {
 } ssn_chain_desc;
 
 int ssn_layer_chain(const ssn_chain_desc *desc, void *stream);
+/* 1 if ssn_layer_chain supports (k, n, ids, p): a pseudo-Mersenne prime within 2^-24 of a
+ * power of two (masked uniform draws) and small-rational protocol constants; else 0. */
+int ssn_chain_supported(int k, int n, const uint64_t *ids, uint64_t p);
 
 #ifdef __cplusplus
 }

@@ -73,6 +73,7 @@ _SIGS = {
     "ssn_im2col_limbs": [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _U64, _U64, _P],
     "ssn_gemm_tc": [_P, _P, _I32, _I32, _I32, _I32, _U64, _U64, _P, _U64, _U64, _P],
     "ssn_layer_chain": [_P, _P],
+    "ssn_chain_supported": [_I32, _I32, _P, _U64],
 }
 
 

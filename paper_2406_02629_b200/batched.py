@@ -120,6 +120,8 @@ class BatchedEngine:
         single consumer into one fused protocol launch (csrc/ssn_chain.cu)."""
         if (self.k, self.n) not in self.CHAIN_SCHEMES:
             return {}
+        if not _lib.load(require_cuda=False).ssn_chain_supported(self.k, self.n, self.ids_all, self.p):
+            return {}
         ops, cons = self.ops, self.cons
         chains = {}
         for idx, op in enumerate(ops):

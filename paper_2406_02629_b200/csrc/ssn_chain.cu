@@ -16,35 +16,51 @@
 // TRUNC_MASKED, SHARE_DIST, NONLIN_MASKED, NONLIN_PLAIN) is computed exactly as the
 // reference computes it, and the hand-off between parties is a register move instead of an
 // HBM round trip.  The trusted source's masks (zero shares, alpha/comp, beta/beta^-1,
-// S/masks.py) are drawn in the same thread from the source's Philox lane.  HBM traffic per
-// element: 8*m bytes of GEMM output in, 8*n bytes of shares out (+8*n for a residual add).
+// S/masks.py) are drawn in the same thread from the source's Philox lane; beta^-1 for the 32
+// windows of a warp comes from one Fermat inversion plus warp-shuffle prefix/suffix
+// products (Montgomery's batch trick across lanes).  HBM traffic per element: 8*m bytes of
+// GEMM output in, 8*n bytes of shares out (+8*n for a residual add).
+//
+// The kernels are specialised to keep their SASS small (they are instruction-fetch bound
+// otherwise): the field must be pseudo-Mersenne with masked uniform draws (the default
+// p = 2^45 - 55, S/field.py:21) and every protocol constant must be a small rational (true
+// for the default party ids 1..n).  ssn_chain_supported() tells the host; other schemes use
+// the unfused kernels of ssn_elementwise.cu.
 #include "ssn.h"
 #include "ssn_field.cuh"
 #include "ssn_lincomb.cuh"
 
 namespace {
 
-template <int N>
-struct ChainTables {
-    LinRow wf;          // Lagrange weights of the front ids at 0 (k entries)
-    LinRow wp;          // Lagrange weights of the participant ids at 0 (m entries)
-    LinRow rt[N];       // R^T rows: out rank t <- participants j (m entries)
-    LinRow ext[N];      // Reed-Solomon rows: id t (t >= k) <- front ids (k entries)
-    LinRow pw[N];       // id_t^(e+1), e < k-1
-    int small_wf, small_wp, small_rt, small_ext, small_pw;
+template <int M>
+struct SRow {            // sum_j n[j] x_j / D  (dinv = D^-1 mod p, one = (D == 1))
+    int32_t n[M];
+    int32_t one;
+    u64 dinv;
+};
+
+template <int K, int N>
+struct STables {
+    static constexpr int M = 2 * K - 1;
+    SRow<K> wf;          // Lagrange weights of the front ids at 0
+    SRow<M> wp;          // Lagrange weights of the participant ids at 0
+    SRow<M> rt[N];       // R^T rows: out rank t <- participants j
+    SRow<K> ext[N];      // Reed-Solomon rows: id t (t >= k) <- front ids
+    uint32_t pw[N][K - 1];   // id_t^(e+1), e < k-1 (small, non-negative)
 };
 
 struct ChainArgs {
     const u64 *acc;
     u64 acc_ps;
     const u64 *bias;
-    u64 bias_ps, bias_div, bias_mod;
+    u64 bias_ps;
+    uint32_t bias_div, bias_mod;
     const u64 *other;
     u64 other_ps;
     u64 *out;
     u64 out_ps;
     u64 nel;
-    int nout, senders, nonlin, relu, pool_kind, c, h, w, kh, kw, fan, nb;
+    int nout, senders, relu, pool_kind, c, h, w, kh, kw, fan, nb;
     i64 lo, r, d;
     u64 neglo_mod, stepm, emax, bmax;
     int rshift;
@@ -53,97 +69,120 @@ struct ChainArgs {
     int fault_rank;
 };
 
-// share of `s` for rank t with coefficients c (K-1 of them)
-template <int K>
-__device__ __forceinline__ u64 share_at(u64 s, const u64 (&c)[SSN_MAXK], const LinRow &pw, int small,
-                                        const SsnField &f) {
-    if (small) {
-        u64 acc = s;
+__device__ __forceinline__ u64 mulmod_pm(u64 a, u64 b, const SsnField &f) {
+    return ssn_pmfold(__umul64hi(a, b), a * b, f);
+}
+__device__ __forceinline__ u64 fold64(u64 x, const SsnField &f) { return ssn_pmfold(0, x, f); }
+
+template <int M>
+__device__ __forceinline__ u64 lin(const u64 (&x)[M], const SRow<M> &r, const SsnField &f) {
+    u64 pos = 0, neg = 0;
 #pragma unroll
-        for (int j = 0; j < K - 1; j++) acc += mul_small(c[j], (uint32_t)pw.n[j]);
-        return ssn_reduce64(acc, f);
+    for (int j = 0; j < M; j++) {
+        const int32_t c = r.n[j];
+        const u64 t = mul_small(x[j], (uint32_t)(c >= 0 ? c : -c));
+        if (c >= 0) pos += t;
+        else neg += t;
     }
-    u64 acc = s;
-#pragma unroll
-    for (int j = 0; j < K - 1; j++) acc = ssn_addmod(acc, ssn_mulmod(c[j], pw.w[j], f), f.p);
-    return acc;
+    const u64 v = ssn_submod(fold64(pos, f), fold64(neg, f), f.p);
+    return r.one ? v : mulmod_pm(v, r.dinv, f);
 }
 
-template <int K>
-__device__ __forceinline__ void coeffs(u64 (&c)[SSN_MAXK], u64 seed, u64 stream, u64 i, const SsnField &f) {
+// share of s at rank t: s + sum_e c_e * id_t^(e+1)
+template <int K, int N>
+__device__ __forceinline__ u64 share_at(u64 s, const u64 (&c)[K - 1], const STables<K, N> &tb, int t,
+                                        const SsnField &f) {
+    u64 acc = s;
 #pragma unroll
-    for (int jp = 0; jp < (K - 1 + 1) / 2; jp++) ssn_rand_field2(seed, stream, i, jp, f, c[2 * jp], c[2 * jp + 1]);
+    for (int e = 0; e < K - 1; e++) acc += mul_small(c[e], tb.pw[t][e]);
+    return fold64(acc, f);
+}
+
+// K-1 uniform field elements (masked 64-bit Philox words; p is 2^-39 close to 2^45)
+template <int K>
+__device__ __forceinline__ void coeffs(u64 (&c)[K - 1], u64 seed, u64 stream, u64 i, const SsnField &f) {
+#pragma unroll
+    for (int jp = 0; jp < K / 2; jp++) {
+        const ssn_u4 r = ssn_philox_at(seed, stream, i, 0x800u | jp);
+        u64 x0 = (((u64)r.x << 32) | r.y) & f.mask;
+        u64 x1 = (((u64)r.z << 32) | r.w) & f.mask;
+        if (x0 >= f.p) x0 -= f.p;
+        if (x1 >= f.p) x1 -= f.p;
+        c[2 * jp] = x0;
+        if (2 * jp + 1 < K - 1) c[2 * jp + 1] = x1;
+    }
 }
 
 // reshare + rerand + bias + truncation (+ residual add) of element i for all N parties.
 template <int K, int N>
-__device__ __forceinline__ void chain_elem(const ChainArgs &a, const ChainTables<N> &tb, u64 i, u64 (&x)[N],
+__device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, N> &tb, uint32_t i, u64 (&x)[N],
                                            unsigned long long &bad, const SsnField &f) {
     constexpr int M = 2 * K - 1;
+    u64 acc[M];
+#pragma unroll
+    for (int j = 0; j < M; j++) acc[j] = a.acc[(u64)j * a.acc_ps + i];
     // ---- reshare step 1 (RESHARE_OUT): participant j sub-shares its local product to the front
-    u64 sub[K][SSN_MAXP];
+    u64 sub[K][M];
 #pragma unroll
     for (int j = 0; j < M; j++) {
-        const u64 v = a.acc[(u64)j * a.acc_ps + i];
-        u64 c[SSN_MAXK];
+        u64 c[K - 1];
         coeffs<K>(c, a.pseed, a.pstream + j, i, f);
 #pragma unroll
-        for (int fr = 0; fr < K; fr++) sub[fr][j] = share_at<K>(v, c, tb.pw[fr], tb.small_pw, f);
+        for (int fr = 0; fr < K; fr++) sub[fr][j] = share_at<K, N>(acc[j], c, tb, fr, f);
     }
-    // ---- step 2 (RESHARE_BACK): front fr applies R^T; step 3: out rank t reconstructs
-    u64 back[N][SSN_MAXP];
-#pragma unroll
-    for (int fr = 0; fr < K; fr++)
-#pragma unroll
-        for (int t = 0; t < N; t++)
-            if (t < a.nout) back[t][fr] = lincomb<SSN_MAXP>(sub[fr], tb.rt[t], tb.small_rt, M, f);
     // source: zero shares (gen_zero_shares) and the truncation masks (gen_additive_mask)
-    u64 z[SSN_MAXK], ca[SSN_MAXK], cc[SSN_MAXK];
+    u64 z[K - 1], ca[K - 1], cc[K - 1];
     coeffs<K>(z, a.sseed, a.sstream + 0, i, f);
     const u64 e = 1 + ssn_rand_range(a.sseed, a.sstream + 1, i, 0, a.emax);
-    const u64 em = ssn_reduce64(e, f);
-    const u64 alpha = ssn_mulmod(em, a.stepm, f);
+    const u64 em = fold64(e, f);
+    const u64 alpha = mulmod_pm(em, a.stepm, f);
     const u64 comp = em ? f.p - em : 0;
     coeffs<K>(ca, a.sseed, a.sstream + 2, i, f);
     coeffs<K>(cc, a.sseed, a.sstream + 3, i, f);
-    const u64 ch = (a.bias_div == 1 ? i : i / a.bias_div) % a.bias_mod;
+    const uint32_t ch = (i / a.bias_div) % a.bias_mod;
+    // ---- step 2 (RESHARE_BACK): front fr applies R^T; step 3: out rank t reconstructs,
+    //      + zero share (rerand) + bias share, then + alpha share (TRUNC_MASKED)
     u64 masked[N];
 #pragma unroll
     for (int t = 0; t < N; t++) {
         if (t < a.senders) {
-            u64 y = lincomb<SSN_MAXP>(back[t], tb.wf, tb.small_wf, K, f);
-            y = ssn_addmod(y, share_at<K>(0, z, tb.pw[t], tb.small_pw, f), f.p);          // rerand
-            y = ssn_addmod(y, a.bias[(u64)t * a.bias_ps + ch], f.p);                       // + bias
+            u64 back[K];
+#pragma unroll
+            for (int fr = 0; fr < K; fr++) back[fr] = lin<M>(sub[fr], tb.rt[t], f);
+            u64 y = lin<K>(back, tb.wf, f);
+            y = ssn_addmod(y, share_at<K, N>(0, z, tb, t, f), f.p);
+            y = ssn_addmod(y, a.bias[(u64)t * a.bias_ps + ch], f.p);
             if (t == a.fault_rank && i == 0) y = ssn_addmod(y, 1, f.p);                   // test hook
-            masked[t] = ssn_addmod(y, share_at<K>(alpha, ca, tb.pw[t], tb.small_pw, f), f.p);  // + alpha
+            masked[t] = ssn_addmod(y, share_at<K, N>(alpha, ca, tb, t, f), f.p);
         }
     }
-    // ---- truncation elite (TRUNC_MASKED from actives): rec, RS check, decode, floor, round
-    u64 front[SSN_MAXP];
+    // ---- truncation elite: rec over the front, RS check of the extra points, decode/floor/round
+    u64 front[K];
 #pragma unroll
     for (int j = 0; j < K; j++) front[j] = masked[j];
-    const u64 v = lincomb<SSN_MAXP>(front, tb.wf, tb.small_wf, K, f);
+    const u64 v = lin<K>(front, tb.wf, f);
 #pragma unroll
     for (int t = K; t < N; t++)
-        if (t < a.senders) bad += (lincomb<SSN_MAXP>(front, tb.ext[t], tb.small_ext, K, f) != masked[t]);
+        if (t < a.senders) bad += (lin<K>(front, tb.ext[t], f) != masked[t]);
     const u64 tm = ssn_trunc_value(v, a.lo, a.neglo_mod, a.r, a.rshift, a.d, f);
     // fresh (k, n) shares of the truncated value (SHARE_DIST), + comp at every rank
-    u64 g[SSN_MAXK];
+    u64 g[K - 1];
     coeffs<K>(g, a.pseed, a.pstream + M, i, f);
 #pragma unroll
     for (int t = 0; t < N; t++) {
-        u64 s = share_at<K>(tm, g, tb.pw[t], tb.small_pw, f);
-        s = ssn_addmod(s, share_at<K>(comp, cc, tb.pw[t], tb.small_pw, f), f.p);
+        u64 s = ssn_addmod(share_at<K, N>(tm, g, tb, t, f), share_at<K, N>(comp, cc, tb, t, f), f.p);
         if (a.other) s = ssn_addmod(s, a.other[(u64)t * a.other_ps + i], f.p);         // residual add
         x[t] = s;
     }
 }
 
 template <int K, int N>
-__global__ void __launch_bounds__(128) k_chain_plain(ChainArgs a, const __grid_constant__ ChainTables<N> tb,
+__global__ void __launch_bounds__(128) k_chain_plain(ChainArgs a, const __grid_constant__ STables<K, N> tb,
                                                      SsnField f) {
     unsigned long long bad = 0;
-    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < a.nel; i += (u64)gridDim.x * blockDim.x) {
+    const uint32_t nel = (uint32_t)a.nel;
+#pragma unroll 1
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nel; i += gridDim.x * blockDim.x) {
         u64 x[N];
         chain_elem<K, N>(a, tb, i, x, bad, f);
 #pragma unroll
@@ -152,137 +191,156 @@ __global__ void __launch_bounds__(128) k_chain_plain(ChainArgs a, const __grid_c
     if (a.fail && bad) atomicAdd(a.fail, bad);
 }
 
-// masked nonlinearity fused after the chain: one thread per output window, WPT windows
-// per thread (spaced a grid apart, coalesced) so beta^-1 costs one Fermat inversion per WPT
-// windows (Montgomery batch inversion).
-constexpr int WPT = 4;
+// exclusive prefix (up) / suffix (down) products across the warp; inactive lanes hold 1
+__device__ __forceinline__ u64 warp_excl_prefix(u64 v, int lane, const SsnField &f) {
+    u64 incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u64 t = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl = mulmod_pm(incl, t, f);
+    }
+    const u64 ex = __shfl_up_sync(0xffffffffu, incl, 1);
+    return lane ? ex : 1;
+}
+__device__ __forceinline__ u64 warp_excl_suffix(u64 v, int lane, const SsnField &f) {
+    u64 incl = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const u64 t = __shfl_down_sync(0xffffffffu, incl, o);
+        if (lane + o < 32) incl = mulmod_pm(incl, t, f);
+    }
+    const u64 ex = __shfl_down_sync(0xffffffffu, incl, 1);
+    return lane < 31 ? ex : 1;
+}
 
+// masked nonlinearity fused after the chain: one thread per output window.
 template <int K, int N>
-__global__ void __launch_bounds__(128) k_chain_nonlin(ChainArgs a, const __grid_constant__ ChainTables<N> tb,
+__global__ void __launch_bounds__(128) k_chain_nonlin(ChainArgs a, const __grid_constant__ STables<K, N> tb,
                                                       SsnField f) {
     constexpr int M = 2 * K - 1;
     unsigned long long bad = 0;
-    const int oh = a.h / a.kh, ow = a.w / a.kw;
-    const u64 n_out = (u64)a.nb * a.c * oh * ow;
-    const u64 T = (u64)gridDim.x * blockDim.x;
-    for (u64 o0 = blockIdx.x * (u64)blockDim.x + threadIdx.x; o0 < n_out; o0 += T * WPT) {
-        u64 plain[WPT], beta[WPT], pre[WPT];
-        u64 run = 1;
-#pragma unroll
-        for (int q = 0; q < WPT; q++) {
-            const u64 o = o0 + (u64)q * T;
-            plain[q] = 0;
-            beta[q] = 1;
-            if (o < n_out) {
-                beta[q] = 1 + ssn_rand_range(a.sseed, a.sstream + 4, o, 0, a.bmax);   // window-constant beta
-                u64 base_in = o;
-                if (a.kh != 1 || a.kw != 1) {
-                    const uint32_t o32 = (uint32_t)o, chw = (uint32_t)(a.c * oh * ow), hw = (uint32_t)(oh * ow);
-                    const uint32_t img = o32 / chw, rem = o32 - img * chw;
-                    const uint32_t ci = rem / hw, rr = rem - ci * hw;
-                    const uint32_t y0 = rr / (uint32_t)ow, x0 = rr - y0 * (uint32_t)ow;
-                    base_in = (((u64)img * a.c + ci) * (u64)a.h + (u64)(y0 * a.kh)) * a.w + (u64)(x0 * a.kw);
-                }
-                i64 acc = a.pool_kind == 1 ? INT64_MIN : 0;
-                for (int wy = 0; wy < a.kh; wy++)
-                    for (int wx = 0; wx < a.kw; wx++) {
-                        const u64 i = base_in + (u64)wy * a.w + wx;
-                        u64 x[N];
-                        chain_elem<K, N>(a, tb, i, x, bad, f);
-                        // participants mask with their beta shares (NONLIN_MASKED), elite rec over m
-                        u64 cb[SSN_MAXK];
-                        coeffs<K>(cb, a.sseed, a.sstream + 5, i, f);
-                        u64 mk[SSN_MAXP];
-#pragma unroll
-                        for (int j = 0; j < M; j++)
-                            mk[j] = ssn_mulmod(x[j], share_at<K>(beta[q], cb, tb.pw[j], tb.small_pw, f), f);
-                        const u64 v = lincomb<SSN_MAXP>(mk, tb.wp, tb.small_wp, M, f);
-                        i64 sv = v > f.half ? (i64)v - (i64)f.p : (i64)v;
-                        if (a.relu && sv <= 0) sv = 0;
-                        if (a.pool_kind == 1) acc = sv > acc ? sv : acc;
-                        else acc += sv;
-                    }
-                plain[q] = acc < 0 ? (u64)((i64)f.p + acc) : (u64)acc;      // encode_signed (NONLIN_PLAIN)
+    const int lane = threadIdx.x & 31;
+    const uint32_t oh = a.h / a.kh, ow = a.w / a.kw;
+    const uint32_t hw = oh * ow, chw = (uint32_t)a.c * hw;
+    const uint32_t n_out = (uint32_t)a.nb * chw;
+    const bool pooled = a.kh != 1 || a.kw != 1;
+#pragma unroll 1
+    for (uint32_t base = blockIdx.x * blockDim.x; base < n_out; base += gridDim.x * blockDim.x) {
+        const uint32_t o = base + threadIdx.x;
+        const bool live = o < n_out;
+        u64 plain = 0, beta = 1;
+        if (live) {
+            beta = 1 + ssn_rand_range(a.sseed, a.sstream + 4, o, 0, a.bmax);     // window-constant beta
+            uint32_t base_in = o;
+            if (pooled) {
+                const uint32_t img = o / chw, rem = o - img * chw;
+                const uint32_t ci = rem / hw, rr = rem - ci * hw;
+                const uint32_t y0 = rr / ow, x0 = rr - y0 * ow;
+                base_in = ((img * a.c + ci) * a.h + y0 * a.kh) * a.w + x0 * a.kw;
             }
-            run = ssn_mulmod(run, beta[q], f);
-            pre[q] = run;
-        }
-        u64 inv = ssn_powmod(run, f.p - 2, f);
+            i64 acc = a.pool_kind == 1 ? INT64_MIN : 0;
+#pragma unroll 1
+            for (int wy = 0; wy < a.kh; wy++)
+#pragma unroll 1
+                for (int wx = 0; wx < a.kw; wx++) {
+                    const uint32_t i = base_in + wy * a.w + wx;
+                    u64 x[N];
+                    chain_elem<K, N>(a, tb, i, x, bad, f);
+                    // participants mask with their beta shares (NONLIN_MASKED); elite rec over m
+                    u64 cb[K - 1];
+                    coeffs<K>(cb, a.sseed, a.sstream + 5, i, f);
+                    u64 mk[M];
 #pragma unroll
-        for (int q = WPT - 1; q >= 0; q--) {
-            const u64 bi = q ? ssn_mulmod(inv, pre[q - 1], f) : inv;
-            inv = ssn_mulmod(inv, beta[q], f);
-            pre[q] = bi;                                     // beta^-1 of window q
+                    for (int j = 0; j < M; j++) mk[j] = mulmod_pm(x[j], share_at<K, N>(beta, cb, tb, j, f), f);
+                    const u64 v = lin<M>(mk, tb.wp, f);
+                    i64 sv = v > f.half ? (i64)v - (i64)f.p : (i64)v;
+                    if (a.relu && sv <= 0) sv = 0;
+                    if (a.pool_kind == 1) acc = sv > acc ? sv : acc;
+                    else acc += sv;
+                }
+            plain = acc < 0 ? (u64)((i64)f.p + acc) : (u64)acc;                  // encode_signed (NONLIN_PLAIN)
         }
-#pragma unroll
-        for (int q = 0; q < WPT; q++) {
-            const u64 o = o0 + (u64)q * T;
-            if (o >= n_out) continue;
-            u64 cbi[SSN_MAXK];
+        // source: beta^-1 per window -- one inversion per warp (prefix/suffix products)
+        const u64 pre = warp_excl_prefix(beta, lane, f);
+        const u64 suf = warp_excl_suffix(beta, lane, f);
+        const u64 all = __shfl_sync(0xffffffffu, mulmod_pm(pre, beta, f), 31);
+        const u64 inv_all = ssn_powmod(all, f.p - 2, f);
+        const u64 binv = mulmod_pm(mulmod_pm(pre, suf, f), inv_all, f);
+        if (live) {
+            u64 cbi[K - 1];
             coeffs<K>(cbi, a.sseed, a.sstream + 6, o, f);
 #pragma unroll
             for (int t = 0; t < N; t++)
-                if (t < a.fan)
-                    a.out[(u64)t * a.out_ps + o] =
-                        ssn_mulmod(plain[q], share_at<K>(pre[q], cbi, tb.pw[t], tb.small_pw, f), f);
+                if (t < a.fan) a.out[(u64)t * a.out_ps + o] = mulmod_pm(plain, share_at<K, N>(binv, cbi, tb, t, f), f);
         }
     }
     if (a.fail && bad) atomicAdd(a.fail, bad);
 }
 
+template <int MM>
+static int make_srow(SRow<MM> &s, const u64 *w, int m, u64 p) {
+    LinRow r;
+    u64 row[SSN_MAXJ] = {0};
+    for (int j = 0; j < m; j++) row[j] = w[j];
+    const int ok = make_row(r, row, m, p);
+    for (int j = 0; j < MM; j++) s.n[j] = j < m ? r.n[j] : 0;
+    s.one = r.one;
+    s.dinv = r.dinv;
+    return ok;
+}
+
+// Lagrange weights at 0 of ids[0..cnt)
+static void lagrange0(u64 *row, const u64 *ids, int cnt, u64 p) {
+    for (int i = 0; i < cnt; i++) {
+        unsigned __int128 num = 1, den = 1;
+        for (int j = 0; j < cnt; j++)
+            if (j != i) {
+                num = num * (ids[j] % p) % p;
+                den = den * ((ids[j] % p + p - ids[i] % p) % p) % p;
+            }
+        row[i] = (u64)(num * inv_host((u64)den, p) % p);
+    }
+}
+
+template <int K, int N>
+int build_tables(STables<K, N> &tb, const u64 *ids, const u64 *rt, const u64 *ext, u64 p) {
+    constexpr int M = 2 * K - 1;
+    const SsnField f = ssn_make_field(p);
+    if (!f.pm || !f.near) return 0;
+    int ok = 1;
+    u64 row[SSN_MAXJ];
+    lagrange0(row, ids, K, p);
+    ok &= make_srow<K>(tb.wf, row, K, p);
+    lagrange0(row, ids, M, p);
+    ok &= make_srow<M>(tb.wp, row, M, p);
+    for (int t = 0; t < N; t++) {
+        if (rt) ok &= make_srow<M>(tb.rt[t], rt + (u64)t * M, M, p);
+        u64 zero[SSN_MAXJ] = {0};
+        if (t >= K && ext) ok &= make_srow<K>(tb.ext[t], ext + (u64)(t - K) * K, K, p);
+        else make_srow<K>(tb.ext[t], zero, K, p);
+        unsigned __int128 acc = 1;
+        for (int e = 0; e < K - 1; e++) {
+            acc = acc * (ids[t] % p) % p;
+            ok &= acc < (1u << 13);
+            tb.pw[t][e] = (uint32_t)acc;
+        }
+    }
+    return ok;
+}
+
 template <int K, int N>
 int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
-    constexpr int M = 2 * K - 1;
     const u64 p = d->p;
-    ChainTables<N> tb;
-    u64 row[SSN_MAXJ];
-    // Lagrange weights at 0 of ids[0..cnt)
-    auto lagrange = [&](int cnt) {
-        for (int i = 0; i < SSN_MAXJ; i++) row[i] = 0;
-        for (int i = 0; i < cnt; i++) {
-            unsigned __int128 num = 1, den = 1;
-            for (int j = 0; j < cnt; j++)
-                if (j != i) {
-                    num = num * (d->ids[j] % p) % p;
-                    den = den * ((d->ids[j] + p - d->ids[i] % p) % p) % p;
-                }
-            row[i] = (u64)(num * inv_host((u64)den, p) % p);
-        }
-    };
-    lagrange(K);
-    tb.small_wf = make_row(tb.wf, row, K, p);
-    lagrange(M);
-    tb.small_wp = make_row(tb.wp, row, M, p);
-    tb.small_rt = tb.small_ext = tb.small_pw = 1;
-    for (int t = 0; t < N; t++) {
-        for (int j = 0; j < SSN_MAXJ; j++) row[j] = 0;
-        for (int j = 0; j < M; j++) row[j] = d->rt[t * M + j];
-        tb.small_rt &= make_row(tb.rt[t], row, M, p);
-        for (int j = 0; j < SSN_MAXJ; j++) row[j] = 0;
-        if (t >= K) {
-            for (int j = 0; j < K; j++) row[j] = d->ext[(t - K) * K + j];
-            tb.small_ext &= make_row(tb.ext[t], row, K, p);
-        } else {
-            make_row(tb.ext[t], row, K, p);
-        }
-        for (int j = 0; j < SSN_MAXJ; j++) row[j] = 0;
-        unsigned __int128 acc = 1;
-        for (int j = 0; j < K - 1; j++) {
-            acc = acc * (d->ids[t] % p) % p;
-            row[j] = (u64)acc;
-        }
-        int ok = make_row(tb.pw[t], row, K - 1, p);
-        for (int j = 0; j < K - 1; j++) ok = ok && tb.pw[t].n[j] >= 0;
-        tb.small_pw &= ok && tb.pw[t].one;
-    }
+    STables<K, N> tb;
+    if (!build_tables<K, N>(tb, d->ids, d->rt, d->ext, p)) return SSN_ERR_UNSUPPORTED;
     const SsnField f = ssn_make_field(p);
     ChainArgs a;
     a.acc = d->acc;
     a.acc_ps = d->acc_pstride;
     a.bias = d->bias;
     a.bias_ps = d->bias_pstride;
-    a.bias_div = d->bias_div;
-    a.bias_mod = d->bias_mod;
+    a.bias_div = (uint32_t)d->bias_div;
+    a.bias_mod = (uint32_t)d->bias_mod;
     a.other = d->other;
     a.other_ps = d->other_pstride;
     a.out = d->out;
@@ -290,7 +348,6 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
     a.nel = d->nel;
     a.nout = d->nout;
     a.senders = d->verify ? N : K;
-    a.nonlin = d->nonlin;
     a.relu = d->relu;
     a.pool_kind = d->pool_kind;
     a.c = d->c;
@@ -321,25 +378,42 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
     if (a.senders > a.nout) return SSN_ERR_ARG;
     if (!d->nonlin) {
         u64 blocks = (a.nel + 127) / 128;
-        if (blocks > 148ull * 12) blocks = 148ull * 12;
+        if (blocks > 148ull * 16) blocks = 148ull * 16;
         k_chain_plain<K, N><<<(unsigned)blocks, 128, 0, st>>>(a, tb, f);
     } else {
         const u64 n_out = (u64)d->nb * d->c * (d->h / d->kh) * (d->w / d->kw);
-        if (n_out >= (1ull << 32)) return SSN_ERR_UNSUPPORTED;
-        u64 blocks = (n_out + 128 * WPT - 1) / (128 * WPT);
-        if (blocks > 148ull * 12) blocks = 148ull * 12;
+        u64 blocks = (n_out + 127) / 128;
+        if (blocks > 148ull * 16) blocks = 148ull * 16;
         if (blocks < 1) blocks = 1;
         k_chain_nonlin<K, N><<<(unsigned)blocks, 128, 0, st>>>(a, tb, f);
     }
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
 
+template <int K, int N>
+int supported(const u64 *ids, u64 p) {
+    STables<K, N> tb;
+    u64 rt[N * (2 * K - 1)] = {0};
+    return build_tables<K, N>(tb, ids, rt, nullptr, p);
+}
+
 }  // namespace
+
+extern "C" int ssn_chain_supported(int k, int n, const uint64_t *ids, uint64_t p) {
+    if (!ids) return 0;
+    if (k == 2 && n == 3) return supported<2, 3>(ids, p);
+    if (k == 3 && n == 5) return supported<3, 5>(ids, p);
+    if (k == 4 && n == 7) return supported<4, 7>(ids, p);
+    return 0;
+}
 
 extern "C" int ssn_layer_chain(const ssn_chain_desc *d, void *stream) {
     if (!d || !d->acc || !d->bias || !d->out || !d->ids || !d->rt) return SSN_ERR_ARG;
     if (d->r < 1 || d->d < 1 || d->emax < 1 || d->nout < d->k || d->nout > d->n) return SSN_ERR_ARG;
     if (d->verify && (!d->ext || d->nout != d->n)) return SSN_ERR_ARG;
+    if (d->nel >= (1ull << 32) || d->bias_div < 1 || d->bias_mod < 1 || d->bias_div >= (1ull << 32) ||
+        d->bias_mod >= (1ull << 32))
+        return SSN_ERR_UNSUPPORTED;
     if (d->nonlin) {
         if (d->kh < 1 || d->kw < 1 || d->h % d->kh || d->w % d->kw || d->bmax < 1 || d->fan < 1 || d->fan > d->n ||
             d->pool_kind < 0 || d->pool_kind > 2 || (d->pool_kind == 0 && (d->kh != 1 || d->kw != 1)))
