@@ -69,13 +69,55 @@ struct ChainArgs {
     int fault_rank;
 };
 
-__device__ __forceinline__ u64 mulmod_pm(u64 a, u64 b, const SsnField &f) {
-    return ssn_pmfold(__umul64hi(a, b), a * b, f);
-}
-__device__ __forceinline__ u64 fold64(u64 x, const SsnField &f) { return ssn_pmfold(0, x, f); }
+constexpr int CHAIN_THREADS = 128;
+constexpr int CHAIN_WARPS = CHAIN_THREADS / 32;
 
+// ---- arithmetic in the default field p = 2^45 - 55 (S/field.py:21) with compile-time fold
+constexpr int PS = 45;
+constexpr u64 PC = 55;
+constexpr u64 PP = (1ull << PS) - PC;
+constexpr u64 PMASK = (1ull << PS) - 1;
+constexpr u64 PHALF = (PP - 1) / 2;
+
+// Intermediates are kept LAZY: any representative below 2^46 (not necessarily < p); only
+// compared and stored values are canonicalised.
+// lz: any x < 2^64 -> < 2^46, since (x >> 45) * 55 < 2^25.
+__device__ __forceinline__ u64 lz(u64 x) { return (x >> PS) * PC + (x & PMASK); }
+// canon: x < 2^64 -> [0, p) ((x >> 45) * 55 + low < 2^45 + 2^25 < 2p)
+__device__ __forceinline__ u64 canon(u64 x) {
+    const u64 t = lz(x);
+    return t >= PP ? t - PP : t;
+}
+__device__ __forceinline__ u64 red64(u64 x) { return canon(x); }
+__device__ __forceinline__ u64 addm(u64 a, u64 b) {
+    const u64 s = a + b;
+    return s >= PP ? s - PP : s;
+}
+// a * b < 2^96 (e.g. both lazy): q = prod >> 45 < 2^51, q*55 + low < 2^58 -> lazy result
+__device__ __forceinline__ u64 mulm(u64 a, u64 b) {
+    const u64 lo = a * b, hi = __umul64hi(a, b);
+    const u64 q = (hi << (64 - PS)) | (lo >> PS);
+    return lz(q * PC + (lo & PMASK));
+}
+__device__ __forceinline__ u64 sqn(u64 x, int n) {
+#pragma unroll 1
+    for (int i = 0; i < n; i++) x = mulm(x, x);
+    return x;
+}
+// x^(p-2) = x^(2^45 - 57) by the addition chain x^(2^39-1)^(2^6) * x^7 (52 multiplications)
+__device__ __noinline__ u64 invm(u64 x) {
+    const u64 x2 = mulm(x, x), x3 = mulm(x2, x), x7 = mulm(mulm(x3, x3), x);
+    const u64 x6b = mulm(sqn(x7, 3), x7);            // x^(2^6-1)
+    const u64 x12 = mulm(sqn(x6b, 6), x6b);          // x^(2^12-1)
+    const u64 x24 = mulm(sqn(x12, 12), x12);         // x^(2^24-1)
+    const u64 x36 = mulm(sqn(x24, 12), x12);         // x^(2^36-1)
+    const u64 x39 = mulm(sqn(x36, 3), x7);           // x^(2^39-1)
+    return mulm(sqn(x39, 6), x7);
+}
+
+// sum_j n_j x_j / D for lazy x_j (< 2^47): |n_j| < 2^13 keeps pos/neg below 2^63 for M <= 7
 template <int M>
-__device__ __forceinline__ u64 lin(const u64 (&x)[M], const SRow<M> &r, const SsnField &f) {
+__device__ __forceinline__ u64 lin(const u64 (&x)[M], const SRow<M> &r) {
     u64 pos = 0, neg = 0;
 #pragma unroll
     for (int j = 0; j < M; j++) {
@@ -84,39 +126,48 @@ __device__ __forceinline__ u64 lin(const u64 (&x)[M], const SRow<M> &r, const Ss
         if (c >= 0) pos += t;
         else neg += t;
     }
-    const u64 v = ssn_submod(fold64(pos, f), fold64(neg, f), f.p);
-    return r.one ? v : mulmod_pm(v, r.dinv, f);
+    const u64 v = lz(pos) + (4 * PP - lz(neg));           // < 2^48
+    return r.one ? lz(v) : mulm(v, r.dinv);
 }
 
-// share of s at rank t: s + sum_e c_e * id_t^(e+1)
+// share of s (< 2^48) at rank t: s + sum_e c_e * id_t^(e+1), lazy
 template <int K, int N>
-__device__ __forceinline__ u64 share_at(u64 s, const u64 (&c)[K - 1], const STables<K, N> &tb, int t,
-                                        const SsnField &f) {
+__device__ __forceinline__ u64 share_at(u64 s, const u64 (&c)[K - 1], const STables<K, N> &tb, int t) {
     u64 acc = s;
 #pragma unroll
     for (int e = 0; e < K - 1; e++) acc += mul_small(c[e], tb.pw[t][e]);
-    return fold64(acc, f);
+    return lz(acc);
 }
 
-// K-1 uniform field elements (masked 64-bit Philox words; p is 2^-39 close to 2^45)
+// K-1 uniform field elements: masked 45-bit Philox words.  Values in [p, 2^45) are lazy
+// representatives of [0, 55), exactly the distribution of the conditional-subtract form.
 template <int K>
-__device__ __forceinline__ void coeffs(u64 (&c)[K - 1], u64 seed, u64 stream, u64 i, const SsnField &f) {
+__device__ __forceinline__ void coeffs(u64 (&c)[K - 1], u64 seed, u64 stream, u64 i) {
 #pragma unroll
     for (int jp = 0; jp < K / 2; jp++) {
         const ssn_u4 r = ssn_philox_at(seed, stream, i, 0x800u | jp);
-        u64 x0 = (((u64)r.x << 32) | r.y) & f.mask;
-        u64 x1 = (((u64)r.z << 32) | r.w) & f.mask;
-        if (x0 >= f.p) x0 -= f.p;
-        if (x1 >= f.p) x1 -= f.p;
-        c[2 * jp] = x0;
-        if (2 * jp + 1 < K - 1) c[2 * jp + 1] = x1;
+        c[2 * jp] = (((u64)r.x << 32) | r.y) & PMASK;
+        if (2 * jp + 1 < K - 1) c[2 * jp + 1] = (((u64)r.z << 32) | r.w) & PMASK;
     }
+}
+
+// elite truncation of the reconstructed masked value (ssn_trunc_value, specialised)
+__device__ __forceinline__ u64 trunc_val(u64 v, const ChainArgs &a) {
+    const i64 shifted = (i64)addm(v, a.neglo_mod) + a.lo;
+    i64 t = a.rshift >= 0 ? (shifted >> a.rshift) : ssn_floordiv(shifted, a.r);
+    if (a.d > 1) {
+        const i64 q = ((t < 0 ? -t : t) * 2 + a.d) / (2 * a.d);
+        t = t < 0 ? -q : q;
+    }
+    if (t >= 0) return red64((u64)t);
+    const u64 mneg = red64((u64)(-t));
+    return mneg ? PP - mneg : 0;
 }
 
 // reshare + rerand + bias + truncation (+ residual add) of element i for all N parties.
 template <int K, int N>
 __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, N> &tb, uint32_t i, u64 (&x)[N],
-                                           unsigned long long &bad, const SsnField &f) {
+                                           unsigned long long &bad) {
     constexpr int M = 2 * K - 1;
     u64 acc[M];
 #pragma unroll
@@ -126,19 +177,19 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
 #pragma unroll
     for (int j = 0; j < M; j++) {
         u64 c[K - 1];
-        coeffs<K>(c, a.pseed, a.pstream + j, i, f);
+        coeffs<K>(c, a.pseed, a.pstream + j, i);
 #pragma unroll
-        for (int fr = 0; fr < K; fr++) sub[fr][j] = share_at<K, N>(acc[j], c, tb, fr, f);
+        for (int fr = 0; fr < K; fr++) sub[fr][j] = share_at<K, N>(acc[j], c, tb, fr);
     }
     // source: zero shares (gen_zero_shares) and the truncation masks (gen_additive_mask)
     u64 z[K - 1], ca[K - 1], cc[K - 1];
-    coeffs<K>(z, a.sseed, a.sstream + 0, i, f);
+    coeffs<K>(z, a.sseed, a.sstream + 0, i);
     const u64 e = 1 + ssn_rand_range(a.sseed, a.sstream + 1, i, 0, a.emax);
-    const u64 em = fold64(e, f);
-    const u64 alpha = mulmod_pm(em, a.stepm, f);
-    const u64 comp = em ? f.p - em : 0;
-    coeffs<K>(ca, a.sseed, a.sstream + 2, i, f);
-    coeffs<K>(cc, a.sseed, a.sstream + 3, i, f);
+    const u64 em = red64(e);
+    const u64 alpha = mulm(em, a.stepm);
+    const u64 comp = em ? PP - em : 0;
+    coeffs<K>(ca, a.sseed, a.sstream + 2, i);
+    coeffs<K>(cc, a.sseed, a.sstream + 3, i);
     const uint32_t ch = (i / a.bias_div) % a.bias_mod;
     // ---- step 2 (RESHARE_BACK): front fr applies R^T; step 3: out rank t reconstructs,
     //      + zero share (rerand) + bias share, then + alpha share (TRUNC_MASKED)
@@ -148,66 +199,64 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
         if (t < a.senders) {
             u64 back[K];
 #pragma unroll
-            for (int fr = 0; fr < K; fr++) back[fr] = lin<M>(sub[fr], tb.rt[t], f);
-            u64 y = lin<K>(back, tb.wf, f);
-            y = ssn_addmod(y, share_at<K, N>(0, z, tb, t, f), f.p);
-            y = ssn_addmod(y, a.bias[(u64)t * a.bias_ps + ch], f.p);
-            if (t == a.fault_rank && i == 0) y = ssn_addmod(y, 1, f.p);                   // test hook
-            masked[t] = ssn_addmod(y, share_at<K, N>(alpha, ca, tb, t, f), f.p);
+            for (int fr = 0; fr < K; fr++) back[fr] = lin<M>(sub[fr], tb.rt[t]);
+            u64 y = lin<K>(back, tb.wf) + share_at<K, N>(0, z, tb, t) + a.bias[(u64)t * a.bias_ps + ch];
+            if (t == a.fault_rank && i == 0) y += 1;                                        // test hook
+            masked[t] = lz(y + share_at<K, N>(alpha, ca, tb, t));
         }
     }
     // ---- truncation elite: rec over the front, RS check of the extra points, decode/floor/round
     u64 front[K];
 #pragma unroll
     for (int j = 0; j < K; j++) front[j] = masked[j];
-    const u64 v = lin<K>(front, tb.wf, f);
+    const u64 v = canon(lin<K>(front, tb.wf));
 #pragma unroll
     for (int t = K; t < N; t++)
-        if (t < a.senders) bad += (lin<K>(front, tb.ext[t], f) != masked[t]);
-    const u64 tm = ssn_trunc_value(v, a.lo, a.neglo_mod, a.r, a.rshift, a.d, f);
+        if (t < a.senders) bad += (canon(lin<K>(front, tb.ext[t])) != canon(masked[t]));
+    const u64 tm = trunc_val(v, a);
     // fresh (k, n) shares of the truncated value (SHARE_DIST), + comp at every rank
     u64 g[K - 1];
-    coeffs<K>(g, a.pseed, a.pstream + M, i, f);
+    coeffs<K>(g, a.pseed, a.pstream + M, i);
 #pragma unroll
     for (int t = 0; t < N; t++) {
-        u64 s = ssn_addmod(share_at<K, N>(tm, g, tb, t, f), share_at<K, N>(comp, cc, tb, t, f), f.p);
-        if (a.other) s = ssn_addmod(s, a.other[(u64)t * a.other_ps + i], f.p);         // residual add
-        x[t] = s;
+        u64 s = share_at<K, N>(tm, g, tb, t) + share_at<K, N>(comp, cc, tb, t);
+        if (a.other) s += a.other[(u64)t * a.other_ps + i];                              // residual add
+        x[t] = lz(s);                                                                   // lazy
     }
 }
 
 template <int K, int N>
-__global__ void __launch_bounds__(128) k_chain_plain(ChainArgs a, const __grid_constant__ STables<K, N> tb,
+__global__ void __launch_bounds__(CHAIN_THREADS) k_chain_plain(ChainArgs a, const __grid_constant__ STables<K, N> tb,
                                                      SsnField f) {
     unsigned long long bad = 0;
     const uint32_t nel = (uint32_t)a.nel;
 #pragma unroll 1
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nel; i += gridDim.x * blockDim.x) {
         u64 x[N];
-        chain_elem<K, N>(a, tb, i, x, bad, f);
+        chain_elem<K, N>(a, tb, i, x, bad);
 #pragma unroll
-        for (int t = 0; t < N; t++) a.out[(u64)t * a.out_ps + i] = x[t];
+        for (int t = 0; t < N; t++) a.out[(u64)t * a.out_ps + i] = canon(x[t]);
     }
     if (a.fail && bad) atomicAdd(a.fail, bad);
 }
 
 // exclusive prefix (up) / suffix (down) products across the warp; inactive lanes hold 1
-__device__ __forceinline__ u64 warp_excl_prefix(u64 v, int lane, const SsnField &f) {
+__device__ __forceinline__ u64 warp_excl_prefix(u64 v, int lane) {
     u64 incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const u64 t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl = mulmod_pm(incl, t, f);
+        if (lane >= o) incl = mulm(incl, t);
     }
     const u64 ex = __shfl_up_sync(0xffffffffu, incl, 1);
     return lane ? ex : 1;
 }
-__device__ __forceinline__ u64 warp_excl_suffix(u64 v, int lane, const SsnField &f) {
+__device__ __forceinline__ u64 warp_excl_suffix(u64 v, int lane) {
     u64 incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const u64 t = __shfl_down_sync(0xffffffffu, incl, o);
-        if (lane + o < 32) incl = mulmod_pm(incl, t, f);
+        if (lane + o < 32) incl = mulm(incl, t);
     }
     const u64 ex = __shfl_down_sync(0xffffffffu, incl, 1);
     return lane < 31 ? ex : 1;
@@ -215,17 +264,19 @@ __device__ __forceinline__ u64 warp_excl_suffix(u64 v, int lane, const SsnField 
 
 // masked nonlinearity fused after the chain: one thread per output window.
 template <int K, int N>
-__global__ void __launch_bounds__(128) k_chain_nonlin(ChainArgs a, const __grid_constant__ STables<K, N> tb,
-                                                      SsnField f) {
+__global__ void __launch_bounds__(CHAIN_THREADS) k_chain_nonlin(ChainArgs a, const __grid_constant__ STables<K, N> tb,
+                                                                SsnField f) {
     constexpr int M = 2 * K - 1;
+    __shared__ u64 s_warp[CHAIN_WARPS];
+    __shared__ u64 s_inv;
     unsigned long long bad = 0;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t oh = a.h / a.kh, ow = a.w / a.kw;
     const uint32_t hw = oh * ow, chw = (uint32_t)a.c * hw;
     const uint32_t n_out = (uint32_t)a.nb * chw;
     const bool pooled = a.kh != 1 || a.kw != 1;
 #pragma unroll 1
-    for (uint32_t base = blockIdx.x * blockDim.x; base < n_out; base += gridDim.x * blockDim.x) {
+    for (uint32_t base = blockIdx.x * CHAIN_THREADS; base < n_out; base += gridDim.x * CHAIN_THREADS) {
         const uint32_t o = base + threadIdx.x;
         const bool live = o < n_out;
         u64 plain = 0, beta = 1;
@@ -245,34 +296,46 @@ __global__ void __launch_bounds__(128) k_chain_nonlin(ChainArgs a, const __grid_
                 for (int wx = 0; wx < a.kw; wx++) {
                     const uint32_t i = base_in + wy * a.w + wx;
                     u64 x[N];
-                    chain_elem<K, N>(a, tb, i, x, bad, f);
+                    chain_elem<K, N>(a, tb, i, x, bad);
                     // participants mask with their beta shares (NONLIN_MASKED); elite rec over m
                     u64 cb[K - 1];
-                    coeffs<K>(cb, a.sseed, a.sstream + 5, i, f);
+                    coeffs<K>(cb, a.sseed, a.sstream + 5, i);
                     u64 mk[M];
 #pragma unroll
-                    for (int j = 0; j < M; j++) mk[j] = mulmod_pm(x[j], share_at<K, N>(beta, cb, tb, j, f), f);
-                    const u64 v = lin<M>(mk, tb.wp, f);
-                    i64 sv = v > f.half ? (i64)v - (i64)f.p : (i64)v;
+                    for (int j = 0; j < M; j++) mk[j] = mulm(x[j], share_at<K, N>(beta, cb, tb, j));
+                    const u64 v = canon(lin<M>(mk, tb.wp));
+                    i64 sv = v > PHALF ? (i64)v - (i64)PP : (i64)v;
                     if (a.relu && sv <= 0) sv = 0;
                     if (a.pool_kind == 1) acc = sv > acc ? sv : acc;
                     else acc += sv;
                 }
-            plain = acc < 0 ? (u64)((i64)f.p + acc) : (u64)acc;                  // encode_signed (NONLIN_PLAIN)
+            plain = acc < 0 ? (u64)((i64)PP + acc) : (u64)acc;                   // encode_signed (NONLIN_PLAIN)
         }
-        // source: beta^-1 per window -- one inversion per warp (prefix/suffix products)
-        const u64 pre = warp_excl_prefix(beta, lane, f);
-        const u64 suf = warp_excl_suffix(beta, lane, f);
-        const u64 all = __shfl_sync(0xffffffffu, mulmod_pm(pre, beta, f), 31);
-        const u64 inv_all = ssn_powmod(all, f.p - 2, f);
-        const u64 binv = mulmod_pm(mulmod_pm(pre, suf, f), inv_all, f);
+        // source: beta^-1 per window -- Montgomery batch inversion over the block's windows
+        // (warp-shuffle prefix/suffix products, one Fermat inversion per block)
+        const u64 pre = warp_excl_prefix(beta, lane);
+        const u64 suf = warp_excl_suffix(beta, lane);
+        if (lane == 31) s_warp[warp] = mulm(pre, beta);
+        __syncthreads();
+        u64 before = 1, after = 1, total = 1;
+#pragma unroll
+        for (int w2 = 0; w2 < CHAIN_WARPS; w2++) {
+            const u64 wv = s_warp[w2];
+            if (w2 < warp) before = mulm(before, wv);
+            if (w2 > warp) after = mulm(after, wv);
+            total = mulm(total, wv);
+        }
+        if (threadIdx.x == 0) s_inv = invm(total);
+        __syncthreads();
+        const u64 binv = mulm(mulm(mulm(before, after), mulm(pre, suf)), s_inv);
         if (live) {
             u64 cbi[K - 1];
-            coeffs<K>(cbi, a.sseed, a.sstream + 6, o, f);
+            coeffs<K>(cbi, a.sseed, a.sstream + 6, o);
 #pragma unroll
             for (int t = 0; t < N; t++)
-                if (t < a.fan) a.out[(u64)t * a.out_ps + o] = mulmod_pm(plain, share_at<K, N>(binv, cbi, tb, t, f), f);
+                if (t < a.fan) a.out[(u64)t * a.out_ps + o] = canon(mulm(plain, share_at<K, N>(binv, cbi, tb, t)));
         }
+        __syncthreads();                       // s_warp / s_inv reuse in the next iteration
     }
     if (a.fail && bad) atomicAdd(a.fail, bad);
 }
@@ -306,7 +369,7 @@ template <int K, int N>
 int build_tables(STables<K, N> &tb, const u64 *ids, const u64 *rt, const u64 *ext, u64 p) {
     constexpr int M = 2 * K - 1;
     const SsnField f = ssn_make_field(p);
-    if (!f.pm || !f.near) return 0;
+    if (p != PP || !f.pm || !f.near) return 0;      // kernels are specialised to the default prime
     int ok = 1;
     u64 row[SSN_MAXJ];
     lagrange0(row, ids, K, p);
