@@ -6,8 +6,9 @@
 // int32 accumulators in TMEM, one per limb diagonal d = i + j:
 //       D_d = sum_{i+j=d} A_i(128 x K) . B_j(32 x K)^T          (exact: <= L*K*255^2 < 2^32)
 // fed by TMA (4-D tensor maps over [party][limb][row][K], 64-byte swizzle) through a
-// 3-stage mbarrier pipeline; one elected thread issues the L^2 tcgen05.mma per 32-wide K
-// slice.  The epilogue reads TMEM (tcgen05.ld), recombines sum_d D_d * (2^(8d) mod p) in
+// 3-stage mbarrier pipeline; one elected thread issues, per 32-wide K slice, L tcgen05.mma
+// of 128 x (L*32) x 32 -- A limb i against all B limbs stacked along N, written at TMEM
+// column offset 32*i so each limb product lands on its diagonal.  The epilogue reads TMEM (tcgen05.ld), recombines sum_d D_d * (2^(8d) mod p) in
 // 128-bit registers and reduces mod p (Barrett), writing canonical u64 shares straight into
 // the [party][img][O][OH*OW] layout the protocol kernels consume.
 //
@@ -26,7 +27,8 @@ constexpr int BM = 128;        // UMMA_M: rows per tile
 constexpr int BN = 32;         // UMMA_N: output channels per tile
 constexpr int BK = 64;         // bytes of K per pipeline stage (= one 64B swizzle atom row)
 constexpr int UK = 32;         // K per tcgen05.mma.kind::i8
-constexpr int STAGES = 3;
+constexpr int STAGES_MAX = 3;
+template <int L> __host__ __device__ constexpr int stages_for() { return L >= 8 ? 2 : STAGES_MAX; }   // 227 KB smem cap
 constexpr int MAXL = 8;
 
 struct CdTable { u64 c[2 * MAXL - 1]; };
@@ -71,15 +73,18 @@ __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
     return d;
 }
 
-// instruction descriptor: D=S32, A=B=U8, K-major both, N=BN, M=BM
-constexpr uint32_t kIdesc = (2u << 4) | ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+// instruction descriptor: D=S32, A=B=U8, K-major both, M=BM, N=n
+__host__ __device__ constexpr uint32_t idesc_i8(int n) {
+    return (2u << 4) | ((uint32_t)(n >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
 
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accumulate) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.b32 p, %4, 0;\n\t"
         "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}"
-        ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(kIdesc), "r"(accumulate));
+        ::"r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
 
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
@@ -115,6 +120,7 @@ __global__ void __launch_bounds__(128, 1)
 k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, u64 *__restrict__ out,
           u64 out_pstride, u64 ohw, int O, int M, int nkb, SsnField f, u64 r64, CdTable cd) {
     constexpr int ND = 2 * L - 1;
+    constexpr int STAGES = stages_for<L>();
     constexpr int A_BYTES = L * BM * BK;
     constexpr int B_BYTES = L * BN * BK;
     constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -157,7 +163,13 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             tma_load_4d(sa + A_BYTES, &tmB, &full[s], kb * BK, n0, 0, party);
         }
     } else if (warp == 1 && lane == 0) {
-        // ---- MMA issuer: L^2 limb products per 32-wide K slice into 2L-1 diagonal accumulators ----
+        // ---- MMA issuer.  The L limb planes of B sit back to back in shared memory, so one
+        // MMA with N = L*BN multiplies A limb i by ALL B limbs at once; writing its D at TMEM
+        // column i*BN lands the product with B limb j on column block (i+j)*BN -- exactly the
+        // limb diagonal d = i+j.  L MMAs of 128 x L*BN x 32 per K slice instead of L^2 of
+        // 128 x BN x 32.  On the very first K slice diagonals >= L are not yet written, so
+        // A limb i >= 1 splits into an accumulating N=(L-1)*BN part and a fresh N=BN part.
+        constexpr uint32_t ID_ALL = idesc_i8(L * BN), ID_HEAD = idesc_i8((L - 1) * BN), ID_ONE = idesc_i8(BN);
         for (int kb = 0; kb < nkb; kb++) {
             const int s = kb % STAGES;
             const uint32_t ph = (kb / STAGES) & 1;
@@ -167,14 +179,20 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
             const uint32_t sb = sa + A_BYTES;
 #pragma unroll 1
             for (int kk = 0; kk < BK / UK; kk++) {
+                const uint64_t bdesc = umma_desc_sw64(sb + kk * UK);
+                const bool first = kb == 0 && kk == 0;
 #pragma unroll 1
                 for (int i = 0; i < L; i++) {
                     const uint64_t adesc = umma_desc_sw64(sa + i * BM * BK + kk * UK);
-#pragma unroll
-                    for (int j = 0; j < L; j++) {
-                        const uint64_t bdesc = umma_desc_sw64(sb + j * BN * BK + kk * UK);
-                        const uint32_t first = (kb == 0 && kk == 0 && (i == 0 || j == L - 1));
-                        mma_i8(tmem + (uint32_t)((i + j) * BN), adesc, bdesc, first ? 0u : 1u);
+                    const uint32_t d = tmem + (uint32_t)(i * BN);
+                    if (!first) {
+                        mma_i8(d, adesc, bdesc, ID_ALL, 1u);
+                    } else if (i == 0) {
+                        mma_i8(d, adesc, bdesc, ID_ALL, 0u);
+                    } else {
+                        mma_i8(d, adesc, bdesc, ID_HEAD, 1u);
+                        mma_i8(d + (uint32_t)((L - 1) * BN), adesc,
+                               umma_desc_sw64(sb + (L - 1) * BN * BK + kk * UK), ID_ONE, 0u);
                     }
                 }
             }
@@ -264,7 +282,7 @@ int launch_tc(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int 
               u64 ohw, u64 p, cudaStream_t st) {
     CUtensorMap ma, mb;
     if (make_map(&ma, a, Kpad, M, L, nparty, BM) || make_map(&mb, b, Kpad, O, L, nparty, BN)) return SSN_ERR_CUDA;
-    constexpr int smem = STAGES * (L * BM * BK + L * BN * BK) + 1024 + 256;
+    constexpr int smem = stages_for<L>() * (L * BM * BK + L * BN * BK) + 1024 + 256;
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(k_gemm_tc<L>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
