@@ -252,6 +252,188 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
+// ============================================================================================
+// Persistent, warp-specialised variant for the default field p = 2^45 - 55 (L = 6 limbs).
+//   warp 0      TMA producer (4-stage smem ring, A 128x64x6 + B 16x64x6 bytes per stage)
+//   warp 1      TMEM allocator + MMA issuer: per 32-wide K slice, 6 MMAs of 128 x 96 x 32
+//   warps 2..5  epilogue: TMEM -> registers -> mod-p recombination -> HBM
+// The 11 limb-diagonal accumulators of a 128 x 16 tile take 176 TMEM columns, so two tiles
+// are in flight (TMEM buffers at columns 0 and 256): the epilogue of tile t overlaps the
+// MMAs of tile t+1.  Epilogue recombination is exact integer arithmetic specialised to p:
+//   g0 = sum_{d<4} D_d 2^{8d},  g1 = sum_{4<=d<8} D_d 2^{8(d-4)},  g2 = sum_{d>=8} D_d 2^{8(d-8)}
+//   (each one IMAD.WIDE per diagonal, all < 2^57), value = g0 + g1 2^32 + g2 2^64, folded with
+//   2^45 == 55 (mod p).
+namespace p45 {
+constexpr int L = 6;
+constexpr int BN2 = 16;                  // output channels per tile
+constexpr int ND = 2 * L - 1;            // 11 limb diagonals
+constexpr int ST = 4;                    // smem stages
+constexpr int A_BYTES = L * BM * BK;     // 49152
+constexpr int B_BYTES = L * BN2 * BK;    // 6144
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM = ST * STAGE_BYTES + 1024 + 256;
+constexpr int THREADS = 192;
+constexpr uint32_t TBUF = 256;           // TMEM column offset of the second accumulator buffer
+constexpr u64 P = (1ull << 45) - 55;
+constexpr u64 MASK45 = (1ull << 45) - 1;
+
+__device__ __forceinline__ u64 lz(u64 x) { return (x >> 45) * 55 + (x & MASK45); }
+
+// (g0 + g1*2^32 + g2*2^64) mod p for g0, g1 < 2^57, g2 < 2^49
+__device__ __forceinline__ u64 combine(u64 g0, u64 g1, u64 g2) {
+    const u64 x = lz(g1);                                   // < 2^46
+    const u64 t1 = (x >> 13) * 55 + ((x & 0x1FFF) << 32);   // x*2^32: (x>>13)*2^45 + (x&8191)*2^32
+    const u64 y = lz(g2);                                   // < 2^46
+    const u64 z = (y >> 26) * 55 + ((y & 0x3FFFFFF) << 19); // y*2^19
+    const u64 t = lz(g0) + t1 + z * 55;                     // y*2^64 == y*2^19*55;  < 2^52
+    const u64 r = lz(t);
+    return r >= P ? r - P : r;
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+k_gemm_p45(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, u64 *__restrict__ out,
+           u64 out_pstride, uint32_t ohw, int O, int M, int nkb, int ntm, int ntn, int ntiles) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *full = reinterpret_cast<uint64_t *>(base + ST * STAGE_BYTES);
+    uint64_t *empty = full + ST;
+    uint64_t *tfull = empty + ST;        // [2]
+    uint64_t *tempty = tfull + 2;        // [2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < ST; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---- TMA producer ----
+            int it = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int nt = t % ntn, mt = (t / ntn) % ntm, party = t / (ntn * ntm);
+                for (int kb = 0; kb < nkb; kb++, it++) {
+                    const int s = it % ST;
+                    mbar_wait(&empty[s], ((it / ST) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
+                    uint8_t *sa = base + s * STAGE_BYTES;
+                    tma_load_4d(sa, &tmA, &full[s], kb * BK, mt * BM, 0, party);
+                    tma_load_4d(sa + A_BYTES, &tmB, &full[s], kb * BK, nt * BN2, 0, party);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---- MMA issuer ----
+            constexpr uint32_t ID_ALL = idesc_i8(L * BN2), ID_HEAD = idesc_i8((L - 1) * BN2), ID_ONE = idesc_i8(BN2);
+            int it = 0, lt = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
+                const int buf = lt & 1;
+                mbar_wait(&tempty[buf], ((lt >> 1) & 1) ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t dbase = tmem + (uint32_t)buf * TBUF;
+                for (int kb = 0; kb < nkb; kb++, it++) {
+                    const int s = it % ST;
+                    mbar_wait(&full[s], (it / ST) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t sa = smem_u32(base + s * STAGE_BYTES);
+                    const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < BK / UK; kk++) {
+                        const uint64_t bdesc = umma_desc_sw64(sb + kk * UK);
+                        const bool first = kb == 0 && kk == 0;
+#pragma unroll
+                        for (int i = 0; i < L; i++) {
+                            const uint64_t adesc = umma_desc_sw64(sa + i * BM * BK + kk * UK);
+                            const uint32_t d = dbase + (uint32_t)(i * BN2);
+                            if (!first) {
+                                mma_i8(d, adesc, bdesc, ID_ALL, 1u);
+                            } else if (i == 0) {
+                                mma_i8(d, adesc, bdesc, ID_ALL, 0u);
+                            } else {
+                                mma_i8(d, adesc, bdesc, ID_HEAD, 1u);
+                                mma_i8(d + (uint32_t)((L - 1) * BN2), adesc,
+                                       umma_desc_sw64(sb + (L - 1) * BN2 * BK + kk * UK), ID_ONE, 0u);
+                            }
+                        }
+                    }
+                    mma_commit(&empty[s]);
+                }
+                mma_commit(&tfull[buf]);
+            }
+        }
+    } else {
+        // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4 ----
+        const int q = warp & 3;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        int lt = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
+            const int buf = lt & 1;
+            const int nt = t % ntn, mt = (t / ntn) % ntm, party = t / (ntn * ntm);
+            mbar_wait(&tfull[buf], (lt >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t taddr = tmem + lane_off + (uint32_t)buf * TBUF;
+            u64 g[3][BN2];
+#pragma unroll
+            for (int grp = 0; grp < 3; grp++) {
+                uint32_t r[4][16];
+#pragma unroll
+                for (int dd = 0; dd < 4; dd++)
+                    if (grp * 4 + dd < ND) {
+                        asm volatile(
+                            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                            : "=r"(r[dd][0]), "=r"(r[dd][1]), "=r"(r[dd][2]), "=r"(r[dd][3]), "=r"(r[dd][4]),
+                              "=r"(r[dd][5]), "=r"(r[dd][6]), "=r"(r[dd][7]), "=r"(r[dd][8]), "=r"(r[dd][9]),
+                              "=r"(r[dd][10]), "=r"(r[dd][11]), "=r"(r[dd][12]), "=r"(r[dd][13]), "=r"(r[dd][14]),
+                              "=r"(r[dd][15])
+                            : "r"(taddr + (uint32_t)((grp * 4 + dd) * BN2)));
+                    }
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int c = 0; c < BN2; c++) {
+                    u64 acc = 0;
+#pragma unroll
+                    for (int dd = 0; dd < 4; dd++)
+                        if (grp * 4 + dd < ND) acc += (u64)r[dd][c] << (8 * dd);
+                    g[grp][c] = acc;
+                }
+            }
+            // TMEM buffer drained: hand it back to the MMA warp before the stores
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
+            const int row = mt * BM + q * 32 + lane;
+            if (row < M) {
+                const uint32_t img = (uint32_t)row / ohw, pix = (uint32_t)row - img * ohw;
+                u64 *ob = out + (u64)party * out_pstride + ((u64)img * O + (u64)nt * BN2) * ohw + pix;
+#pragma unroll
+                for (int c = 0; c < BN2; c++)
+                    if (nt * BN2 + c < O) ob[(u64)c * ohw] = combine(g[0][c], g[1][c], g[2][c]);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+}  // namespace p45
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -299,6 +481,33 @@ int launch_tc(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int 
     u64 r64 = (u64)((((unsigned __int128)1) << 64) % p);
     dim3 grid((O + BN - 1) / BN, (M + BM - 1) / BM, nparty);
     k_gemm_tc<L><<<grid, 128, smem, st>>>(ma, mb, out, out_pstride, ohw, O, M, (Kpad + BK - 1) / BK, f, r64, cd);
+    return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
+}
+
+int launch_p45(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int Kpad, u64 *out, u64 out_pstride,
+               u64 ohw, cudaStream_t st) {
+    using namespace p45;
+    CUtensorMap ma, mb;
+    if (make_map(&ma, a, Kpad, M, L, nparty, BM) || make_map(&mb, b, Kpad, O, L, nparty, BN2)) return SSN_ERR_CUDA;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_gemm_p45, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
+            return SSN_ERR_CUDA;
+        attr = true;
+    }
+    if (ohw >= (1ull << 32) || (u64)M * 1 >= (1ull << 31)) return SSN_ERR_UNSUPPORTED;
+    const int ntm = (M + BM - 1) / BM, ntn = (O + BN2 - 1) / BN2;
+    const long long ntiles = (long long)ntm * ntn * nparty;
+    if (ntiles >= (1ll << 31)) return SSN_ERR_UNSUPPORTED;
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int grid = (int)(ntiles < nsm ? ntiles : nsm);
+    k_gemm_p45<<<grid, THREADS, SMEM, st>>>(ma, mb, out, out_pstride, (uint32_t)ohw, O, M, (Kpad + BK - 1) / BK, ntm,
+                                            ntn, (int)ntiles);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
 
@@ -414,6 +623,7 @@ extern "C" int ssn_gemm_tc(const uint8_t *a_planes, const uint8_t *b_planes, int
     if (L < 1 || L > MAXL || Kpad % 16 || M < 1 || O < 1 || nparty < 1 || ohw < 1) return SSN_ERR_ARG;
     if ((unsigned __int128)L * Kpad * 65025 >= ((unsigned __int128)1 << 32)) return SSN_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
+    if (L == 6 && p == p45::P && M >= BM) return launch_p45(a_planes, b_planes, nparty, M, O, (int)Kpad, out, out_pstride, ohw, st);
     switch (L) {
         case 6: return launch_tc<6>(a_planes, b_planes, nparty, M, O, (int)Kpad, out, out_pstride, ohw, p, st);
         case 7: return launch_tc<7>(a_planes, b_planes, nparty, M, O, (int)Kpad, out, out_pstride, ohw, p, st);
