@@ -34,7 +34,8 @@ namespace {
 
 template <int M>
 struct SRow {            // sum_j n[j] x_j / D  (dinv = D^-1 mod p, one = (D == 1))
-    int32_t n[M];
+    uint32_t nn[M];      // n[j] + off >= 0 (< 2^14): sum_j n_j x_j = sum_j nn_j x_j - off * sum_j x_j
+    uint32_t off;
     int32_t one;
     u64 dinv;
 };
@@ -69,7 +70,8 @@ struct ChainArgs {
     int fault_rank;
 };
 
-constexpr int CHAIN_THREADS = 128;
+constexpr int CHAIN_THREADS = 256;   // nonlin: beta^-1 batch-inverted over the block
+constexpr int PLAIN_THREADS = 128;
 constexpr int CHAIN_WARPS = CHAIN_THREADS / 32;
 
 // ---- arithmetic in the default field p = 2^45 - 55 (S/field.py:21) with compile-time fold
@@ -115,19 +117,33 @@ __device__ __noinline__ u64 invm(u64 x) {
     return mulm(sqn(x39, 6), x7);
 }
 
-// sum_j n_j x_j / D for lazy x_j (< 2^47): |n_j| < 2^13 keeps pos/neg below 2^63 for M <= 7
+// sum_j n_j x_j / D for lazy x_j (< 2^46), |n_j| < 2^13, M <= 7.  With non-negative
+// nn_j = n_j + off the products split into 32-bit halves: sum nn_j lo_j (< 2^49, one
+// IMAD.WIDE each) + (sum nn_j hi_j) << 32 (hi < 2^14, < 2^31) -- then subtract off * sum x_j.
 template <int M>
-__device__ __forceinline__ u64 lin(const u64 (&x)[M], const SRow<M> &r) {
-    u64 pos = 0, neg = 0;
+__device__ __forceinline__ u64 lin_s(const u64 (&x)[M], u64 xsum, const SRow<M> &r) {
+    u64 lo = 0;
+    uint32_t hi = 0;
 #pragma unroll
     for (int j = 0; j < M; j++) {
-        const int32_t c = r.n[j];
-        const u64 t = mul_small(x[j], (uint32_t)(c >= 0 ? c : -c));
-        if (c >= 0) pos += t;
-        else neg += t;
+        lo += (u64)(uint32_t)x[j] * r.nn[j];
+        hi += (uint32_t)(x[j] >> 32) * r.nn[j];
     }
+    const u64 pos = lo + ((u64)hi << 32);                 // < 2^64
+    const u64 neg = mul_small(xsum, r.off);               // < 2^62
     const u64 v = lz(pos) + (4 * PP - lz(neg));           // < 2^48
     return r.one ? lz(v) : mulm(v, r.dinv);
+}
+template <int M>
+__device__ __forceinline__ u64 xsum_of(const u64 (&x)[M]) {
+    u64 s = 0;
+#pragma unroll
+    for (int j = 0; j < M; j++) s += x[j];
+    return s;
+}
+template <int M>
+__device__ __forceinline__ u64 lin(const u64 (&x)[M], const SRow<M> &r) {
+    return lin_s<M>(x, xsum_of<M>(x), r);
 }
 
 // share of s (< 2^48) at rank t: s + sum_e c_e * id_t^(e+1), lazy
@@ -181,6 +197,9 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
 #pragma unroll
         for (int fr = 0; fr < K; fr++) sub[fr][j] = share_at<K, N>(acc[j], c, tb, fr);
     }
+    u64 subsum[K];
+#pragma unroll
+    for (int fr = 0; fr < K; fr++) subsum[fr] = xsum_of<M>(sub[fr]);
     // source: zero shares (gen_zero_shares) and the truncation masks (gen_additive_mask)
     u64 z[K - 1], ca[K - 1], cc[K - 1];
     coeffs<K>(z, a.sseed, a.sstream + 0, i);
@@ -199,7 +218,7 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
         if (t < a.senders) {
             u64 back[K];
 #pragma unroll
-            for (int fr = 0; fr < K; fr++) back[fr] = lin<M>(sub[fr], tb.rt[t]);
+            for (int fr = 0; fr < K; fr++) back[fr] = lin_s<M>(sub[fr], subsum[fr], tb.rt[t]);
             u64 y = lin<K>(back, tb.wf) + share_at<K, N>(0, z, tb, t) + a.bias[(u64)t * a.bias_ps + ch];
             if (t == a.fault_rank && i == 0) y += 1;                                        // test hook
             masked[t] = lz(y + share_at<K, N>(alpha, ca, tb, t));
@@ -226,7 +245,7 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
 }
 
 template <int K, int N>
-__global__ void __launch_bounds__(CHAIN_THREADS) k_chain_plain(ChainArgs a, const __grid_constant__ STables<K, N> tb,
+__global__ void __launch_bounds__(PLAIN_THREADS, 4) k_chain_plain(ChainArgs a, const __grid_constant__ STables<K, N> tb,
                                                      SsnField f) {
     unsigned long long bad = 0;
     const uint32_t nel = (uint32_t)a.nel;
@@ -264,7 +283,7 @@ __device__ __forceinline__ u64 warp_excl_suffix(u64 v, int lane) {
 
 // masked nonlinearity fused after the chain: one thread per output window.
 template <int K, int N>
-__global__ void __launch_bounds__(CHAIN_THREADS) k_chain_nonlin(ChainArgs a, const __grid_constant__ STables<K, N> tb,
+__global__ void __launch_bounds__(CHAIN_THREADS, 2) k_chain_nonlin(ChainArgs a, const __grid_constant__ STables<K, N> tb,
                                                                 SsnField f) {
     constexpr int M = 2 * K - 1;
     __shared__ u64 s_warp[CHAIN_WARPS];
@@ -346,7 +365,11 @@ static int make_srow(SRow<MM> &s, const u64 *w, int m, u64 p) {
     u64 row[SSN_MAXJ] = {0};
     for (int j = 0; j < m; j++) row[j] = w[j];
     const int ok = make_row(r, row, m, p);
-    for (int j = 0; j < MM; j++) s.n[j] = j < m ? r.n[j] : 0;
+    int32_t off = 0;
+    for (int j = 0; j < m; j++)
+        if (-r.n[j] > off) off = -r.n[j];
+    for (int j = 0; j < MM; j++) s.nn[j] = j < m ? (uint32_t)(r.n[j] + off) : 0;
+    s.off = (uint32_t)off;
     s.one = r.one;
     s.dinv = r.dinv;
     return ok;
@@ -440,15 +463,15 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
     a.fault_rank = d->fault_rank;
     if (a.senders > a.nout) return SSN_ERR_ARG;
     if (!d->nonlin) {
-        u64 blocks = (a.nel + 127) / 128;
+        u64 blocks = (a.nel + PLAIN_THREADS - 1) / PLAIN_THREADS;
         if (blocks > 148ull * 16) blocks = 148ull * 16;
-        k_chain_plain<K, N><<<(unsigned)blocks, 128, 0, st>>>(a, tb, f);
+        k_chain_plain<K, N><<<(unsigned)blocks, PLAIN_THREADS, 0, st>>>(a, tb, f);
     } else {
         const u64 n_out = (u64)d->nb * d->c * (d->h / d->kh) * (d->w / d->kw);
-        u64 blocks = (n_out + 127) / 128;
+        u64 blocks = (n_out + CHAIN_THREADS - 1) / CHAIN_THREADS;
         if (blocks > 148ull * 16) blocks = 148ull * 16;
         if (blocks < 1) blocks = 1;
-        k_chain_nonlin<K, N><<<(unsigned)blocks, 128, 0, st>>>(a, tb, f);
+        k_chain_nonlin<K, N><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a, tb, f);
     }
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
