@@ -70,7 +70,7 @@ struct ChainArgs {
     int fault_rank;
 };
 
-constexpr int CHAIN_THREADS = 256;   // nonlin: beta^-1 batch-inverted over the block
+constexpr int CHAIN_THREADS = 128;
 constexpr int PLAIN_THREADS = 128;
 constexpr int CHAIN_WARPS = CHAIN_THREADS / 32;
 
@@ -281,80 +281,87 @@ __device__ __forceinline__ u64 warp_excl_suffix(u64 v, int lane) {
     return lane < 31 ? ex : 1;
 }
 
-// masked nonlinearity fused after the chain: one thread per output window.
+// masked nonlinearity fused after the chain: one thread per output window, WPT windows per
+// thread (a block-stride apart, coalesced).  beta^-1 of all 32*WPT windows of a warp comes
+// from ONE Fermat inversion: per-thread running products over its WPT windows, warp-shuffle
+// exclusive prefix/suffix products across lanes (Montgomery's batch trick), then a backward
+// pass.  No block barrier: warps never wait for each other.
+constexpr int WPT = 4;
+
 template <int K, int N>
-__global__ void __launch_bounds__(CHAIN_THREADS, 2) k_chain_nonlin(ChainArgs a, const __grid_constant__ STables<K, N> tb,
+__global__ void __launch_bounds__(CHAIN_THREADS, 4) k_chain_nonlin(ChainArgs a, const __grid_constant__ STables<K, N> tb,
                                                                 SsnField f) {
     constexpr int M = 2 * K - 1;
-    __shared__ u64 s_warp[CHAIN_WARPS];
-    __shared__ u64 s_inv;
     unsigned long long bad = 0;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
     const uint32_t oh = a.h / a.kh, ow = a.w / a.kw;
     const uint32_t hw = oh * ow, chw = (uint32_t)a.c * hw;
     const uint32_t n_out = (uint32_t)a.nb * chw;
     const bool pooled = a.kh != 1 || a.kw != 1;
+    const uint32_t span = CHAIN_THREADS * WPT;
 #pragma unroll 1
-    for (uint32_t base = blockIdx.x * CHAIN_THREADS; base < n_out; base += gridDim.x * CHAIN_THREADS) {
-        const uint32_t o = base + threadIdx.x;
-        const bool live = o < n_out;
-        u64 plain = 0, beta = 1;
-        if (live) {
-            beta = 1 + ssn_rand_range(a.sseed, a.sstream + 4, o, 0, a.bmax);     // window-constant beta
-            uint32_t base_in = o;
-            if (pooled) {
-                const uint32_t img = o / chw, rem = o - img * chw;
-                const uint32_t ci = rem / hw, rr = rem - ci * hw;
-                const uint32_t y0 = rr / ow, x0 = rr - y0 * ow;
-                base_in = ((img * a.c + ci) * a.h + y0 * a.kh) * a.w + x0 * a.kw;
-            }
-            i64 acc = a.pool_kind == 1 ? INT64_MIN : 0;
+    for (uint32_t base = blockIdx.x * span; base < n_out; base += gridDim.x * span) {
+        u64 plain[WPT], beta[WPT], pre[WPT];
+        u64 run = 1;
 #pragma unroll 1
-            for (int wy = 0; wy < a.kh; wy++)
-#pragma unroll 1
-                for (int wx = 0; wx < a.kw; wx++) {
-                    const uint32_t i = base_in + wy * a.w + wx;
-                    u64 x[N];
-                    chain_elem<K, N>(a, tb, i, x, bad);
-                    // participants mask with their beta shares (NONLIN_MASKED); elite rec over m
-                    u64 cb[K - 1];
-                    coeffs<K>(cb, a.sseed, a.sstream + 5, i);
-                    u64 mk[M];
-#pragma unroll
-                    for (int j = 0; j < M; j++) mk[j] = mulm(x[j], share_at<K, N>(beta, cb, tb, j));
-                    const u64 v = canon(lin<M>(mk, tb.wp));
-                    i64 sv = v > PHALF ? (i64)v - (i64)PP : (i64)v;
-                    if (a.relu && sv <= 0) sv = 0;
-                    if (a.pool_kind == 1) acc = sv > acc ? sv : acc;
-                    else acc += sv;
+        for (int q = 0; q < WPT; q++) {
+            const uint32_t o = base + q * CHAIN_THREADS + threadIdx.x;
+            u64 pl = 0, bt = 1;
+            if (o < n_out) {
+                bt = 1 + ssn_rand_range(a.sseed, a.sstream + 4, o, 0, a.bmax);     // window-constant beta
+                uint32_t base_in = o;
+                if (pooled) {
+                    const uint32_t img = o / chw, rem = o - img * chw;
+                    const uint32_t ci = rem / hw, rr = rem - ci * hw;
+                    const uint32_t y0 = rr / ow, x0 = rr - y0 * ow;
+                    base_in = ((img * a.c + ci) * a.h + y0 * a.kh) * a.w + x0 * a.kw;
                 }
-            plain = acc < 0 ? (u64)((i64)PP + acc) : (u64)acc;                   // encode_signed (NONLIN_PLAIN)
-        }
-        // source: beta^-1 per window -- Montgomery batch inversion over the block's windows
-        // (warp-shuffle prefix/suffix products, one Fermat inversion per block)
-        const u64 pre = warp_excl_prefix(beta, lane);
-        const u64 suf = warp_excl_suffix(beta, lane);
-        if (lane == 31) s_warp[warp] = mulm(pre, beta);
-        __syncthreads();
-        u64 before = 1, after = 1, total = 1;
+                i64 acc = a.pool_kind == 1 ? INT64_MIN : 0;
+#pragma unroll 1
+                for (int wy = 0; wy < a.kh; wy++)
+#pragma unroll 1
+                    for (int wx = 0; wx < a.kw; wx++) {
+                        const uint32_t i = base_in + wy * a.w + wx;
+                        u64 x[N];
+                        chain_elem<K, N>(a, tb, i, x, bad);
+                        // participants mask with their beta shares (NONLIN_MASKED); elite rec over m
+                        u64 cb[K - 1];
+                        coeffs<K>(cb, a.sseed, a.sstream + 5, i);
+                        u64 mk[M];
 #pragma unroll
-        for (int w2 = 0; w2 < CHAIN_WARPS; w2++) {
-            const u64 wv = s_warp[w2];
-            if (w2 < warp) before = mulm(before, wv);
-            if (w2 > warp) after = mulm(after, wv);
-            total = mulm(total, wv);
+                        for (int j = 0; j < M; j++) mk[j] = mulm(x[j], share_at<K, N>(bt, cb, tb, j));
+                        const u64 v = canon(lin<M>(mk, tb.wp));
+                        i64 sv = v > PHALF ? (i64)v - (i64)PP : (i64)v;
+                        if (a.relu && sv <= 0) sv = 0;
+                        if (a.pool_kind == 1) acc = sv > acc ? sv : acc;
+                        else acc += sv;
+                    }
+                pl = acc < 0 ? (u64)((i64)PP + acc) : (u64)acc;                  // encode_signed (NONLIN_PLAIN)
+            }
+            plain[q] = pl;
+            beta[q] = bt;
+            pre[q] = run;                       // product of this thread's earlier betas
+            run = mulm(run, bt);
         }
-        if (threadIdx.x == 0) s_inv = invm(total);
-        __syncthreads();
-        const u64 binv = mulm(mulm(mulm(before, after), mulm(pre, suf)), s_inv);
-        if (live) {
-            u64 cbi[K - 1];
-            coeffs<K>(cbi, a.sseed, a.sstream + 6, o);
+        // source: beta^-1 for every window of the warp from one inversion
+        const u64 wpre = warp_excl_prefix(run, lane);
+        const u64 wsuf = warp_excl_suffix(run, lane);
+        const u64 total = __shfl_sync(0xffffffffu, mulm(wpre, run), 31);
+        u64 inv = mulm(mulm(invm(total), wpre), wsuf);      // = run^-1
+#pragma unroll 1
+        for (int q = WPT - 1; q >= 0; q--) {
+            const uint32_t o = base + q * CHAIN_THREADS + threadIdx.x;
+            const u64 binv = mulm(inv, pre[q]);
+            inv = mulm(inv, beta[q]);
+            if (o < n_out) {
+                u64 cbi[K - 1];
+                coeffs<K>(cbi, a.sseed, a.sstream + 6, o);
 #pragma unroll
-            for (int t = 0; t < N; t++)
-                if (t < a.fan) a.out[(u64)t * a.out_ps + o] = canon(mulm(plain, share_at<K, N>(binv, cbi, tb, t)));
+                for (int t = 0; t < N; t++)
+                    if (t < a.fan)
+                        a.out[(u64)t * a.out_ps + o] = canon(mulm(plain[q], share_at<K, N>(binv, cbi, tb, t)));
+            }
         }
-        __syncthreads();                       // s_warp / s_inv reuse in the next iteration
     }
     if (a.fail && bad) atomicAdd(a.fail, bad);
 }
@@ -468,7 +475,7 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
         k_chain_plain<K, N><<<(unsigned)blocks, PLAIN_THREADS, 0, st>>>(a, tb, f);
     } else {
         const u64 n_out = (u64)d->nb * d->c * (d->h / d->kh) * (d->w / d->kw);
-        u64 blocks = (n_out + CHAIN_THREADS - 1) / CHAIN_THREADS;
+        u64 blocks = (n_out + CHAIN_THREADS * WPT - 1) / (CHAIN_THREADS * WPT);
         if (blocks > 148ull * 16) blocks = 148ull * 16;
         if (blocks < 1) blocks = 1;
         k_chain_nonlin<K, N><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a, tb, f);
