@@ -108,7 +108,7 @@ def measured_peaks():
     try:
         with open(path) as fh:
             d = json.load(fh)
-        return d.get("hbm_gbs", 6545.3), d.get("bf16_tflops", 1653.7), "measured"
+        return d.get("hbm_gbs", 6545.3), d.get("bf16_tflops_sustained", d.get("bf16_tflops", 1653.7)), "measured sustained"
     except OSError:
         return 6650.0, 1590.0, "fallback"
 
@@ -176,6 +176,59 @@ def cpu_baseline_sample(model, k, n, verify, budget_s=20.0):
                        f"({len(sub) - 1} ops, {blk_macs / 1e9:.3f} of {total_macs / 1e9:.2f} GMAC) for 1 image: "
                        f"{dt:.1f} s, extrapolated by field-MAC share"),
             "s_per_image": s_per_img}
+
+
+def load_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch, averaged per kernel class over
+    one full step, from the committed ncu capture (profiles/<round>/traffic.json), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")))
+    if not files:
+        return {}
+    try:
+        with open(files[-1]) as fh:
+            return json.load(fh).get("bytes_per_launch", {})
+    except (OSError, ValueError):
+        return {}
+
+
+def roofline(kstats, eng, dev_ms, bf16, hbm, src):
+    """Roofline of the dominant kernel class of the step (by device time), plus every class.
+    gemm: int8 tensor ops = L^2 * 2 * field MACs (L = 6 u8 limbs per 45-bit share) against the
+    int8 peak, 2 x measured dense bf16 (sustained: the GEMM runs inside a long step).
+    chain / im2col: algorithmic HBM bytes against the measured copy bandwidth."""
+    traffic = load_traffic()
+    L2 = eng.limb_products()
+    peak_int8 = 2.0 * bf16
+    rows = {}
+    for cls, st in kstats.items():
+        if not st["launches_per_step"] or cls == "gemm_simt":
+            continue
+        sec = st["ms_per_launch"] / 1e3
+        if cls == "gemm":
+            achieved = 2.0 * L2 * st["work_per_launch"] / sec / 1e12
+            r = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak_int8, 1), "unit": "TFLOP/s",
+                 "frac": round(achieved / peak_int8, 4),
+                 "field_gops": round(2.0 * st["work_per_launch"] / sec / 1e9, 1),
+                 "note": (f"int8 ops = {L2} u8 limb products x 2 x field MACs; peak = 2 x {src} dense bf16 "
+                          f"({bf16} TF/s, sm_100 int8 MMA rate is 2x bf16)")}
+        else:
+            achieved = st["work_per_launch"] / sec / 1e9
+            r = {"bound": "hbm", "achieved": round(achieved, 1), "peak": round(hbm, 1), "unit": "GB/s",
+                 "frac": round(achieved / hbm, 4),
+                 "note": "algorithmic bytes per launch (DESIGN.md section 3) / CUDA-event launch time"}
+        t = traffic.get(cls)
+        r["traffic"] = round(t) if t else None
+        r["kernel"] = st["kernel"]
+        r["launches_per_step"] = round(st["launches_per_step"], 1)
+        r["ms_per_step"] = round(st["ms_per_step"], 3)
+        r["share_of_step"] = round(st["ms_per_step"] / dev_ms, 4)
+        r["work_per_launch"] = st["work_per_launch"]
+        rows[cls] = r
+    if not rows:
+        return None, {}
+    dom = max(rows, key=lambda c: rows[c]["ms_per_step"])
+    return dict(rows[dom], kernel_class=dom), rows
 
 
 def run_reference(args):
@@ -275,7 +328,7 @@ def main():
     # ---- device-resident timed region (value) ----
     sampler = ClockSampler(local)
     sampler.start()
-    gemm_prof = eng.enable_gemm_profiling()
+    eng.enable_profiling()
     sync_all()
     l0 = _lib.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -286,8 +339,8 @@ def main():
     sync_all()
     launches = (_lib.launch_count() - l0) // args.steps
     dev_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
-    gemm_stats = eng.gemm_profile_summary(args.steps)
-    eng.disable_gemm_profiling()
+    kstats = eng.profile_summary(args.steps)
+    eng.disable_profiling()
     clocks = sampler.stop()
     # ---- end-to-end through the public API with host buffers (e2e) ----
     out_host = torch.empty((B,) + eng.out_shape(), dtype=torch.int64).pin_memory()
@@ -316,17 +369,7 @@ def main():
     e2e = imgs / (e2e_ms / 1000.0)
     hbm, bf16, src = measured_peaks()
     online, offline = eng.comm_per_image()
-    roof = None
-    if gemm_stats["launches"]:
-        achieved = gemm_stats["int8_ops_per_launch"] / (gemm_stats["ms_per_launch"] / 1000.0) / 1e12
-        peak = 2.0 * bf16
-        roof = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "TFLOP/s",
-                "frac": round(achieved / peak, 4), "traffic": None,
-                "kernel": gemm_stats["kernel"],
-                "note": (f"int8 tensor ops = L*2*M*N*K with L={gemm_stats['limb_products']} u8 limb products per "
-                         f"field product; peak = 2 x {src} dense bf16 ({bf16} TF/s): sm_100 int8 rate is 2x bf16"),
-                "field_gops": round(gemm_stats["field_ops_per_launch"] / (gemm_stats["ms_per_launch"] / 1e3) / 1e9, 1),
-                "gemm_share_of_step": round(gemm_stats["ms_total"] / dev_ms, 4)}
+    roof, by_kernel = roofline(kstats, eng, dev_ms, bf16, hbm, src)
     cpu = None
     if not args.no_cpu_baseline:
         try:
@@ -345,6 +388,7 @@ def main():
                 "h2d_bytes_per_step": int(x_host.numel() * 8), "d2h_bytes_per_step": int(out_host.numel() * 8)},
         "gpu_launches": int(launches),
         "roofline": roof,
+        "roofline_by_kernel": by_kernel,
         "cpu_baseline": cpu,
         "clocks": clocks,
         "outputs_match_plaintext": outputs_match,

@@ -190,7 +190,12 @@ class BatchedEngine:
         d.ext = ctypes.addressof(self._ext_host) if self._ext_host is not None else None
         d.p = p
         d.fault_rank = self.fault[1] if (self.fault is not None and self.fault[0] == chain[0]) else -1
+        e0 = self._event() if self._prof is not None else None
         _lib.call("ssn_layer_chain", ctypes.byref(d), _lib.stream_ptr())
+        if e0 is not None:
+            nbytes = 8 * m * nel + (8 * n * nel if add is not None else 0)
+            nbytes += 8 * (d.fan * n_out if nl is not None else n * nel)
+            self._record("chain", e0, self._event(), nbytes, "k_chain_nonlin" if nl is not None else "k_chain_plain")
         self.kernel_launches += 1
         return Y
 
@@ -203,29 +208,41 @@ class BatchedEngine:
         self.kernel_launches += 1
 
     # ------------------------------------------------------------------ instrumentation
-    _gemm_prof = None
+    # Per kernel class, CUDA events recorded on the launching stream around every launch of
+    # the timed steps, with the launch's algorithmic work (bench roofline):
+    #   gemm    field MACs (x L^2 u8 limb products on the tensor pipe)    k_gemm_p45 / k_gemm_tc
+    #   chain   algorithmic HBM bytes (8*m in + 8*n out [+ 8*n add])      k_chain_*
+    #   im2col  algorithmic HBM bytes (8 B per input share read once + limb-plane bytes written)
+    _prof = None
 
-    def enable_gemm_profiling(self):
-        """Record CUDA events around every share-GEMM launch (bench roofline)."""
-        self._gemm_prof = []
-        return self._gemm_prof
+    def enable_profiling(self):
+        self._prof = {}
+        return self._prof
 
-    def disable_gemm_profiling(self):
-        self._gemm_prof = None
+    def disable_profiling(self):
+        self._prof = None
 
-    def gemm_profile_summary(self, steps):
-        prof = self._gemm_prof or []
+    def _record(self, cls, e0, e1, work, kernel):
+        if self._prof is not None:
+            self._prof.setdefault(cls, []).append((e0, e1, work, kernel))
+
+    @staticmethod
+    def _event():
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        return e
+
+    def profile_summary(self, steps):
         torch.cuda.synchronize()
-        ms = [a.elapsed_time(b) for a, b, _, _ in prof]
-        macs = [mac for _, _, mac, _ in prof]
-        kernels = sorted({kname for _, _, _, kname in prof})
-        nl = len(prof)
-        L = self.limb_products()
-        return {"launches": nl // max(steps, 1), "ms_total": sum(ms) / max(steps, 1),
-                "ms_per_launch": (sum(ms) / nl) if nl else 0.0,
-                "field_ops_per_launch": (2.0 * sum(macs) / nl) if nl else 0.0,
-                "int8_ops_per_launch": (2.0 * L * sum(macs) / nl) if nl else 0.0,
-                "limb_products": L, "kernel": ",".join(kernels)}
+        out = {}
+        for cls, rec in (self._prof or {}).items():
+            ms = [a.elapsed_time(b) for a, b, _, _ in rec]
+            work = [w for _, _, w, _ in rec]
+            nl = len(rec)
+            out[cls] = {"launches_per_step": nl / max(steps, 1), "ms_per_step": sum(ms) / max(steps, 1),
+                        "ms_per_launch": sum(ms) / nl if nl else 0.0, "work_per_launch": sum(work) / nl if nl else 0.0,
+                        "kernel": ",".join(sorted({k for _, _, _, k in rec}))}
+        return out
 
     def limb_products(self):
         L = (self.p.bit_length() + 7) // 8
@@ -342,10 +359,7 @@ class BatchedEngine:
         w = self.W[op.weight + ".w"]
         O = op.out_shape[0]
         conv = w.dim() == 5
-        prof = self._gemm_prof
-        if prof is not None:
-            g0 = torch.cuda.Event(enable_timing=True)
-            g0.record()
+        timing = {} if self._prof is not None else None
         K = _count(w.shape[2:])
         ohw = _count(op.out_shape[1:]) if conv else 1
         tc = gemm_mod.use_tc(p, B * ohw, K, O)
@@ -357,15 +371,19 @@ class BatchedEngine:
         if conv:
             C, H, Wd = op.in_shape
             acc = field_conv(w[:m], X[:m].reshape(m, B, C, H, Wd), op.stride, op.padding, p, nimg=B, nparty=m,
-                             planes=planes, force="tc" if tc else "simt")
+                             planes=planes, force="tc" if tc else "simt", timing=timing)
         else:
             acc = field_dense(w[:m], X[:m].reshape(m, B, -1), p, nimg=B, nparty=m, planes=planes,
-                              force="tc" if tc else "simt")
-        if prof is not None:
-            g1 = torch.cuda.Event(enable_timing=True)
-            g1.record()
-            kname = "ssn_gemm_tc" if tc else ("ssn_conv_simt" if conv else "ssn_dense_simt")
-            prof.append((g0, g1, m * B * ohw * O * K, kname))
+                              force="tc" if tc else "simt", timing=timing)
+        if timing:
+            L = gemm_mod.limbs(p)
+            macs = m * B * ohw * O * K
+            e0, e1, kname = timing["gemm"]
+            self._record("gemm" if tc else "gemm_simt", e0, e1, macs, kname)
+            if "prep" in timing:
+                e0, e1, kname = timing["prep"]
+                in_el = m * B * _count(op.in_shape)
+                self._record("im2col", e0, e1, 8 * in_el + L * m * B * ohw * gemm_mod.kpad(K), kname)
         return acc
 
     def _linear(self, idx, op, X, src_rng, party_rng):

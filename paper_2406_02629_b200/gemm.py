@@ -38,13 +38,25 @@ def weight_planes(w, p, nparty=1):
     return planes
 
 
+def gemm_kernel_name(p, L, rows):
+    """The kernel ssn_gemm_tc dispatches to (csrc/ssn_gemm_tc.cu)."""
+    return "k_gemm_p45" if (L == 6 and p == (1 << 45) - 55 and rows >= 128) else f"k_gemm_tc<{L}>"
+
+
 def use_tc(p, rows, K, O):
     return rows >= TC_MIN_ROWS and O >= 16 and K >= 32 and tc_supported(p, K)
 
 
-def field_conv(w, x, stride, padding, p, nimg=1, nparty=1, planes=None, force=None):
+def _ev():
+    e = torch.cuda.Event(enable_timing=True)
+    e.record()
+    return e
+
+
+def field_conv(w, x, stride, padding, p, nimg=1, nparty=1, planes=None, force=None, timing=None):
     """w: (nparty, O, C, kh, kw), x: (nparty, nimg, C, H, W) -> (nparty, nimg, O, OH, OW)
-    (leading unit dims squeezed when nparty == nimg == 1)."""
+    (leading unit dims squeezed when nparty == nimg == 1).  timing: optional dict that
+    receives CUDA events around the operand-prep and GEMM launches."""
     O, C, kh, kw = w.shape[-4:]
     H, W = x.shape[-2:]
     OH = (H + 2 * padding - kh) // stride + 1
@@ -60,18 +72,26 @@ def field_conv(w, x, stride, padding, p, nimg=1, nparty=1, planes=None, force=No
         if planes is None:
             planes = weight_planes(w.reshape(nparty, O, K), p, nparty)
         a = torch.empty((nparty, L, rows, Kp), dtype=torch.uint8, device=x.device)
+        e0 = _ev() if timing is not None else None
         _lib.call("ssn_im2col_limbs", _lib.ptr(x), nparty, nimg, C, H, W, kh, kw, stride, padding, L, _lib.ptr(a),
                   Kp, nimg * C * H * W, _lib.stream_ptr())
+        e1 = _ev() if timing is not None else None
         _lib.call("ssn_gemm_tc", _lib.ptr(a), _lib.ptr(planes), nparty, L, rows, O, Kp, OH * OW, _lib.ptr(out),
                   nimg * O * OH * OW, p, _lib.stream_ptr())
+        if timing is not None:
+            timing["prep"] = (e0, e1, "k_im2col_limbs")
+            timing["gemm"] = (e1, _ev(), gemm_kernel_name(p, L, rows))
         return out
     w = w.contiguous()
+    e0 = _ev() if timing is not None else None
     _lib.call("ssn_conv_simt", _lib.ptr(w), O * C * kh * kw, _lib.ptr(x), nimg * C * H * W, _lib.ptr(out),
               nimg * O * OH * OW, nparty, nimg, O, C, H, W, kh, kw, stride, padding, p, _lib.stream_ptr())
+    if timing is not None:
+        timing["gemm"] = (e0, _ev(), "k_conv_simt")
     return out
 
 
-def field_dense(w, x, p, nimg=1, nparty=1, planes=None, force=None):
+def field_dense(w, x, p, nimg=1, nparty=1, planes=None, force=None, timing=None):
     """w: (nparty, O, K), x: (nparty, nimg, K) -> (nparty, nimg, O) (squeezed for 1 x 1)."""
     O, K = w.shape[-2:]
     x = x.contiguous()
@@ -83,11 +103,19 @@ def field_dense(w, x, p, nimg=1, nparty=1, planes=None, force=None):
         if planes is None:
             planes = weight_planes(w.reshape(nparty, O, K), p, nparty)
         a = torch.empty((nparty, L, nimg, Kp), dtype=torch.uint8, device=x.device)
+        e0 = _ev() if timing is not None else None
         _lib.call("ssn_limb_split", _lib.ptr(x), nimg, K, Kp, L, _lib.ptr(a), nimg * K, nparty, _lib.stream_ptr())
+        e1 = _ev() if timing is not None else None
         _lib.call("ssn_gemm_tc", _lib.ptr(a), _lib.ptr(planes), nparty, L, nimg, O, Kp, 1, _lib.ptr(out), nimg * O,
                   p, _lib.stream_ptr())
+        if timing is not None:
+            timing["prep"] = (e0, e1, "k_limb_split")
+            timing["gemm"] = (e1, _ev(), gemm_kernel_name(p, L, nimg))
         return out
     w = w.contiguous()
+    e0 = _ev() if timing is not None else None
     _lib.call("ssn_dense_simt", _lib.ptr(w), O * K, _lib.ptr(x), nimg * K, _lib.ptr(out), nimg * O, nparty,
               nimg, O, K, p, _lib.stream_ptr())
+    if timing is not None:
+        timing["gemm"] = (e0, _ev(), "k_dense_simt")
     return out
