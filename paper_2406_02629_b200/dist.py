@@ -55,16 +55,30 @@ class DistTransport:
         self.record = record
         self.frames = {}             # (src, dst) -> [frame bytes]  (sent frames, when recording)
         self.decode_object = decode_object
+        self._pending = []           # in-flight isend works (+ their tensors, kept alive)
 
     # -- wire helpers
     def _comm_device(self):
         return self.device if self.backend == "nccl" else torch.device("cpu")
 
     def _send_tensor(self, t, dst):
+        # Non-blocking: every party sends to several peers before it receives (e.g. reshare
+        # step 1), so a blocking send would deadlock two parties sending to each other.
+        # Per-(src, dst) FIFO order is preserved by the backend.
         t = t.contiguous()
         if self.backend != "nccl" and t.device.type != "cpu":
             t = t.cpu()
-        dist.send(t, dst)
+        self._pending.append((dist.isend(t, dst), t))
+        if len(self._pending) > 64:
+            self._reap()
+
+    def _reap(self):
+        self._pending = [(w, t) for (w, t) in self._pending if not w.is_completed()]
+
+    def flush(self):
+        for w, _ in self._pending:
+            w.wait()
+        self._pending = []
 
     def _recv_tensor(self, shape, dtype, src):
         t = torch.empty(shape, dtype=dtype, device=self._comm_device())
@@ -132,7 +146,7 @@ class DistTransport:
         return msg
 
     def close(self):
-        pass
+        self.flush()
 
 
 def mask_bundle_decoder(scheme, device):
@@ -185,6 +199,7 @@ def run_party_dist(model, scheme, seed, input_int, device, ordering="ltn", rng_m
     tr = DistTransport(rank, device, metrics, record=record, decode_object=mask_bundle_decoder(scheme, device))
     if rank == 0:
         send_bundles(tr, ops, scheme, seed, metrics, rng_mode)
+        tr.close()
         return None, metrics, tr.frames
     # model owner / input owner dealing, replayed from the seed (S/engine.py:40-54)
     weight_values = {name: qt.values for name, qt in model.weights.items()}
@@ -194,6 +209,7 @@ def run_party_dist(model, scheme, seed, input_int, device, ordering="ltn", rng_m
     metrics.set_op(rank, "offline", -1)
     receive_bundle(ctx)
     out = run_party_online(ctx, ops, w_share, x_share, metrics)
+    tr.close()
     if out is not None:
         out = np.asarray(out, dtype=np.int64)
     return out, metrics, tr.frames

@@ -3,6 +3,7 @@ world_size 2 and 3: addressed FIFO delivery, phase checks (ScheduleDivergence, l
 S/transport.py:98-109), the reference's element / frame-byte accounting (S/metrics.py:46-60,
 S/wire.py:104-107) and the recorded canonical frames.  No kernels run here."""
 
+import datetime
 import os
 import socket
 
@@ -23,7 +24,7 @@ def _worker(rank, world, port, q):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=90))
     from paper_2406_02629_b200.dist import DistTransport
     from paper_2406_02629_b200.metrics import CommMetrics
     from paper_2406_02629_b200.transport import ScheduleDivergence
@@ -59,6 +60,7 @@ def _worker(rank, world, port, q):
                     res["divergence"] = True
             t = m._tally(rank)
             res["recv"] = (t.elements_received, t.bytes_received)
+        tr.close()                            # complete the in-flight isends
         res["frame_sizes"] = (share_frame_bytes((3, 4)), plain_frame_bytes((3,)))
         q.put((rank, res))
     finally:
@@ -73,7 +75,7 @@ def test_dist_transport_gloo(world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    out = dict(q.get(timeout=120) for _ in range(world))
+    out = dict(q.get(timeout=60) for _ in range(world))
     for p in procs:
         p.join(60)
         assert p.exitcode == 0

@@ -4,6 +4,7 @@ single GPU cannot host several NCCL ranks).  Shares, masks and every message are
 to the reference run: decoded outputs equal the lockstep oracle and the canonical transcript
 digest (S/transport.py:68-80) of all ranks' frames equals the oracle's."""
 
+import datetime
 import os
 import socket
 
@@ -28,7 +29,7 @@ def _party(rank, world, port, k, n, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     torch.cuda.set_device(0)
-    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dist.init_process_group("gloo", rank=rank, world_size=world, timeout=datetime.timedelta(seconds=90))
     try:
         import paper_2406_02629_b200 as P
         from paper_2406_02629_b200.dist import run_party_dist
@@ -38,6 +39,9 @@ def _party(rank, world, port, k, n, q):
         out, metrics, frames = run_party_dist(model, scheme, 7, x, "cuda:0", record=True)
         t = metrics._tally(rank)
         q.put((rank, out, frames, t.elements_sent))
+    except BaseException as exc:             # surface worker failures instead of hanging
+        q.put((rank, "error", repr(exc), 0))
+        raise
     finally:
         dist.destroy_process_group()
 
@@ -56,7 +60,8 @@ def test_party_per_process_matches_reference(k, n):
         p.start()
     res = {}
     for _ in range(world):
-        rank, out, frames, sent = q.get(timeout=300)
+        rank, out, frames, sent = q.get(timeout=180)
+        assert not (isinstance(out, str) and out == "error"), f"rank {rank}: {frames}"
         res[rank] = (out, frames, sent)
     for p in procs:
         p.join(120)
