@@ -170,9 +170,11 @@ def mask_bundle_decoder(scheme, device):
 
 
 def transcript_digest(frames_by_rank):
-    """Canonical transcript sha256 (S/transport.py:68-80) from every rank's sent frames."""
+    """Canonical transcript sha256 (S/transport.py:68-80) from every rank's sent frames
+    (list indexed by rank).  Every ordered channel (src != dst) appears, empty ones too."""
     import hashlib
-    merged = {}
+    world = len(frames_by_rank)
+    merged = {(s, d): [] for s in range(world) for d in range(world) if s != d}
     for frames in frames_by_rank:
         merged.update(frames)
     parts = []
