@@ -536,54 +536,71 @@ __global__ void k_limb_split(const u64 *__restrict__ x, u64 rows, u64 K, u64 Kpa
 }
 
 // conv: x [P][img][C][H][W] -> planes [P][L][img*OH*OW][Kpad], k = (c, i, j) like im2col.
-// Block: 32 rows x 64 k; gather coalesced along rows, transpose in shared memory, write
-// 8-byte limb packs along k.
-__global__ void __launch_bounds__(256) k_im2col_limbs(const u64 *__restrict__ x, int C, int H, int W, int kh, int kw,
-                                                       int stride, int pad, int OH, int OW, int L, u64 rows, int K,
-                                                       int Kpad, uint8_t *__restrict__ planes, u64 x_pstride) {
-    __shared__ u64 sv[32][65];
+// Block: 64 rows x 64 k.  Gather coalesced along rows (consecutive output pixels) into
+// shared memory, then each thread emits one 16-byte vector per limb plane (16 k of one row).
+constexpr int IC_ROWS = 64, IC_K = 64, IC_THREADS = 256;
+
+__global__ void __launch_bounds__(IC_THREADS) k_im2col_limbs(const u64 *__restrict__ x, int C, int H, int W, int kh,
+                                                              int kw, int stride, int pad, int OH, int OW, int L,
+                                                              uint32_t rows, int K, int Kpad,
+                                                              uint8_t *__restrict__ planes, u64 x_pstride) {
+    __shared__ u64 sv[IC_ROWS][IC_K + 1];
     const int party = blockIdx.z;
-    const u64 r0 = (u64)blockIdx.y * 32;
-    const int k0 = blockIdx.x * 64;
+    const uint32_t r0 = blockIdx.y * IC_ROWS;
+    const int k0 = blockIdx.x * IC_K;
     const int t = threadIdx.x;
     const u64 *xp = x + (u64)party * x_pstride;
-    const int ohw = OH * OW;
+    const uint32_t ohw = (uint32_t)(OH * OW);
+    const int khw = kh * kw;
     {
-        const int rr = t & 31;
-        const u64 r = r0 + rr;
-        u64 img = 0;
-        int oy = 0, ox = 0;
+        const int rr = t & (IC_ROWS - 1);
+        const uint32_t r = r0 + rr;
         const bool rok = r < rows;
+        uint32_t img = 0;
+        int oy = 0, ox = 0;
         if (rok) {
             img = r / ohw;
-            int pix = (int)(r - img * ohw);
+            const int pix = (int)(r - img * ohw);
             oy = pix / OW;
             ox = pix - oy * OW;
         }
-        for (int kk = t >> 5; kk < 64; kk += 8) {
+        const u64 *ximg = xp + (u64)img * C * H * W;
+#pragma unroll 4
+        for (int kk = t / IC_ROWS; kk < IC_K; kk += IC_THREADS / IC_ROWS) {
             const int k = k0 + kk;
             u64 v = 0;
             if (rok && k < K) {
-                const int c = k / (kh * kw);
-                const int rem = k - c * kh * kw;
+                const int c = k / khw;
+                const int rem = k - c * khw;
                 const int i = rem / kw, j = rem - i * kw;
                 const int sy = oy * stride + i - pad, sx = ox * stride + j - pad;
-                if (sy >= 0 && sy < H && sx >= 0 && sx < W) v = xp[((img * C + c) * H + sy) * (u64)W + sx];
+                if (sy >= 0 && sy < H && sx >= 0 && sx < W) v = ximg[((u64)c * H + sy) * W + sx];
             }
             sv[rr][kk] = v;
         }
     }
     __syncthreads();
     {
-        const int rr = t >> 3, kc = (t & 7) * 8;
-        const u64 r = r0 + rr;
+        const int rr = t >> 2, kc = (t & 3) * 16;
+        const uint32_t r = r0 + rr;
         if (r < rows && k0 + kc < Kpad) {
-            uint8_t *dst = planes + (u64)party * L * rows * Kpad + r * Kpad + k0 + kc;
-            for (int l = 0; l < L; l++) {
-                u64 packed = 0;
+            uint8_t *dst = planes + (u64)party * L * rows * Kpad + (u64)r * Kpad + k0 + kc;
+            u64 v[16];
 #pragma unroll
-                for (int q = 0; q < 8; q++) packed |= ((sv[rr][kc + q] >> (8 * l)) & 0xFF) << (8 * q);
-                *reinterpret_cast<u64 *>(dst + (u64)l * rows * Kpad) = packed;
+            for (int q = 0; q < 16; q++) v[q] = sv[rr][kc + q];          // one pass over smem
+#pragma unroll 1
+            for (int l = 0; l < L; l++) {
+                uint32_t w[4];
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    // byte l of 4 consecutive elements -> one 32-bit word (PRMT-friendly)
+                    const uint32_t b0 = (uint32_t)(v[4 * q] >> (8 * l)) & 0xFF;
+                    const uint32_t b1 = (uint32_t)(v[4 * q + 1] >> (8 * l)) & 0xFF;
+                    const uint32_t b2 = (uint32_t)(v[4 * q + 2] >> (8 * l)) & 0xFF;
+                    const uint32_t b3 = (uint32_t)(v[4 * q + 3] >> (8 * l)) & 0xFF;
+                    w[q] = b0 | (b1 << 8) | (b2 << 16) | (b3 << 24);
+                }
+                *reinterpret_cast<uint4 *>(dst + (u64)l * rows * Kpad) = make_uint4(w[0], w[1], w[2], w[3]);
             }
         }
     }
@@ -609,9 +626,10 @@ extern "C" int ssn_im2col_limbs(const u64 *x, int nparty, int nimg, int C, int H
     const int K = C * kh * kw;
     if ((u64)K > Kpad || OH < 1 || OW < 1) return SSN_ERR_ARG;
     const u64 rows = (u64)nimg * OH * OW;
-    dim3 grid((unsigned)((Kpad + 63) / 64), (unsigned)((rows + 31) / 32), (unsigned)nparty);
-    k_im2col_limbs<<<grid, 256, 0, (cudaStream_t)stream>>>(x, C, H, W, kh, kw, stride, pad, OH, OW, L, rows, K,
-                                                           (int)Kpad, planes, x_pstride);
+    if (rows >= (1ull << 32)) return SSN_ERR_UNSUPPORTED;
+    dim3 grid((unsigned)((Kpad + IC_K - 1) / IC_K), (unsigned)((rows + IC_ROWS - 1) / IC_ROWS), (unsigned)nparty);
+    k_im2col_limbs<<<grid, IC_THREADS, 0, (cudaStream_t)stream>>>(x, C, H, W, kh, kw, stride, pad, OH, OW, L,
+                                                                  (uint32_t)rows, K, (int)Kpad, planes, x_pstride);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
 
