@@ -255,6 +255,88 @@ def run_reference(args):
     print(json.dumps(out), flush=True)
 
 
+def run_party_placement(args):
+    """Party-per-GPU placement (sharded.PartyShardedEngine): ranks [g*(n+1), (g+1)*(n+1)) form
+    group g (source + n parties); leftover ranks idle.  value = G*B images / max-over-ranks step."""
+    import torch
+    import torch.distributed as dist
+    from paper_2406_02629_b200 import resnet
+    from paper_2406_02629_b200.field import PrimeField
+    from paper_2406_02629_b200.sharded import PartyShardedEngine
+    from paper_2406_02629_b200.sss import SssScheme
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SSN_SHARED_GPU=1: every rank on cuda:0 with host-staged gloo (single-GPU functional check)
+    shared = os.environ.get("SSN_SHARED_GPU") == "1"
+    if shared:
+        local = 0
+    torch.cuda.set_device(local)
+    kind, k, n, verify, dflt_batch = WORKLOADS[args.workload]
+    groups = world // (n + 1)
+    if groups < 1:
+        if rank == 0:
+            print(json.dumps({"metric": metric_for(args.workload), "unavailable":
+                              f"party placement needs >= n+1 = {n + 1} GPUs, got {world}"}), flush=True)
+        return
+    if shared:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    B = args.batch or dflt_batch
+    model = build_model(kind)
+    scheme = SssScheme(PrimeField(), k, n)
+    g = rank // (n + 1)
+    eng = PartyShardedEngine(model, scheme, batch=B, seed=7 + g, verify=verify, group=g) if g < groups else None
+    xb = (model.random_inputs(seed=100 + g, batch=B) if hasattr(model, "random_inputs")
+          else np.stack([__import__("paper_2406_02629_b200.model", fromlist=["random_input"])
+                         .random_input(100 + g, model, index=i)[0] for i in range(B)]))
+    x_dev = torch.as_tensor(xb, device="cuda")
+    outputs_match = None
+    if eng is not None and not args.no_check:
+        got = eng.run(xb)
+        if eng.role == 1:
+            want = resnet.plaintext_forward(model, xb, device="cuda")[0] if hasattr(model, "nodes") else None
+            outputs_match = bool(np.array_equal(got, want)) if want is not None else None
+    for _ in range(args.warmup):
+        if eng is not None:
+            eng.run_device(x_dev)
+    torch.cuda.synchronize()
+    dist.barrier()
+    sampler = ClockSampler(local)
+    sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        if eng is not None:
+            eng.run_device(x_dev)
+    e1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = sampler.stop()
+    cdev = "cpu" if shared else "cuda"
+    t = torch.tensor([e0.elapsed_time(e1) / args.steps], dtype=torch.float64, device=cdev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    m = torch.tensor([float(outputs_match is True), float(outputs_match is not None)], device=cdev)
+    dist.all_reduce(m, op=dist.ReduceOp.SUM)
+    ms = float(t.item())
+    checked = int(m[1].item())
+    match = None if checked == 0 else int(m[0].item()) == checked
+    if rank == 0:
+        imgs = groups * B
+        line = {"metric": metric_for(args.workload), "value": round(imgs / (ms / 1e3), 3), "unit": "images/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+                "data": "synthetic",
+                "config": {"workload": args.workload, "model": model.name, "k": k, "n": n, "verify": verify,
+                           "placement": f"party-per-GPU: {groups} group(s) x (source + {n} parties), "
+                                        f"{world - groups * (n + 1)} idle",
+                           "batch_per_group": B, "global_batch": imgs, "parallelism": f"party{n + 1} x dp{groups}"},
+                "gpu_launches": None, "clocks": clocks, "outputs_match_plaintext": match}
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -266,9 +348,15 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--placement", default="coresident", choices=["coresident", "party"],
+                    help="coresident: every GPU runs all n parties on its own batch (default); "
+                         "party: one GPU per party + one for the trusted source, NCCL p2p per hop, "
+                         "G = N // (n+1) groups data-parallel over images")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.placement == "party":
+        return run_party_placement(args)
 
     import torch
     import torch.distributed as dist
