@@ -29,7 +29,10 @@ WORKLOADS = {
     "resnet50-3pc": ("imagenet50", 2, 3, False, 16),
     "resnet18-cifar-3pc": ("cifar18", 2, 3, False, 128),
     "lenet-3pc": ("reference", 2, 3, False, 1024),
+    "gemm-sweep": ("gemm", 0, 0, False, 0),          # config 5: mod-p share GEMM + reshare sweep
 }
+SWEEP = [(256, 256, 256), (1024, 1024, 1024), (2048, 2048, 2048), (4096, 4096, 4096), (8192, 8192, 8192),
+         (16384, 4096, 4096), (4096, 4096, 16384), (16384, 16384, 16384)]
 METRIC = "ResNet-152 secure-inference images/s (5PC t=2, verification on, 224x224)"
 
 
@@ -231,9 +234,41 @@ def roofline(kstats, eng, dev_ms, bf16, hbm, src):
     return dict(rows[dom], kernel_class=dom), rows
 
 
+def gemm_reference(args):
+    """Reference arm of config 5: the oracle's exact mod-p GEMM (oracle/ssn_oracle.c, the C
+    restatement of `(w @ x) % p`, S/layers.py:252, all host threads) on a 512^3 sample,
+    extrapolated to the sweep's largest shape by MAC count."""
+    import oracle
+    oracle.build()
+    rng = np.random.default_rng(0)
+    p = oracle.DEFAULT_PRIME
+    S = 512
+    a = rng.integers(0, p, size=(S, S), dtype=np.int64)
+    b = rng.integers(0, p, size=(S, S), dtype=np.int64)
+    vals = []
+    for _ in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        oracle.gemm(a, b, p)
+        vals.append(2.0 * S ** 3 / (time.perf_counter() - t0) / 1e9)
+    v = float(np.median(vals[args.warmup:] or vals))
+    M, N, K = SWEEP[-1]
+    return {"metric": "mod-p share GEMM field Gop/s (largest sweep shape, summed over GPUs)", "value": round(v, 3),
+            "unit": "Gop/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(2.0 * M * N * K / (v * 1e9) * 1e3, 1), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic (uniform field elements)",
+            "config": {"workload": "gemm-sweep"},
+            "cpu_baseline": {"value": round(v, 3), "unit": "Gop/s", "cores": os.cpu_count(), "kind": "port",
+                             "sample": f"oracle C exact mod-p GEMM {S}^3 (u128 accumulate, OpenMP); rate is "
+                                       "size-independent, ms_per_step extrapolated to the largest shape"},
+            "e2e": {"value": round(v, 3), "unit": "Gop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
+        return
+    if args.workload == "gemm-sweep":
+        print(json.dumps(gemm_reference(args)), flush=True)
         return
     name = WORKLOADS[args.workload]
     model = build_model(name[0])
@@ -253,6 +288,89 @@ def run_reference(args):
            "cpu_baseline": cb,
            "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
+
+
+def run_gemm_sweep(args):
+    """Config 5: one party's mod-p share GEMM C = A.B^T over uniform field elements (u8 limb
+    planes, tcgen05) for M,N,K in SWEEP, plus the co-resident (3,5) reshare chain on the GEMM
+    output.  Every rank runs the sweep on its own GPU (weak scaling, no collective); value =
+    summed field Gop/s of the largest shape.  Exactness: a 256^3 slice against the CUDA-core
+    reference GEMM (ssn_dense_simt)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2406_02629_b200 import _lib, gemm as G
+    from paper_2406_02629_b200.field import PrimeField
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    p = PrimeField().p
+    L = G.limbs(p)
+    hbm, bf16, src = measured_peaks()
+    peak = 2.0 * bf16
+    st = torch.cuda.current_stream()
+
+    def rand_field(n, stream_id):
+        t = torch.empty(n, dtype=torch.int64, device="cuda")
+        _lib.call("ssn_rand", _lib.ptr(t), n, 0, p, 1234 + rank, stream_id, _lib.stream_ptr())
+        return t
+
+    def planes_of(x, rows, K):
+        pl = torch.empty((L, rows, G.kpad(K)), dtype=torch.uint8, device="cuda")
+        _lib.call("ssn_limb_split", _lib.ptr(x), rows, K, G.kpad(K), L, _lib.ptr(pl), rows * K, 1, _lib.stream_ptr())
+        return pl
+
+    # exactness gate: tensor-core vs CUDA-core GEMM on 256^3
+    a = rand_field(256 * 256, 1).reshape(256, 256)
+    b = rand_field(256 * 256, 2).reshape(256, 256)
+    ref = torch.empty((256, 256), dtype=torch.int64, device="cuda")     # [img=m][o=n]
+    _lib.call("ssn_dense_simt", _lib.ptr(b), 0, _lib.ptr(a), 0, _lib.ptr(ref), 0, 1, 256, 256, 256, p,
+              _lib.stream_ptr())
+    tc = G.field_matmul(planes_of(a, 256, 256), planes_of(b, 256, 256), 256, 256, 256, p)   # [n][m]
+    exact = bool(torch.equal(tc.t(), ref))
+    rows = []
+    for (M, N, K) in SWEEP:
+        A = planes_of(rand_field(M * K, 3), M, K)
+        Bp = planes_of(rand_field(N * K, 4), N, K)
+        out = torch.empty((N, M), dtype=torch.int64, device="cuda")
+        for _ in range(max(1, args.warmup)):
+            G.field_matmul(A, Bp, M, N, K, p, out=out)
+        torch.cuda.synchronize()
+        reps = max(1, args.steps)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            G.field_matmul(A, Bp, M, N, K, p, out=out)
+        e1.record(st)
+        torch.cuda.synchronize()
+        sec = e0.elapsed_time(e1) / reps / 1e3
+        fops = 2.0 * M * N * K / sec
+        rows.append({"M": M, "N": N, "K": K, "ms": round(sec * 1e3, 3), "field_gops": round(fops / 1e9, 1),
+                     "int8_tops": round(L * L * fops / 1e12, 1), "frac_int8": round(L * L * fops / 1e12 / peak, 4),
+                     "split_k": G.kpad(K) > G.max_k_chunk(p)})
+        del A, Bp, out
+    top = rows[-1]
+    value = top["field_gops"]
+    if world > 1:
+        t = torch.tensor([value], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        value = float(t.item())
+    if rank == 0:
+        line = {"metric": "mod-p share GEMM field Gop/s (largest sweep shape, summed over GPUs)",
+                "value": round(value, 1), "unit": "Gop/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": top["ms"], "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "u64", "data": "synthetic (uniform field elements)",
+                "config": {"workload": "gemm-sweep", "shapes": [list(r) for r in SWEEP], "limbs": L,
+                           "int8_products_per_field_mac": L * L},
+                "roofline": {"bound": "tensor", "achieved": top["int8_tops"], "peak": round(peak, 1),
+                             "unit": "TFLOP/s", "frac": top["frac_int8"], "traffic": None,
+                             "note": f"peak = 2 x {src} dense bf16"},
+                "exact_vs_cuda_core_gemm": exact, "sweep": rows}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def run_party_placement(args):
@@ -355,6 +473,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.workload == "gemm-sweep":
+        return run_gemm_sweep(args)
     if args.placement == "party":
         return run_party_placement(args)
 

@@ -119,3 +119,44 @@ def field_dense(w, x, p, nimg=1, nparty=1, planes=None, force=None, timing=None)
     if timing is not None:
         timing["gemm"] = (e0, _ev(), "k_dense_simt")
     return out
+
+
+# Largest K per tensor-core pass: L * Kpad * 255^2 < 2^32 keeps every limb-diagonal int32
+# accumulator exact (L = 6: Kpad <= 11008).  Larger K is split and the partial products are
+# added mod p.
+def max_k_chunk(p):
+    L = limbs(p)
+    return ((1 << 32) - 1) // (L * 65025) // 64 * 64
+
+
+def field_matmul(a_planes, b_planes, M, N, K, p, out=None, timing=None):
+    """C[N-major] = A (M x K) . B (N x K)^T mod p from pre-split u8 limb planes
+    a_planes [L][M][Kp], b_planes [L][N][Kp] (Kp = kpad(K)); C is (N, M) row-major = (M x N)^T,
+    i.e. out[n*M + m] -- the conv output layout with ohw = M.  Split-K above max_k_chunk."""
+    L, Kp = limbs(p), kpad(K)
+    out = torch.empty((N, M), dtype=torch.int64, device=a_planes.device) if out is None else out
+    chunk = max_k_chunk(p)
+    if Kp <= chunk:
+        e0 = _ev() if timing is not None else None
+        _lib.call("ssn_gemm_tc", _lib.ptr(a_planes), _lib.ptr(b_planes), 1, L, M, N, Kp, M, _lib.ptr(out), M * N, p,
+                  _lib.stream_ptr())
+        if timing is not None:
+            timing.append((e0, _ev()))
+        return out
+    part = torch.empty_like(out)
+    first = True
+    for k0 in range(0, Kp, chunk):
+        kc = min(chunk, Kp - k0)
+        a = a_planes[:, :, k0:k0 + kc].contiguous()
+        b = b_planes[:, :, k0:k0 + kc].contiguous()
+        dst = out if first else part
+        e0 = _ev() if timing is not None else None
+        _lib.call("ssn_gemm_tc", _lib.ptr(a), _lib.ptr(b), 1, L, M, N, kc, M, _lib.ptr(dst), M * N, p,
+                  _lib.stream_ptr())
+        if not first:
+            _lib.call("ssn_ewise", 0, _lib.ptr(out), _lib.ptr(part), _lib.ptr(out), M * N, 1, M * N, 1 << 62, 0, p,
+                      _lib.stream_ptr())
+        if timing is not None:
+            timing.append((e0, _ev()))
+        first = False
+    return out
