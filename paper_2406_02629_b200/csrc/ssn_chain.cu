@@ -95,7 +95,7 @@ __device__ __forceinline__ u64 addm(u64 a, u64 b) {
     const u64 s = a + b;
     return s >= PP ? s - PP : s;
 }
-// a * b < 2^96 (e.g. both lazy): q = prod >> 45 < 2^51, q*55 + low < 2^58 -> lazy result
+// a * b < 2^103: q = prod >> 45 < 2^58, q*55 + low < 2^64 -> lazy result
 __device__ __forceinline__ u64 mulm(u64 a, u64 b) {
     const u64 lo = a * b, hi = __umul64hi(a, b);
     const u64 q = (hi << (64 - PS)) | (lo >> PS);
@@ -146,13 +146,19 @@ __device__ __forceinline__ u64 lin(const u64 (&x)[M], const SRow<M> &r) {
     return lin_s<M>(x, xsum_of<M>(x), r);
 }
 
-// share of s (< 2^48) at rank t: s + sum_e c_e * id_t^(e+1), lazy
+// share of s at rank t: s + sum_e c_e * id_t^(e+1), UNREDUCED: for s < 2^48 and id powers
+// < 2^9 (n <= 7) the value stays below 2^57, a valid mulm operand and summand before lz.
 template <int K, int N>
-__device__ __forceinline__ u64 share_at(u64 s, const u64 (&c)[K - 1], const STables<K, N> &tb, int t) {
+__device__ __forceinline__ u64 share_raw(u64 s, const u64 (&c)[K - 1], const STables<K, N> &tb, int t) {
     u64 acc = s;
 #pragma unroll
     for (int e = 0; e < K - 1; e++) acc += mul_small(c[e], tb.pw[t][e]);
-    return lz(acc);
+    return acc;
+}
+// the same, lazily reduced (< 2^46): operand of lin_s
+template <int K, int N>
+__device__ __forceinline__ u64 share_at(u64 s, const u64 (&c)[K - 1], const STables<K, N> &tb, int t) {
+    return lz(share_raw<K, N>(s, c, tb, t));
 }
 
 // K-1 uniform field elements: masked 45-bit Philox words.  Values in [p, 2^45) are lazy
@@ -219,9 +225,9 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
             u64 back[K];
 #pragma unroll
             for (int fr = 0; fr < K; fr++) back[fr] = lin_s<M>(sub[fr], subsum[fr], tb.rt[t]);
-            u64 y = lin<K>(back, tb.wf) + share_at<K, N>(0, z, tb, t) + a.bias[(u64)t * a.bias_ps + ch];
+            u64 y = lin<K>(back, tb.wf) + share_raw<K, N>(0, z, tb, t) + a.bias[(u64)t * a.bias_ps + ch];
             if (t == a.fault_rank && i == 0) y += 1;                                        // test hook
-            masked[t] = lz(y + share_at<K, N>(alpha, ca, tb, t));
+            masked[t] = lz(y + share_raw<K, N>(alpha, ca, tb, t));
         }
     }
     // ---- truncation elite: rec over the front, RS check of the extra points, decode/floor/round
@@ -238,7 +244,7 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
     coeffs<K>(g, a.pseed, a.pstream + M, i);
 #pragma unroll
     for (int t = 0; t < N; t++) {
-        u64 s = share_at<K, N>(tm, g, tb, t) + share_at<K, N>(comp, cc, tb, t);
+        u64 s = share_raw<K, N>(tm, g, tb, t) + share_raw<K, N>(comp, cc, tb, t);
         if (a.other) s += a.other[(u64)t * a.other_ps + i];                              // residual add
         x[t] = lz(s);                                                                   // lazy
     }
@@ -329,7 +335,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 4) k_chain_nonlin(ChainArgs a, 
                         coeffs<K>(cb, a.sseed, a.sstream + 5, i);
                         u64 mk[M];
 #pragma unroll
-                        for (int j = 0; j < M; j++) mk[j] = mulm(x[j], share_at<K, N>(bt, cb, tb, j));
+                        for (int j = 0; j < M; j++) mk[j] = mulm(x[j], share_raw<K, N>(bt, cb, tb, j));
                         const u64 v = canon(lin<M>(mk, tb.wp));
                         i64 sv = v > PHALF ? (i64)v - (i64)PP : (i64)v;
                         if (a.relu && sv <= 0) sv = 0;
@@ -359,7 +365,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 4) k_chain_nonlin(ChainArgs a, 
 #pragma unroll
                 for (int t = 0; t < N; t++)
                     if (t < a.fan)
-                        a.out[(u64)t * a.out_ps + o] = canon(mulm(plain[q], share_at<K, N>(binv, cbi, tb, t)));
+                        a.out[(u64)t * a.out_ps + o] = canon(mulm(plain[q], share_raw<K, N>(binv, cbi, tb, t)));
             }
         }
     }
