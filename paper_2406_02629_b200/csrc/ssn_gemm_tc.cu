@@ -16,6 +16,7 @@
 // weights once per model, dense activations) and ssn_im2col_limbs (implicit conv unfold
 // S/model.py:354-371 fused with the limb split, shared-memory transposed so both the gather
 // and the plane writes are coalesced).
+#include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include "ssn_field.cuh"
@@ -432,6 +433,156 @@ k_gemm_p45(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
     __syncthreads();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
+
+// ---- wide variant: 128 x 32 tiles, N = 6 x 32 = 192 per MMA (A re-read from smem 6x less
+// than with 16-wide tiles: ~107 B/clk of operand traffic per SM), one TMEM accumulator of
+// 11 x 32 = 352 columns.  Eight epilogue warps (two per TMEM lane quarter, 16 columns each)
+// drain TMEM into registers and release it BEFORE the mod-p recombination and the stores,
+// so the next tile's MMAs overlap the arithmetic and the HBM writes.
+namespace wide {
+constexpr int BNW = 32;
+constexpr int STW = 3;
+constexpr int B_BYTES_W = L * BNW * BK;                 // 12288
+constexpr int STAGE_W = A_BYTES + B_BYTES_W;
+constexpr int SMEM_W = STW * STAGE_W + 1024 + 256;
+constexpr int THREADS_W = 320;                          // TMA, MMA, 8 epilogue warps
+
+__global__ void __launch_bounds__(THREADS_W, 1)
+k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, u64 *__restrict__ out,
+            u64 out_pstride, uint32_t ohw, int O, int M, int nkb, int ntm, int ntn, int ntiles) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t *full = reinterpret_cast<uint64_t *>(base + STW * STAGE_W);
+    uint64_t *empty = full + STW;
+    uint64_t *tfull = empty + STW;
+    uint64_t *tempty = tfull + 1;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STW; s++) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 8);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int it = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int nt = t % ntn, mt = (t / ntn) % ntm, party = t / (ntn * ntm);
+                for (int kb = 0; kb < nkb; kb++, it++) {
+                    const int s = it % STW;
+                    mbar_wait(&empty[s], ((it / STW) & 1) ^ 1);
+                    mbar_arrive_expect_tx(&full[s], STAGE_W);
+                    uint8_t *sa = base + s * STAGE_W;
+                    tma_load_4d(sa, &tmA, &full[s], kb * BK, mt * BM, 0, party);
+                    tma_load_4d(sa + A_BYTES, &tmB, &full[s], kb * BK, nt * BNW, 0, party);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t ID_ALL = idesc_i8(L * BNW), ID_HEAD = idesc_i8((L - 1) * BNW), ID_ONE = idesc_i8(BNW);
+            int it = 0, lt = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
+                mbar_wait(tempty, (lt & 1) ^ 1);
+                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                for (int kb = 0; kb < nkb; kb++, it++) {
+                    const int s = it % STW;
+                    mbar_wait(&full[s], (it / STW) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const uint32_t sa = smem_u32(base + s * STAGE_W);
+                    const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < BK / UK; kk++) {
+                        const uint64_t bdesc = umma_desc_sw64(sb + kk * UK);
+                        const bool first = kb == 0 && kk == 0;
+#pragma unroll
+                        for (int i = 0; i < L; i++) {
+                            const uint64_t adesc = umma_desc_sw64(sa + i * BM * BK + kk * UK);
+                            const uint32_t d = tmem + (uint32_t)(i * BNW);
+                            if (!first) {
+                                mma_i8(d, adesc, bdesc, ID_ALL, 1u);
+                            } else if (i == 0) {
+                                mma_i8(d, adesc, bdesc, ID_ALL, 0u);
+                            } else {
+                                mma_i8(d, adesc, bdesc, ID_HEAD, 1u);
+                                mma_i8(d + (uint32_t)((L - 1) * BNW), adesc,
+                                       umma_desc_sw64(sb + (L - 1) * BNW * BK + kk * UK), ID_ONE, 0u);
+                            }
+                        }
+                    }
+                    mma_commit(&empty[s]);
+                }
+                mma_commit(tfull);
+            }
+        }
+    } else {
+        // epilogue warps 2..9: TMEM lane quarter = warp % 4, column half = (warp - 2) / 4
+        const int q = warp & 3, half = (warp - 2) >> 2;
+        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        int lt = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
+            const int nt = t % ntn, mt = (t / ntn) % ntm, party = t / (ntn * ntm);
+            mbar_wait(tfull, lt & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t taddr = tmem + lane_off + (uint32_t)(half * 16);
+            u64 g[3][16];
+#pragma unroll
+            for (int grp = 0; grp < 3; grp++) {
+                uint32_t r[4][16];
+#pragma unroll
+                for (int dd = 0; dd < 4; dd++)
+                    if (grp * 4 + dd < ND) {
+                        asm volatile(
+                            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                            : "=r"(r[dd][0]), "=r"(r[dd][1]), "=r"(r[dd][2]), "=r"(r[dd][3]), "=r"(r[dd][4]),
+                              "=r"(r[dd][5]), "=r"(r[dd][6]), "=r"(r[dd][7]), "=r"(r[dd][8]), "=r"(r[dd][9]),
+                              "=r"(r[dd][10]), "=r"(r[dd][11]), "=r"(r[dd][12]), "=r"(r[dd][13]), "=r"(r[dd][14]),
+                              "=r"(r[dd][15])
+                            : "r"(taddr + (uint32_t)((grp * 4 + dd) * BNW)));
+                    }
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int c = 0; c < 16; c++) {
+                    u64 acc = 0;
+#pragma unroll
+                    for (int dd = 0; dd < 4; dd++)
+                        if (grp * 4 + dd < ND) acc += (u64)r[dd][c] << (8 * dd);
+                    g[grp][c] = acc;
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tempty)) : "memory");
+            const int row = mt * BM + q * 32 + lane;
+            const int c0 = nt * BNW + half * 16;
+            if (row < M) {
+                const uint32_t img = (uint32_t)row / ohw, pix = (uint32_t)row - img * ohw;
+                u64 *ob = out + (u64)party * out_pstride + ((u64)img * O + (u64)c0) * ohw + pix;
+#pragma unroll
+                for (int c = 0; c < 16; c++)
+                    if (c0 + c < O) ob[(u64)c * ohw] = combine(g[0][c], g[1][c], g[2][c]);
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+}  // namespace wide
 }  // namespace p45
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -487,16 +638,24 @@ int launch_tc(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int 
 int launch_p45(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int Kpad, u64 *out, u64 out_pstride,
                u64 ohw, cudaStream_t st) {
     using namespace p45;
+    static int variant = -1;            // 1: wide 128x32 tiles (default), 0: 128x16 double-buffered
+    if (variant < 0) {
+        const char *e = getenv("SSN_GEMM_VARIANT");
+        variant = (e && e[0] == '0') ? 0 : 1;
+    }
+    const int bn = variant ? wide::BNW : BN2;
     CUtensorMap ma, mb;
-    if (make_map(&ma, a, Kpad, M, L, nparty, BM) || make_map(&mb, b, Kpad, O, L, nparty, BN2)) return SSN_ERR_CUDA;
+    if (make_map(&ma, a, Kpad, M, L, nparty, BM) || make_map(&mb, b, Kpad, O, L, nparty, bn)) return SSN_ERR_CUDA;
     static bool attr = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(k_gemm_p45, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess)
+        if (cudaFuncSetAttribute(k_gemm_p45, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess ||
+            cudaFuncSetAttribute(wide::k_gemm_p45w, cudaFuncAttributeMaxDynamicSharedMemorySize, wide::SMEM_W) !=
+                cudaSuccess)
             return SSN_ERR_CUDA;
         attr = true;
     }
     if (ohw >= (1ull << 32) || (u64)M * 1 >= (1ull << 31)) return SSN_ERR_UNSUPPORTED;
-    const int ntm = (M + BM - 1) / BM, ntn = (O + BN2 - 1) / BN2;
+    const int ntm = (M + BM - 1) / BM, ntn = (O + bn - 1) / bn;
     const long long ntiles = (long long)ntm * ntn * nparty;
     if (ntiles >= (1ll << 31)) return SSN_ERR_UNSUPPORTED;
     static int nsm = 0;
@@ -506,8 +665,12 @@ int launch_p45(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
     const int grid = (int)(ntiles < nsm ? ntiles : nsm);
-    k_gemm_p45<<<grid, THREADS, SMEM, st>>>(ma, mb, out, out_pstride, (uint32_t)ohw, O, M, (Kpad + BK - 1) / BK, ntm,
-                                            ntn, (int)ntiles);
+    if (variant)
+        wide::k_gemm_p45w<<<grid, wide::THREADS_W, wide::SMEM_W, st>>>(ma, mb, out, out_pstride, (uint32_t)ohw, O, M,
+                                                                    (Kpad + BK - 1) / BK, ntm, ntn, (int)ntiles);
+    else
+        k_gemm_p45<<<grid, THREADS, SMEM, st>>>(ma, mb, out, out_pstride, (uint32_t)ohw, O, M, (Kpad + BK - 1) / BK,
+                                                ntm, ntn, (int)ntiles);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
 
