@@ -292,7 +292,7 @@ __device__ __forceinline__ u64 warp_excl_suffix(u64 v, int lane) {
 // from ONE Fermat inversion: per-thread running products over its WPT windows, warp-shuffle
 // exclusive prefix/suffix products across lanes (Montgomery's batch trick), then a backward
 // pass.  No block barrier: warps never wait for each other.
-constexpr int WPT = 4;
+constexpr int WPT = 8;
 
 template <int K, int N>
 __global__ void __launch_bounds__(CHAIN_THREADS, 4) k_chain_nonlin(ChainArgs a, const __grid_constant__ STables<K, N> tb,
