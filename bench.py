@@ -472,6 +472,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--streams", type=int, default=1,
+                    help="co-resident: split the batch over this many CUDA streams (GEMM/chain overlap)")
     ap.add_argument("--placement", default="coresident", choices=["coresident", "party"],
                     help="coresident: every GPU runs all n parties on its own batch (default); "
                          "party: one GPU per party + one for the trusted source, NCCL p2p per hop, "
@@ -501,7 +503,11 @@ def main():
     B = args.batch or dflt_batch
     model = build_model(kind)
     scheme = SssScheme(PrimeField(), k, n)
-    eng = BatchedEngine(model, scheme, batch=B, seed=7 + rank, verify=verify)
+    if args.streams > 1:
+        from paper_2406_02629_b200.batched import StreamPipelinedEngine
+        eng = StreamPipelinedEngine(model, scheme, batch=B, streams=args.streams, seed=7 + rank, verify=verify)
+    else:
+        eng = BatchedEngine(model, scheme, batch=B, seed=7 + rank, verify=verify)
     shape = (B,) + tuple(model.input_shape)
     if hasattr(model, "random_inputs"):
         xb = model.random_inputs(seed=100 + rank, batch=B)

@@ -47,7 +47,7 @@ def _count(shape):
 
 class BatchedEngine:
     def __init__(self, model, scheme, batch, seed=7, rng_mode="device", verify=False, ordering="ltn",
-                 profile=False, fuse=True):
+                 profile=False, fuse=True, share_weights_with=None):
         if rng_mode != "device":
             raise ValueError("the batched engine draws its randomness on the device (rng_mode='device'); "
                              "use simulate_inference for reference-stream parity runs")
@@ -72,8 +72,11 @@ class BatchedEngine:
         self.ids_front = _lib.u64_array(scheme.front_ids)
         self.runs = 0
         self.fail = torch.zeros(1, dtype=torch.int64, device=self.dev)
-        self._planes = {}
-        self._deal_weights()
+        if share_weights_with is not None:      # same dealt weight shares / limb planes (read-only)
+            self.W, self._planes = share_weights_with.W, share_weights_with._planes
+        else:
+            self._planes = {}
+            self._deal_weights()
         self.kernel_launches = 0
         self.fault = None
         self.fuse = fuse
@@ -512,3 +515,62 @@ class BatchedEngine:
         if bad:
             self.fail.zero_()
             raise VerificationError(f"{bad} share(s) failed the Reed-Solomon check")
+
+
+class StreamPipelinedEngine:
+    """S BatchedEngines on S CUDA streams, each on 1/S of the batch.  The share GEMMs are
+    tensor-pipe bound and the fused protocol chains integer-ALU bound, so kernels of different
+    streams co-reside on the SMs (the persistent GEMM leaves registers for a chain block) and
+    overlap.  Weight shares and limb planes are shared.  Same outputs as one engine."""
+
+    def __init__(self, model, scheme, batch, streams=2, seed=7, verify=False, **kw):
+        if batch % streams:
+            raise ValueError(f"batch {batch} not divisible by {streams} streams")
+        self.batch, self.nstreams = batch, streams
+        first = BatchedEngine(model, scheme, batch // streams, seed=seed, verify=verify, **kw)
+        self.engines = [first] + [BatchedEngine(model, scheme, batch // streams, seed=seed + 1000 * i, verify=verify,
+                                                share_weights_with=first, **kw) for i in range(1, streams)]
+        self.streams = [torch.cuda.Stream() for _ in range(streams)]
+        self.scheme, self.ops = scheme, first.ops
+
+    def __getattr__(self, name):                  # out_shape, comm_per_image, limb_products, ...
+        return getattr(self.engines[0], name)
+
+    def run(self, x_int, timings=None):
+        return self.run_device(x_int).cpu().numpy()
+
+    def run_device(self, x_int, timings=None):
+        if not isinstance(x_int, torch.Tensor):
+            x_int = torch.as_tensor(np.asarray(x_int, dtype=np.int64))
+        x = x_int.to(device=self.engines[0].dev, dtype=torch.int64)
+        cur = torch.cuda.current_stream()
+        parts = x.chunk(self.nstreams)
+        outs = []
+        for eng, st, xp in zip(self.engines, self.streams, parts):
+            st.wait_stream(cur)
+            with torch.cuda.stream(st):
+                outs.append(eng.run_device(xp))
+        for st, o in zip(self.streams, outs):
+            cur.wait_stream(st)
+            o.record_stream(cur)
+        return torch.cat(outs)
+
+    def enable_profiling(self):
+        for e in self.engines:
+            e.enable_profiling()
+
+    def disable_profiling(self):
+        for e in self.engines:
+            e.disable_profiling()
+
+    def profile_summary(self, steps):
+        merged = {}
+        for e in self.engines:
+            for cls, rec in (e._prof or {}).items():
+                merged.setdefault(cls, []).extend(rec)
+        e0 = self.engines[0]
+        saved, e0._prof = e0._prof, merged
+        try:
+            return e0.profile_summary(steps)
+        finally:
+            e0._prof = saved
