@@ -145,6 +145,23 @@ int ssn_im2col_limbs(const uint64_t *x, int nparty, int nimg, int C, int H, int 
 int ssn_gemm_tc(const uint8_t *a_planes, const uint8_t *b_planes, int nparty, int L, int M, int O, uint64_t Kpad,
                 uint64_t ohw, uint64_t *out, uint64_t out_pstride, uint64_t p, void *stream);
 
+/* Implicit-GEMM convolution on the tensor cores from CHANNEL-MAJOR limb planes (the A operand
+ * is M-major: TMA loads 128 consecutive output pixels x 64 channels per limb; p = 2^45 - 55):
+ *  mode 1 (1x1, stride 1, pad 0): a_planes [party][L][C][nimg*H*W];
+ *  mode 2 (3x3, stride 1, pad 1): a_planes [3][party][L][C][nimg][H][Wp], Wp > W, Wp % 16 == 0:
+ *    copy dx holds the rows shifted by dx - 1 columns, zero where the shift leaves the image
+ *    (that and TMA's out-of-range zero fill for rows are the convolution's zero padding).
+ * b_planes [party][L][O][taps*C] with k = tap*C + c (tap = dy*3 + dx; weights (O,C,kh,kw)
+ * permuted to (O,kh,kw,C)).  out as ssn_gemm_tc with ohw = H*W.  C % 64 == 0.
+ * Replaces im2col + GEMM of sss_linear (S/model.py:354-371, S/layers.py:252). */
+int ssn_gemm_tc_conv(const uint8_t *a_planes, int mode, int nimg, int C, int H, int W, int Wp, const uint8_t *b_planes,
+                     int nparty, int O, uint64_t *out, uint64_t out_pstride, uint64_t p, void *stream);
+/* x [party][img][C][H][W] -> channel-major limb planes [copies][party][L][C][img][H][Wp].
+ * copies == 1 (Wp == W: the contiguous mode-1 layout) or 3 (mode 2: copy dx at column x+1-dx);
+ * unwritten bytes are untouched -- the caller zeroes the buffer once. */
+int ssn_planes_cn(const uint64_t *x, int nparty, int nimg, int C, int H, int W, int Wp, int L, uint8_t *planes,
+                  uint64_t x_pstride, int copies, void *stream);
+
 /* Fused per-layer protocol chain for co-resident parties (one launch per secure layer after
  * its share GEMM).  Per element i of the linear op's output, for all n parties at once:
  *   reshare_degree_reduce (S/protocol.py:131-199): participant j (j < m = 2k-1) sub-shares

@@ -73,6 +73,8 @@ _SIGS = {
     "ssn_im2col_limbs": [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _U64, _U64, _P],
     "ssn_gemm_tc": [_P, _P, _I32, _I32, _I32, _I32, _U64, _U64, _P, _U64, _U64, _P],
     "ssn_layer_chain": [_P, _P],
+    "ssn_gemm_tc_conv": [_P, _I32, _I32, _I32, _I32, _I32, _I32, _P, _I32, _I32, _P, _U64, _U64, _P],
+    "ssn_planes_cn": [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _U64, _I32, _P],
     "ssn_chain_supported": [_I32, _I32, _P, _U64],
 }
 

@@ -63,6 +63,26 @@ __device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, u
         : "memory");
 }
 
+__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                            int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+
+// UMMA shared-memory descriptor for an MN-major (M contiguous) operand, 128-byte swizzle:
+// each K row holds 128 M-bytes, 8-row (1 KB) swizzle atoms stacked along K (SBO = 1 KB).
+__device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);          // start address
+    d |= (uint64_t)0 << 16;                          // LBO: one atom along M (unused)
+    d |= (uint64_t)(1024 >> 4) << 32;                // SBO: next 8 K rows
+    d |= (uint64_t)1 << 46;                          // version (sm_100)
+    d |= (uint64_t)2 << 61;                          // SWIZZLE_128B
+    return d;
+}
+
 // UMMA shared-memory descriptor: K-major, 64-byte swizzle, 8-row core groups 512 B apart.
 __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
     uint64_t d = 0;
@@ -447,9 +467,20 @@ constexpr int STAGE_W = A_BYTES + B_BYTES_W;
 constexpr int SMEM_W = STW * STAGE_W + 1024 + 256;
 constexpr int THREADS_W = 320;                          // TMA, MMA, 8 epilogue warps
 
+// A operand modes: 0 = K-major limb planes [party][L][rows][Kpad] (explicit im2col / dense);
+// 1 = channel-major planes [party*L][C][B*H*W] of a 1x1 stride-1 conv input (M-major, TMA 3-D);
+// 2 = channel-major row-padded planes [3][party*L][C][B][H*Wp] (Wp > W) of a 3x3 stride-1
+//     pad-1 conv input, copy dx holding the rows shifted by dx - 1 columns (zero where the shift
+//     leaves the image): implicit GEMM, tap (dy, dx) reads copy dx at a flattened (y, x) offset
+//     of (dy-1)*Wp; out-of-range rows are TMA zero fill -- the convolution's zero padding.
+struct ConvGeom {
+    int C, H, W, Wp, cblocks, ntf, nparty;   // ntf: 128-row tiles per image (mode 2)
+};
+
+template <int AMODE>
 __global__ void __launch_bounds__(THREADS_W, 1)
 k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, u64 *__restrict__ out,
-            u64 out_pstride, uint32_t ohw, int O, int M, int nkb, int ntm, int ntn, int ntiles) {
+            u64 out_pstride, uint32_t ohw, int O, int M, int nkb, int ntm, int ntn, int ntiles, ConvGeom geo) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *full = reinterpret_cast<uint64_t *>(base + STW * STAGE_W);
@@ -487,14 +518,28 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     mbar_wait(&empty[s], ((it / STW) & 1) ^ 1);
                     mbar_arrive_expect_tx(&full[s], STAGE_W);
                     uint8_t *sa = base + s * STAGE_W;
-                    tma_load_4d(sa, &tmA, &full[s], kb * BK, mt * BM, 0, party);
+                    if (AMODE == 0) {
+                        tma_load_4d(sa, &tmA, &full[s], kb * BK, mt * BM, 0, party);
+                    } else if (AMODE == 1) {
+                        tma_load_3d(sa, &tmA, &full[s], mt * BM, kb * BK, party * L);
+                    } else {
+                        const int tap = kb / geo.cblocks, cb = kb - tap * geo.cblocks;
+                        const int dy = tap / 3, dx = tap - dy * 3;
+                        const int img = mt / geo.ntf, ft = mt - img * geo.ntf;
+                        // column shift dx - 1 comes from the dx-th pre-shifted copy (TMA inner
+                        // coordinates must stay 16-byte aligned); the row shift is (dy - 1) * Wp
+                        tma_load_4d(sa, &tmA, &full[s], ft * BM + (dy - 1) * geo.Wp, img, cb * BK,
+                                    (dx * geo.nparty + party) * L);
+                    }
                     tma_load_4d(sa + A_BYTES, &tmB, &full[s], kb * BK, nt * BNW, 0, party);
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            constexpr uint32_t ID_ALL = idesc_i8(L * BNW), ID_HEAD = idesc_i8((L - 1) * BNW), ID_ONE = idesc_i8(BNW);
+            constexpr uint32_t AM = AMODE ? (1u << 15) : 0u;          // A major-ness: MN for conv planes
+            constexpr uint32_t ID_ALL = idesc_i8(L * BNW) | AM, ID_HEAD = idesc_i8((L - 1) * BNW) | AM,
+                               ID_ONE = idesc_i8(BNW) | AM;
             int it = 0, lt = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
                 mbar_wait(tempty, (lt & 1) ^ 1);
@@ -511,7 +556,8 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         const bool first = kb == 0 && kk == 0;
 #pragma unroll
                         for (int i = 0; i < L; i++) {
-                            const uint64_t adesc = umma_desc_sw64(sa + i * BM * BK + kk * UK);
+                            const uint64_t adesc = AMODE ? umma_desc_sw128_mn(sa + i * BM * BK + kk * UK * BM)
+                                                         : umma_desc_sw64(sa + i * BM * BK + kk * UK);
                             const uint32_t d = tmem + (uint32_t)(i * BNW);
                             if (!first) {
                                 mma_i8(d, adesc, bdesc, ID_ALL, 1u);
@@ -567,10 +613,23 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tempty)) : "memory");
-            const int row = mt * BM + q * 32 + lane;
+            const int v = q * 32 + lane;
             const int c0 = nt * BNW + half * 16;
-            if (row < M) {
-                const uint32_t img = (uint32_t)row / ohw, pix = (uint32_t)row - img * ohw;
+            bool ok;
+            uint32_t img, pix;
+            if (AMODE == 2) {
+                img = (uint32_t)(mt / geo.ntf);
+                const int f = (mt - (int)img * geo.ntf) * BM + v;
+                const int y = f / geo.Wp, x = f - y * geo.Wp;
+                ok = y < geo.H && x < geo.W;
+                pix = (uint32_t)(y * geo.W + x);
+            } else {
+                const int row = mt * BM + v;
+                ok = row < M;
+                img = (uint32_t)row / ohw;
+                pix = (uint32_t)row - img * ohw;
+            }
+            if (ok) {
                 u64 *ob = out + (u64)party * out_pstride + ((u64)img * O + (u64)c0) * ohw + pix;
 #pragma unroll
                 for (int c = 0; c < 16; c++)
@@ -649,7 +708,7 @@ int launch_p45(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(k_gemm_p45, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess ||
-            cudaFuncSetAttribute(wide::k_gemm_p45w, cudaFuncAttributeMaxDynamicSharedMemorySize, wide::SMEM_W) !=
+            cudaFuncSetAttribute(wide::k_gemm_p45w<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, wide::SMEM_W) !=
                 cudaSuccess)
             return SSN_ERR_CUDA;
         attr = true;
@@ -666,11 +725,88 @@ int launch_p45(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int
     }
     const int grid = (int)(ntiles < nsm ? ntiles : nsm);
     if (variant)
-        wide::k_gemm_p45w<<<grid, wide::THREADS_W, wide::SMEM_W, st>>>(ma, mb, out, out_pstride, (uint32_t)ohw, O, M,
-                                                                    (Kpad + BK - 1) / BK, ntm, ntn, (int)ntiles);
+        wide::k_gemm_p45w<0><<<grid, wide::THREADS_W, wide::SMEM_W, st>>>(
+            ma, mb, out, out_pstride, (uint32_t)ohw, O, M, (Kpad + BK - 1) / BK, ntm, ntn, (int)ntiles, wide::ConvGeom{});
     else
         k_gemm_p45<<<grid, THREADS, SMEM, st>>>(ma, mb, out, out_pstride, (uint32_t)ohw, O, M, (Kpad + BK - 1) / BK,
                                                 ntm, ntn, (int)ntiles);
+    return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
+}
+
+static int num_sms() {
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    return nsm;
+}
+
+// Implicit-GEMM convolution from channel-major limb planes (modes 1 and 2 of k_gemm_p45w).
+int launch_cn(const uint8_t *a, int mode, int nimg, int C, int H, int W, int Wp, const uint8_t *b, int nparty, int O,
+              u64 *out, u64 out_pstride, cudaStream_t st) {
+    using namespace p45;
+    auto enc = get_encode();
+    if (!enc) return SSN_ERR_CUDA;
+    if (C % BK) return SSN_ERR_UNSUPPORTED;
+    const int taps = mode == 2 ? 9 : 1;
+    const int Kpad = taps * C;
+    CUtensorMap ma, mb;
+    const cuuint64_t PL = (cuuint64_t)nparty * L;
+    CUresult r;
+    if (mode == 1) {
+        const cuuint64_t bhw = (cuuint64_t)nimg * H * W;
+        if (bhw % 16) return SSN_ERR_UNSUPPORTED;
+        cuuint64_t dims[3] = {bhw, (cuuint64_t)C, PL};
+        cuuint64_t strides[2] = {bhw, bhw * C};
+        cuuint32_t box[3] = {(cuuint32_t)BM, (cuuint32_t)BK, (cuuint32_t)L};
+        cuuint32_t estr[3] = {1, 1, 1};
+        r = enc(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t *>(a), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        if (Wp <= W || Wp % 16 || ((u64)H * Wp) % 16) return SSN_ERR_UNSUPPORTED;
+        const cuuint64_t hw = (cuuint64_t)H * Wp;
+        cuuint64_t dims[4] = {hw, (cuuint64_t)nimg, (cuuint64_t)C, 3 * PL};
+        cuuint64_t strides[3] = {hw, hw * nimg, hw * nimg * C};
+        cuuint32_t box[4] = {(cuuint32_t)BM, 1, (cuuint32_t)BK, (cuuint32_t)L};
+        cuuint32_t estr[4] = {1, 1, 1, 1};
+        r = enc(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t *>(a), dims, strides, box, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    if (r != CUDA_SUCCESS) return SSN_ERR_CUDA;
+    if (make_map(&mb, b, Kpad, O, L, nparty, wide::BNW)) return SSN_ERR_CUDA;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(wide::k_gemm_p45w<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, wide::SMEM_W) !=
+                cudaSuccess ||
+            cudaFuncSetAttribute(wide::k_gemm_p45w<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, wide::SMEM_W) !=
+                cudaSuccess)
+            return SSN_ERR_CUDA;
+        attr = true;
+    }
+    wide::ConvGeom geo{C, H, W, Wp, C / BK, 0, nparty};
+    const int M = nimg * H * W;
+    int ntm;
+    if (mode == 1) {
+        ntm = (M + BM - 1) / BM;
+    } else {
+        geo.ntf = (H * Wp + BM - 1) / BM;
+        ntm = nimg * geo.ntf;
+    }
+    const int ntn = (O + wide::BNW - 1) / wide::BNW;
+    const long long ntiles = (long long)ntm * ntn * nparty;
+    if (ntiles >= (1ll << 31)) return SSN_ERR_UNSUPPORTED;
+    const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
+    const uint32_t ohw = (uint32_t)(H * W);
+    if (mode == 1)
+        wide::k_gemm_p45w<1><<<grid, wide::THREADS_W, wide::SMEM_W, st>>>(ma, mb, out, out_pstride, ohw, O, M, taps * geo.cblocks,
+                                                                       ntm, ntn, (int)ntiles, geo);
+    else
+        wide::k_gemm_p45w<2><<<grid, wide::THREADS_W, wide::SMEM_W, st>>>(ma, mb, out, out_pstride, ohw, O, M, taps * geo.cblocks,
+                                                                       ntm, ntn, (int)ntiles, geo);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
 
@@ -769,7 +905,44 @@ __global__ void __launch_bounds__(IC_THREADS) k_im2col_limbs(const u64 *__restri
     }
 }
 
+// x [P][img][C][H][W] u64 -> channel-major limb planes [P][L][C][img][H][Wp] (Wp >= W; pad
+// columns untouched: the caller zeroes the buffer once).  Wp == W gives the contiguous layout
+// [P][L][C][img*H*W] of mode 1.
+__global__ void k_planes_cn(const u64 *__restrict__ x, int nimg, int C, int H, int W, int Wp, int L,
+                            uint8_t *__restrict__ planes, u64 x_pstride, u64 total, int copies, int nparty) {
+    const u64 per_party = (u64)nimg * C * H * W;
+    const u64 plane = (u64)C * nimg * H * Wp;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < total; i += (u64)gridDim.x * blockDim.x) {
+        const u64 party = i / per_party;
+        const u64 r = i - party * per_party;
+        const uint32_t xx = (uint32_t)(r % W);
+        const u64 r2 = r / W;
+        const uint32_t y = (uint32_t)(r2 % H);
+        const u64 r3 = r2 / H;
+        const uint32_t c = (uint32_t)(r3 % C), img = (uint32_t)(r3 / C);
+        const u64 v = x[party * x_pstride + r];
+        for (int dx = 0; dx < copies; dx++) {
+            const int xc = copies == 1 ? (int)xx : (int)xx + 1 - dx;     // copy dx holds column x + dx - 1
+            if (xc < 0 || xc >= Wp) continue;
+            uint8_t *dst = planes + ((u64)dx * nparty + party) * L * plane + (((u64)c * nimg + img) * H + y) * Wp + xc;
+            for (int l = 0; l < L; l++) dst[(u64)l * plane] = (uint8_t)(v >> (8 * l));
+        }
+    }
+}
+
 }  // namespace
+
+extern "C" int ssn_planes_cn(const u64 *x, int nparty, int nimg, int C, int H, int W, int Wp, int L, uint8_t *planes,
+                             u64 x_pstride, int copies, void *stream) {
+    if (nparty < 1 || nimg < 1 || C < 1 || H < 1 || W < 1 || Wp < W || L < 1 || L > MAXL) return SSN_ERR_ARG;
+    if (copies != 1 && (copies != 3 || Wp <= W)) return SSN_ERR_ARG;
+    const u64 total = (u64)nparty * nimg * C * H * W;
+    u64 blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_planes_cn<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, nimg, C, H, W, Wp, L, planes, x_pstride, total,
+                                                                     copies, nparty);
+    return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
+}
 
 extern "C" int ssn_limb_split(const u64 *x, u64 rows, u64 K, u64 Kpad, int L, uint8_t *planes, u64 x_pstride,
                               int nparty, void *stream) {
@@ -794,6 +967,14 @@ extern "C" int ssn_im2col_limbs(const u64 *x, int nparty, int nimg, int C, int H
     k_im2col_limbs<<<grid, IC_THREADS, 0, (cudaStream_t)stream>>>(x, C, H, W, kh, kw, stride, pad, OH, OW, L,
                                                                   (uint32_t)rows, K, (int)Kpad, planes, x_pstride);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
+}
+
+extern "C" int ssn_gemm_tc_conv(const uint8_t *a_planes, int mode, int nimg, int C, int H, int W, int Wp,
+                                const uint8_t *b_planes, int nparty, int O, u64 *out, u64 out_pstride, u64 p,
+                                void *stream) {
+    if ((mode != 1 && mode != 2) || nimg < 1 || C < 1 || H < 1 || W < 1 || nparty < 1 || O < 1) return SSN_ERR_ARG;
+    if (p != p45::P) return SSN_ERR_UNSUPPORTED;
+    return launch_cn(a_planes, mode, nimg, C, H, W, Wp, b_planes, nparty, O, out, out_pstride, (cudaStream_t)stream);
 }
 
 // planes A [P][L][M][Kpad] (rows = activation pixels), B [P][L][O][Kpad] (weights);

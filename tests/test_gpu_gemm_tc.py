@@ -84,3 +84,33 @@ def test_conv_tc_vs_simt(g, C, H, W, O, k, s, pad, nimg, nparty):
     want = oracle.gemm(w[0].reshape(O, -1), oracle.im2col(x[0, 0], k, k, s, pad))
     got = host(tc).reshape(nparty, nimg, O, -1)[0, 0] if (nparty > 1 or nimg > 1) else host(tc).reshape(O, -1)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("kh,C,H,W,O", [(1, 64, 56, 56, 64), (1, 128, 14, 14, 96), (3, 64, 56, 56, 64),
+                                        (3, 128, 28, 28, 128), (3, 64, 14, 14, 32)])
+def test_implicit_conv_planes_vs_im2col(kh, C, H, W, O):
+    """Implicit GEMM from channel-major planes (TMA M-major A, modes 1 and 2) equals the
+    explicit im2col + tcgen05 GEMM path bit for bit, including the zero padding of 3x3."""
+    import torch
+    from paper_2406_02629_b200 import _lib, gemm as G
+    p = (1 << 45) - 55
+    rng = np.random.default_rng(C + H + O + kh)
+    nparty, B = 2, 4          # mode 1 needs B*H*W % 16 == 0 (TMA stride alignment)
+    x = torch.as_tensor(rng.integers(0, p, size=(nparty, B, C, H, W)), device="cuda")
+    w = torch.as_tensor(rng.integers(0, p, size=(nparty, O, C, kh, kh)), device="cuda")
+    pad = (kh - 1) // 2
+    want = G.field_conv(w, x, 1, pad, p, nimg=B, nparty=nparty, force="tc")
+    mode = 1 if kh == 1 else 2
+    Wp = W if mode == 1 else (W + 16) // 16 * 16
+    L = G.limbs(p)
+    copies = 1 if mode == 1 else 3
+    planes = torch.zeros((copies, nparty, L, C, B, H, Wp), dtype=torch.uint8, device="cuda")
+    _lib.call("ssn_planes_cn", _lib.ptr(x), nparty, B, C, H, W, Wp, L, _lib.ptr(planes), B * C * H * W,
+              copies, _lib.stream_ptr())
+    wt = w.permute(0, 1, 3, 4, 2).contiguous().reshape(nparty, O, kh * kh * C)
+    bpl = G.weight_planes(wt, p, nparty)
+    out = torch.empty((nparty, B, O, H, W), dtype=torch.int64, device="cuda")
+    _lib.call("ssn_gemm_tc_conv", _lib.ptr(planes), mode, B, C, H, W, Wp, _lib.ptr(bpl), nparty, O, _lib.ptr(out),
+              B * O * H * W, p, _lib.stream_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(out, want)
