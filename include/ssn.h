@@ -161,6 +161,9 @@ int ssn_gemm_tc_conv(const uint8_t *a_planes, int mode, int nimg, int C, int H, 
  * unwritten bytes are untouched -- the caller zeroes the buffer once. */
 int ssn_planes_cn(const uint64_t *x, int nparty, int nimg, int C, int H, int W, int Wp, int L, uint8_t *planes,
                   uint64_t x_pstride, int copies, void *stream);
+/* Fill mode-2 copies 0 and 2 from copy 1 (planes [3][rows][Wp], rows = party*L*C*img*H): the
+ * +-1 column shifts, 16-byte vectorised. */
+int ssn_planes_shift(uint8_t *planes, uint64_t rows, int Wp, void *stream);
 
 /* Fused per-layer protocol chain for co-resident parties (one launch per secure layer after
  * its share GEMM).  Per element i of the linear op's output, for all n parties at once:
@@ -204,6 +207,13 @@ typedef struct ssn_chain_desc {
     const uint64_t *ids, *rt, *ext;
     uint64_t p;
     int fault_rank;   /* test hook: < 0 off; else rank's reshared share of element 0 is corrupted */
+    /* optional (nonlin chains): channel-major u8 limb planes of the output for the next
+     * implicit-GEMM conv (ssn_gemm_tc_conv), participants t < plane_nparty, 6 limbs:
+     * planes[(dx*plane_nparty + t)*plane_pstride + l*plane_lstride + c*plane_cstride
+     *        + img*plane_istride + y*plane_wp + x + 1 - dx] for plane_copies copies (1: x). */
+    uint8_t *planes;
+    uint64_t plane_pstride, plane_lstride, plane_cstride, plane_istride;
+    int plane_wp, plane_copies, plane_nparty;
 } ssn_chain_desc;
 
 int ssn_layer_chain(const ssn_chain_desc *desc, void *stream);

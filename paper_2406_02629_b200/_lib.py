@@ -74,6 +74,7 @@ _SIGS = {
     "ssn_gemm_tc": [_P, _P, _I32, _I32, _I32, _I32, _U64, _U64, _P, _U64, _U64, _P],
     "ssn_layer_chain": [_P, _P],
     "ssn_gemm_tc_conv": [_P, _I32, _I32, _I32, _I32, _I32, _I32, _P, _I32, _I32, _P, _U64, _U64, _P],
+    "ssn_planes_shift": [_P, _U64, _I32, _P],
     "ssn_planes_cn": [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _U64, _I32, _P],
     "ssn_chain_supported": [_I32, _I32, _P, _U64],
 }
@@ -100,6 +101,9 @@ class ChainDesc(ctypes.Structure):
         ("ids", _P), ("rt", _P), ("ext", _P),
         ("p", _U64),
         ("fault_rank", _I32),
+        ("planes", _P),
+        ("plane_pstride", _U64), ("plane_lstride", _U64), ("plane_cstride", _U64), ("plane_istride", _U64),
+        ("plane_wp", _I32), ("plane_copies", _I32), ("plane_nparty", _I32),
     ]
 
 _lib = None

@@ -47,7 +47,7 @@ def _count(shape):
 
 class BatchedEngine:
     def __init__(self, model, scheme, batch, seed=7, rng_mode="device", verify=False, ordering="ltn",
-                 profile=False, fuse=True, share_weights_with=None):
+                 profile=False, fuse=True, share_weights_with=None, implicit=True):
         if rng_mode != "device":
             raise ValueError("the batched engine draws its randomness on the device (rng_mode='device'); "
                              "use simulate_inference for reference-stream parity runs")
@@ -83,6 +83,7 @@ class BatchedEngine:
         self.chains = self._plan_chains() if fuse else {}
         self._chain_member = {i: start for start, ch in self.chains.items() for i in ch[1:]}
         self._rt_all = _lib.u64_array([R[i][t] for t in range(n) for i in range(self.m)])
+        self._plan_implicit_convs(implicit)
         self._ext_host = _lib.u64_array(self.ext) if self.ext else None
 
     # ------------------------------------------------------------------ setup
@@ -106,6 +107,89 @@ class BatchedEngine:
         ovf = torch.zeros(1, dtype=torch.int64, device=self.dev)
         _lib.call("ssn_encode_signed", _lib.ptr(v), _lib.ptr(out), v.numel(), _lib.ptr(ovf), self.p,
                   _lib.stream_ptr())
+        return out
+
+    # ------------------------------------------------------------------ implicit-GEMM convs
+    IMPLICIT_MIN_W = 14          # 3x3 row-padded tiles waste (Wp - W)/Wp; below 14x14 use im2col
+
+    def _plan_implicit_convs(self, enabled):
+        """Convs whose A operand is read straight from channel-major limb planes (no im2col):
+        1x1/stride 1 (mode 1) and 3x3/stride 1/pad 1 (mode 2).  The planes are emitted by the
+        producing chain kernel, or by ssn_planes_cn from the u64 shares otherwise."""
+        self._conv_mode, self._plane_src, self._plane_buf, self._planes_ready = {}, {}, {}, set()
+        if not enabled or not gemm_mod.conv_planes_supported(self.p):
+            return
+        B = self.batch
+        wants = {}
+        for idx, op in enumerate(self.ops):
+            if op.kind != "linear":
+                continue
+            w = self.W[op.weight + ".w"]
+            if w.dim() != 5 or len(op.in_shape) != 3:
+                continue
+            C, H, Wd = op.in_shape
+            kh = int(w.shape[-1])
+            if C % 64 or B * H * Wd >= (1 << 31) or not gemm_mod.use_tc(self.p, B * H * Wd, C * kh * kh,
+                                                                     op.out_shape[0]):
+                continue
+            if kh == 1 and op.stride == 1 and op.padding == 0 and (B * H * Wd) % 16 == 0:
+                mode = (1, Wd, 1)
+            elif kh == 3 and op.stride == 1 and op.padding == 1 and Wd >= self.IMPLICIT_MIN_W:
+                mode = (2, (Wd // 16 + 1) * 16, 3)
+            else:
+                continue
+            src = idx - 1 if op.src is None else op.src
+            wants.setdefault(src, []).append((idx, mode, (C, H, Wd)))
+        for src, lst in wants.items():
+            if len({m for _, m, _ in lst}) != 1:      # consumers disagree on the layout: im2col
+                continue
+            for idx, mode, _ in lst:
+                self._conv_mode[idx] = (src,) + mode
+            self._plane_src[src] = lst[0][1] + lst[0][2]
+
+    def _plane_buffer(self, src):
+        """Persistent zeroed planes [copies][m][L][C][B][H][Wp] for producer `src` (pad bytes
+        are never written, so they stay zero across runs)."""
+        buf = self._plane_buf.get(src)
+        if buf is None:
+            mode, Wp, copies, C, H, Wd = self._plane_src[src]
+            L = gemm_mod.limbs(self.p)
+            buf = self._plane_buf[src] = torch.zeros((copies, self.m, L, C, self.batch, H, Wp), dtype=torch.uint8,
+                                                     device=self.dev)
+        return buf
+
+    def _conv_weight_planes(self, op, mode):
+        key = (op.weight, "cn", mode)
+        pl = self._planes.get(key)
+        if pl is None:
+            w = self.W[op.weight + ".w"][:self.m]
+            O, C, kh, kw = w.shape[1:]
+            wt = w.permute(0, 1, 3, 4, 2).contiguous().reshape(self.m, O, kh * kw * C)   # k = (tap, c)
+            pl = self._planes[key] = gemm_mod.weight_planes(wt, self.p, self.m)
+        return pl
+
+    def _gemm_implicit(self, idx, op, X):
+        src, mode, Wp, copies = self._conv_mode[idx]
+        B, m, p = self.batch, self.m, self.p
+        C, H, Wd = op.in_shape
+        O = op.out_shape[0]
+        buf = self._plane_buffer(src)
+        prof = self._prof is not None
+        if src not in self._planes_ready:                 # producer was not a plane-emitting chain
+            e0 = self._event() if prof else None
+            _lib.call("ssn_planes_cn", _lib.ptr(X), m, B, C, H, Wd, Wp, gemm_mod.limbs(p), _lib.ptr(buf),
+                      B * C * H * Wd, copies, _lib.stream_ptr())
+            if prof:
+                self._record("im2col", e0, self._event(), (8 + 6 * copies) * m * B * C * H * Wd, "k_planes_cn")
+            self._planes_ready.add(src)
+        bpl = self._conv_weight_planes(op, mode)
+        out = torch.empty((m, B, O, H, Wd), dtype=torch.int64, device=self.dev)
+        e0 = self._event() if prof else None
+        _lib.call("ssn_gemm_tc_conv", _lib.ptr(buf), mode, B, C, H, Wd, Wp, _lib.ptr(bpl), m, O, _lib.ptr(out),
+                  B * O * H * Wd, p, _lib.stream_ptr())
+        if prof:
+            K = C * (9 if mode == 2 else 1)
+            self._record("gemm", e0, self._event(), m * B * H * Wd * O * K, f"k_gemm_p45w<{mode}>")
         return out
 
     # ------------------------------------------------------------------ fused chains
@@ -193,8 +277,25 @@ class BatchedEngine:
         d.ext = ctypes.addressof(self._ext_host) if self._ext_host is not None else None
         d.p = p
         d.fault_rank = self.fault[1] if (self.fault is not None and self.fault[0] == chain[0]) else -1
+        shift_rows = 0
+        ps = self._plane_src.get(chain[-1])
+        if ps is not None and nl is not None and tuple(last.out_shape) == tuple(ps[3:]):
+            _, Wp, copies, C2, H2, W2 = ps
+            buf = self._plane_buffer(chain[-1])
+            # the chain writes the unshifted copy (index 1 of 3 for mode 2); ssn_planes_shift
+            # derives the +-1 column copies with 16-byte vector moves
+            d.planes = buf[1 if copies == 3 else 0].data_ptr()
+            d.plane_istride = H2 * Wp
+            d.plane_cstride = B * H2 * Wp
+            d.plane_lstride = C2 * B * H2 * Wp
+            d.plane_pstride = gemm_mod.limbs(p) * C2 * B * H2 * Wp
+            d.plane_wp, d.plane_copies, d.plane_nparty = Wp, 1, m
+            self._planes_ready.add(chain[-1])
+            shift_rows = m * gemm_mod.limbs(p) * C2 * B * H2 if copies == 3 else 0
         e0 = self._event() if self._prof is not None else None
         _lib.call("ssn_layer_chain", ctypes.byref(d), _lib.stream_ptr())
+        if d.planes and shift_rows:
+            _lib.call("ssn_planes_shift", buf.data_ptr(), shift_rows, d.plane_wp, _lib.stream_ptr())
         if e0 is not None:
             nbytes = 8 * m * nel + (8 * n * nel if add is not None else 0)
             nbytes += 8 * (d.fan * n_out if nl is not None else n * nel)
@@ -311,6 +412,7 @@ class BatchedEngine:
         remaining = {i: len(c) for i, c in self.cons.items()}
         result = None
         pending = {}
+        self._planes_ready = set()
         for idx, op in enumerate(self.ops):
             src = idx - 1 if op.src is None else op.src
             xin = vals.get(src)
@@ -358,6 +460,8 @@ class BatchedEngine:
     # ------------------------------------------------------------------ ops
     def _gemm(self, idx, op, X):
         """Local share products of the m participants (S/layers.py:245-255): acc [m][B][O][ohw]."""
+        if idx in self._conv_mode:
+            return self._gemm_implicit(idx, op, X)
         B, m, p = self.batch, self.m, self.p
         w = self.W[op.weight + ".w"]
         O = op.out_shape[0]

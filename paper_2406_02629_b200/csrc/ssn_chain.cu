@@ -68,6 +68,13 @@ struct ChainArgs {
     u64 pseed, pstream, sseed, sstream;
     unsigned long long *fail;
     int fault_rank;
+    // channel-major u8 limb planes of the output for the next implicit-GEMM conv (may be null):
+    // byte l of participant t's share of (img, c, y, x) at
+    //   planes + (dx*pl_nparty + t)*pl_ps + l*pl_ls + c*pl_cs + img*pl_is + y*pl_wp + x + 1 - dx
+    // for each of pl_copies column-shifted copies (1: unshifted, 3: shifts -1, 0, +1)
+    uint8_t *planes;
+    u64 pl_ps, pl_ls, pl_cs, pl_is;
+    int pl_wp, pl_copies, pl_nparty;
 };
 
 constexpr int CHAIN_THREADS = 128;
@@ -362,10 +369,30 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 4) k_chain_nonlin(ChainArgs a, 
             if (o < n_out) {
                 u64 cbi[K - 1];
                 coeffs<K>(cbi, a.sseed, a.sstream + 6, o);
+                uint8_t *pb = nullptr;
+                int xq = 0;
+                if (a.planes) {
+                    const uint32_t img = o / chw, rem = o - img * chw;
+                    const uint32_t ci = rem / hw, pix = rem - ci * hw;
+                    const uint32_t y = pix / ow;
+                    xq = (int)(pix - y * ow);
+                    pb = a.planes + (u64)ci * a.pl_cs + (u64)img * a.pl_is + (u64)y * a.pl_wp;
+                }
 #pragma unroll
                 for (int t = 0; t < N; t++)
-                    if (t < a.fan)
-                        a.out[(u64)t * a.out_ps + o] = canon(mulm(plain[q], share_raw<K, N>(binv, cbi, tb, t)));
+                    if (t < a.fan) {
+                        const u64 v = canon(mulm(plain[q], share_raw<K, N>(binv, cbi, tb, t)));
+                        a.out[(u64)t * a.out_ps + o] = v;
+                        if (pb != nullptr && t < a.pl_nparty) {      // limb planes for the next conv
+                            for (int dx = 0; dx < a.pl_copies; dx++) {
+                                const int xc = a.pl_copies == 1 ? xq : xq + 1 - dx;
+                                if (xc < 0 || xc >= a.pl_wp) continue;
+                                uint8_t *dst = pb + ((u64)dx * a.pl_nparty + t) * a.pl_ps + xc;
+#pragma unroll
+                                for (int l = 0; l < 6; l++) dst[(u64)l * a.pl_ls] = (uint8_t)(v >> (8 * l));
+                            }
+                        }
+                    }
             }
         }
     }
@@ -474,6 +501,15 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
     a.sstream = d->src_stream;
     a.fail = d->verify ? d->fail : nullptr;
     a.fault_rank = d->fault_rank;
+    a.planes = d->planes;
+    a.pl_ps = d->plane_pstride;
+    a.pl_ls = d->plane_lstride;
+    a.pl_cs = d->plane_cstride;
+    a.pl_is = d->plane_istride;
+    a.pl_wp = d->plane_wp;
+    a.pl_copies = d->plane_copies;
+    a.pl_nparty = d->plane_nparty;
+    if (a.planes && (!d->nonlin || a.pl_copies < 1 || a.pl_nparty < 1 || a.pl_nparty > N)) return SSN_ERR_ARG;
     if (a.senders > a.nout) return SSN_ERR_ARG;
     if (!d->nonlin) {
         u64 blocks = (a.nel + PLAIN_THREADS - 1) / PLAIN_THREADS;

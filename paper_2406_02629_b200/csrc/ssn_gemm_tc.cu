@@ -930,7 +930,46 @@ __global__ void k_planes_cn(const u64 *__restrict__ x, int nimg, int C, int H, i
     }
 }
 
+// Mode-2 column copies from the unshifted copy: planes [3][rows][Wp] with rows = party*L*C*img*H;
+// copy 0 at x = copy 1 at x - 1 (0 at x = 0), copy 2 at x = copy 1 at x + 1 (copy 1's pad
+// columns x >= W are zero).  One thread per 16-byte chunk, funnel-shifted in registers.
+__global__ void k_planes_shift(uint8_t *__restrict__ planes, u64 rows, int Wp) {
+    const int cpr = Wp / 16;                                   // chunks per row
+    const u64 total = rows * cpr;
+    const u64 cs = rows * (u64)Wp;                             // copy stride
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < total; i += (u64)gridDim.x * blockDim.x) {
+        const u64 row = i / cpr;
+        const int ch = (int)(i - row * cpr);
+        const uint8_t *src = planes + cs + row * Wp + ch * 16;
+        const uint4 cur = *reinterpret_cast<const uint4 *>(src);
+        const uint32_t prev = ch > 0 ? *reinterpret_cast<const uint32_t *>(src - 4) : 0u;          // bytes x-4..x-1
+        const uint32_t next = ch + 1 < cpr ? *reinterpret_cast<const uint32_t *>(src + 16) : 0u;  // bytes x+16..
+        // left shift by one byte (copy 0): out[j] = in[j-1]
+        uint4 l, r;
+        l.x = __funnelshift_l(prev, cur.x, 8);
+        l.y = __funnelshift_l(cur.x, cur.y, 8);
+        l.z = __funnelshift_l(cur.y, cur.z, 8);
+        l.w = __funnelshift_l(cur.z, cur.w, 8);
+        // right shift by one byte (copy 2): out[j] = in[j+1]
+        r.x = __funnelshift_r(cur.x, cur.y, 8);
+        r.y = __funnelshift_r(cur.y, cur.z, 8);
+        r.z = __funnelshift_r(cur.z, cur.w, 8);
+        r.w = __funnelshift_r(cur.w, next, 8);
+        *reinterpret_cast<uint4 *>(planes + row * Wp + ch * 16) = l;
+        *reinterpret_cast<uint4 *>(planes + 2 * cs + row * Wp + ch * 16) = r;
+    }
+}
+
 }  // namespace
+
+extern "C" int ssn_planes_shift(uint8_t *planes, uint64_t rows, int Wp, void *stream) {
+    if (Wp < 16 || Wp % 16 || rows == 0) return SSN_ERR_ARG;
+    const u64 total = rows * (Wp / 16);
+    u64 blocks = (total + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    k_planes_shift<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(planes, rows, Wp);
+    return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
+}
 
 extern "C" int ssn_planes_cn(const u64 *x, int nparty, int nimg, int C, int H, int W, int Wp, int L, uint8_t *planes,
                              u64 x_pstride, int copies, void *stream) {

@@ -38,6 +38,11 @@ def weight_planes(w, p, nparty=1):
     return planes
 
 
+def conv_planes_supported(p):
+    """Implicit-GEMM convs from channel-major planes (ssn_gemm_tc_conv): default prime only."""
+    return p == (1 << 45) - 55
+
+
 def gemm_kernel_name(p, L, rows):
     """The kernel ssn_gemm_tc dispatches to (csrc/ssn_gemm_tc.cu)."""
     return "k_gemm_p45" if (L == 6 and p == (1 << 45) - 55 and rows >= 128) else f"k_gemm_tc<{L}>"

@@ -108,3 +108,22 @@ def test_verification_detects_corruption(ssn, fuse):
         eng.run(xb)
     eng.fault = None
     assert np.array_equal(eng.run(xb), want)
+
+
+def test_implicit_conv_path_resnet50_small(ssn):
+    """Bottleneck ResNet-50 at 64x64: 1x1 stride-1 convs read channel-major planes (mode 1),
+    3x3 pad-1 convs on 16x16 maps use the implicit GEMM with pre-shifted copies (mode 2); the
+    planes come from the chain kernels.  Outputs equal the im2col path and the plaintext."""
+    from paper_2406_02629_b200 import resnet
+    from paper_2406_02629_b200.batched import BatchedEngine
+    net = resnet.imagenet_resnet(50, image=64)
+    scheme = ssn.SssScheme(ssn.PrimeField(), 3, 5)
+    xb = net.random_inputs(seed=2, batch=2)
+    want, _ = resnet.plaintext_forward(net, xb)
+    eng = BatchedEngine(net, scheme, batch=2, seed=5, verify=True)
+    modes = {m[1] for m in eng._conv_mode.values()}
+    assert modes == {1, 2}, modes
+    assert np.array_equal(eng.run(xb), want)
+    ref = BatchedEngine(net, scheme, batch=2, seed=5, verify=True, implicit=False)
+    assert not ref._conv_mode
+    assert np.array_equal(ref.run(xb), want)

@@ -87,7 +87,8 @@ def test_conv_tc_vs_simt(g, C, H, W, O, k, s, pad, nimg, nparty):
 
 
 @pytest.mark.parametrize("kh,C,H,W,O", [(1, 64, 56, 56, 64), (1, 128, 14, 14, 96), (3, 64, 56, 56, 64),
-                                        (3, 128, 28, 28, 128), (3, 64, 14, 14, 32)])
+                                        (3, 128, 28, 28, 128), (3, 64, 14, 14, 32), (3, 64, 32, 32, 64),
+                                        (3, 128, 16, 16, 128)])
 def test_implicit_conv_planes_vs_im2col(kh, C, H, W, O):
     """Implicit GEMM from channel-major planes (TMA M-major A, modes 1 and 2) equals the
     explicit im2col + tcgen05 GEMM path bit for bit, including the zero padding of 3x3."""
@@ -101,7 +102,7 @@ def test_implicit_conv_planes_vs_im2col(kh, C, H, W, O):
     pad = (kh - 1) // 2
     want = G.field_conv(w, x, 1, pad, p, nimg=B, nparty=nparty, force="tc")
     mode = 1 if kh == 1 else 2
-    Wp = W if mode == 1 else (W + 16) // 16 * 16
+    Wp = W if mode == 1 else (W // 16 + 1) * 16
     L = G.limbs(p)
     copies = 1 if mode == 1 else 3
     planes = torch.zeros((copies, nparty, L, C, B, H, Wp), dtype=torch.uint8, device="cuda")
