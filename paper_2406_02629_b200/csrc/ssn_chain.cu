@@ -294,6 +294,18 @@ __device__ __forceinline__ u64 warp_excl_suffix(u64 v, int lane) {
     return lane < 31 ? ex : 1;
 }
 
+// u8 limb planes of one share value for the next implicit-GEMM conv.  Out of line: the chain
+// kernel sits near the instruction-cache limit, and 5 inlined copies pushed it over.
+__device__ __noinline__ void emit_planes(uint8_t *row, u64 v, int xq, int copies, u64 copy_stride, u64 ls, int wp) {
+    for (int dx = 0; dx < copies; dx++) {
+        const int xc = copies == 1 ? xq : xq + 1 - dx;
+        if (xc < 0 || xc >= wp) continue;
+        uint8_t *dst = row + (u64)dx * copy_stride + xc;
+#pragma unroll
+        for (int l = 0; l < 6; l++) dst[(u64)l * ls] = (uint8_t)(v >> (8 * l));
+    }
+}
+
 // masked nonlinearity fused after the chain: one thread per output window, WPT windows per
 // thread (a block-stride apart, coalesced).  beta^-1 of all 32*WPT windows of a warp comes
 // from ONE Fermat inversion: per-thread running products over its WPT windows, warp-shuffle
@@ -383,15 +395,9 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 4) k_chain_nonlin(ChainArgs a, 
                     if (t < a.fan) {
                         const u64 v = canon(mulm(plain[q], share_raw<K, N>(binv, cbi, tb, t)));
                         a.out[(u64)t * a.out_ps + o] = v;
-                        if (pb != nullptr && t < a.pl_nparty) {      // limb planes for the next conv
-                            for (int dx = 0; dx < a.pl_copies; dx++) {
-                                const int xc = a.pl_copies == 1 ? xq : xq + 1 - dx;
-                                if (xc < 0 || xc >= a.pl_wp) continue;
-                                uint8_t *dst = pb + ((u64)dx * a.pl_nparty + t) * a.pl_ps + xc;
-#pragma unroll
-                                for (int l = 0; l < 6; l++) dst[(u64)l * a.pl_ls] = (uint8_t)(v >> (8 * l));
-                            }
-                        }
+                        if (pb != nullptr && t < a.pl_nparty)          // limb planes for the next conv
+                            emit_planes(pb + (u64)t * a.pl_ps, v, xq, a.pl_copies, a.pl_nparty * a.pl_ps,
+                                        a.pl_ls, a.pl_wp);
                     }
             }
         }
