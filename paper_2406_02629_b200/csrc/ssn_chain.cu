@@ -225,8 +225,10 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
     const uint32_t ch = (i / a.bias_div) % a.bias_mod;
     // ---- step 2 (RESHARE_BACK): front fr applies R^T; step 3: out rank t reconstructs,
     //      + zero share (rerand) + bias share, then + alpha share (TRUNC_MASKED)
+    // Rolled loop over the out ranks (the unrolled form pushed the kernel past the instruction
+    // cache); masked[] then lives in local memory (L1), tb.rt[t] is an indexed constant load.
     u64 masked[N];
-#pragma unroll
+#pragma unroll 1
     for (int t = 0; t < N; t++) {
         if (t < a.senders) {
             u64 back[K];
