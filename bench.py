@@ -29,6 +29,7 @@ WORKLOADS = {
     "resnet50-3pc": ("imagenet50", 2, 3, False, 16),
     "resnet18-cifar-3pc": ("cifar18", 2, 3, False, 128),
     "lenet-3pc": ("reference", 2, 3, False, 1024),
+    "lenet28-3pc": ("lenet28", 2, 3, False, 1024),     # config 1: LeNet-style CNN on 1x28x28
     "gemm-sweep": ("gemm", 0, 0, False, 0),          # config 5: mod-p share GEMM + reshare sweep
 }
 SWEEP = [(256, 256, 256), (1024, 1024, 1024), (2048, 2048, 2048), (4096, 4096, 4096), (8192, 8192, 8192),
@@ -45,6 +46,9 @@ def build_model(kind):
         return resnet.imagenet_resnet(50)
     if kind == "cifar18":
         return resnet.cifar_resnet18()
+    if kind == "lenet28":
+        from paper_2406_02629_b200.model import build_lenet28
+        return build_lenet28(7, pool="max")[0]
     return build_reference_model(7, pool="max")[0]
 
 

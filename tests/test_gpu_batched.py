@@ -127,3 +127,19 @@ def test_implicit_conv_path_resnet50_small(ssn):
     ref = BatchedEngine(net, scheme, batch=2, seed=5, verify=True, implicit=False)
     assert not ref._conv_mode
     assert np.array_equal(ref.run(xb), want)
+
+
+@pytest.mark.parametrize("k,n", [(2, 3), (3, 5)])
+def test_lenet28_config1(ssn, k, n):
+    """Config 1 (LeNet-style CNN on 1x28x28, built from the reference's layer kinds): the
+    reference-API simulation and the batched engine both equal plaintext_infer exactly."""
+    from paper_2406_02629_b200.batched import BatchedEngine
+    from paper_2406_02629_b200.model import build_lenet28
+    model, _ = build_lenet28(7)
+    scheme = ssn.SssScheme(ssn.PrimeField(), k, n)
+    xb = np.stack([ssn.random_input(7, model, index=i)[0] for i in range(4)])
+    want = np.stack([ssn.plaintext_infer(model, xb[i]) for i in range(4)])
+    got = ssn.simulate_inference(model, scheme, seed=7, input_int=xb[0])
+    assert np.array_equal(got.output, want[0])
+    eng = BatchedEngine(model, scheme, batch=4, seed=3)
+    assert np.array_equal(eng.run(xb), want)
