@@ -128,9 +128,8 @@ def cpu_baseline_sample(model, k, n, verify, budget_s=20.0):
     from oracle import sim
     from paper_2406_02629_b200.layers import ScheduledOp, _flag_passive
     oracle.build()
-    weights = model.weight_values()
-    total_macs = model.macs()
-    if not hasattr(model, "nodes"):          # chain models: the whole network is the sample
+    if not hasattr(model, "nodes"):          # chain models (ModelGraph): the whole network is the sample
+        weights = {name: qt.values for name, qt in model.weights.items()}
         from paper_2406_02629_b200.layers import plan_schedule
         from paper_2406_02629_b200.model import random_input
         from paper_2406_02629_b200.sss import SssScheme
@@ -144,6 +143,8 @@ def cpu_baseline_sample(model, k, n, verify, budget_s=20.0):
         dt = (time.perf_counter() - t0) / reps
         return {"value": 1.0 / dt, "unit": "images/s", "cores": os.cpu_count(), "kind": "port",
                 "sample": f"oracle/sim.py full {n}PC protocol, 1 image x {reps}", "s_per_image": dt}
+    weights = model.weight_values()
+    total_macs = model.macs()
     # residual nets: one representative residual block (the network's most repeated kind),
     # run as its own schedule through the full protocol, extrapolated by field-MAC share
     ops = _flag_passive(model.plan_ops(), verify)
