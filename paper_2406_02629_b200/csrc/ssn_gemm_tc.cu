@@ -1024,7 +1024,7 @@ extern "C" int ssn_gemm_tc(const uint8_t *a_planes, const uint8_t *b_planes, int
     if (L < 1 || L > MAXL || Kpad % 16 || M < 1 || O < 1 || nparty < 1 || ohw < 1) return SSN_ERR_ARG;
     if ((unsigned __int128)L * Kpad * 65025 >= ((unsigned __int128)1 << 32)) return SSN_ERR_ARG;
     cudaStream_t st = (cudaStream_t)stream;
-    if (L == 6 && p == p45::P && M >= BM) return launch_p45(a_planes, b_planes, nparty, M, O, (int)Kpad, out, out_pstride, ohw, st);
+    if (L == 6 && p == p45::P) return launch_p45(a_planes, b_planes, nparty, M, O, (int)Kpad, out, out_pstride, ohw, st);
     switch (L) {
         case 6: return launch_tc<6>(a_planes, b_planes, nparty, M, O, (int)Kpad, out, out_pstride, ohw, p, st);
         case 7: return launch_tc<7>(a_planes, b_planes, nparty, M, O, (int)Kpad, out, out_pstride, ohw, p, st);

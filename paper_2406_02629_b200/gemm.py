@@ -45,11 +45,14 @@ def conv_planes_supported(p):
 
 def gemm_kernel_name(p, L, rows):
     """The kernel ssn_gemm_tc dispatches to (csrc/ssn_gemm_tc.cu)."""
-    return "k_gemm_p45" if (L == 6 and p == (1 << 45) - 55 and rows >= 128) else f"k_gemm_tc<{L}>"
+    return "k_gemm_p45w<0>" if (L == 6 and p == (1 << 45) - 55) else f"k_gemm_tc<{L}>"
 
 
 def use_tc(p, rows, K, O):
-    return rows >= TC_MIN_ROWS and O >= 16 and K >= 32 and tc_supported(p, K)
+    # the persistent p45 kernel zero-fills (TMA out-of-range) a partial 128-row tile, so small
+    # row counts (e.g. the classifier's batch rows) still run on the tensor cores
+    min_rows = 16 if p == (1 << 45) - 55 else TC_MIN_ROWS
+    return rows >= min_rows and O >= 16 and K >= 32 and tc_supported(p, K)
 
 
 def _ev():

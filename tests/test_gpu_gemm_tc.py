@@ -115,3 +115,16 @@ def test_implicit_conv_planes_vs_im2col(kh, C, H, W, O):
               B * O * H * W, p, _lib.stream_ptr())
     torch.cuda.synchronize()
     assert torch.equal(out, want)
+
+
+@pytest.mark.parametrize("rows,K,O", [(16, 2048, 1000), (40, 512, 64), (1, 256, 32)])
+def test_small_row_dense_on_tensor_cores(rows, K, O):
+    """Partial 128-row tiles (TMA zero fill beyond the rows) stay exact: classifier-sized GEMMs."""
+    from paper_2406_02629_b200 import gemm as G
+    p = (1 << 45) - 55
+    rng = np.random.default_rng(rows + K + O)
+    w = torch.as_tensor(rng.integers(0, p, size=(2, O, K)), device="cuda")
+    x = torch.as_tensor(rng.integers(0, p, size=(2, rows, K)), device="cuda")
+    tc = G.field_dense(w, x, p, nimg=rows, nparty=2, force="tc")
+    simt = G.field_dense(w, x, p, nimg=rows, nparty=2, force="simt")
+    assert torch.equal(tc, simt)
