@@ -300,6 +300,13 @@ constexpr u64 MASK45 = (1ull << 45) - 1;
 
 __device__ __forceinline__ u64 lz(u64 x) { return (x >> 45) * 55 + (x & MASK45); }
 
+// acc + a * b in ONE IMAD.WIDE.U32 (a shift-and-add compiles to four 32-bit ops)
+__device__ __forceinline__ u64 mad_wide(uint32_t a, uint32_t b, u64 acc) {
+    u64 r;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(a), "r"(b), "l"(acc));
+    return r;
+}
+
 // (g0 + g1*2^32 + g2*2^64) mod p for g0, g1 < 2^57, g2 < 2^49
 __device__ __forceinline__ u64 combine(u64 g0, u64 g1, u64 g2) {
     const u64 x = lz(g1);                                   // < 2^46
@@ -431,7 +438,7 @@ k_gemm_p45(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUte
                     u64 acc = 0;
 #pragma unroll
                     for (int dd = 0; dd < 4; dd++)
-                        if (grp * 4 + dd < ND) acc += (u64)r[dd][c] << (8 * dd);
+                        if (grp * 4 + dd < ND) acc = mad_wide(r[dd][c], 1u << (8 * dd), acc);
                     g[grp][c] = acc;
                 }
             }
@@ -606,7 +613,7 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     u64 acc = 0;
 #pragma unroll
                     for (int dd = 0; dd < 4; dd++)
-                        if (grp * 4 + dd < ND) acc += (u64)r[dd][c] << (8 * dd);
+                        if (grp * 4 + dd < ND) acc = mad_wide(r[dd][c], 1u << (8 * dd), acc);
                     g[grp][c] = acc;
                 }
             }
