@@ -200,6 +200,11 @@ def load_traffic():
         return {}
 
 
+# executed thread instructions per element of the fused chain kernels (ncu
+# smsp__inst_executed x 32 / elements, ResNet-152 5PC, profiles/r01/README.md)
+CHAIN_ALU = {"chain": 3970}
+
+
 def roofline(kstats, eng, dev_ms, bf16, hbm, src):
     """Roofline of the dominant kernel class of the step (by device time), plus every class.
     gemm: int8 tensor ops = L^2 * 2 * field MACs (L = 6 u8 limbs per 45-bit share) against the
@@ -225,6 +230,14 @@ def roofline(kstats, eng, dev_ms, bf16, hbm, src):
             r = {"bound": "hbm", "achieved": round(achieved, 1), "peak": round(hbm, 1), "unit": "GB/s",
                  "frac": round(achieved / hbm, 4),
                  "note": "algorithmic bytes per launch (DESIGN.md section 3) / CUDA-event launch time"}
+            alu = CHAIN_ALU.get(cls)
+            if alu and st.get("elems_per_launch"):
+                # the fused protocol chain is integer-ALU bound: executed thread instructions per
+                # element (ncu, profiles/r01/README.md) x elements / time vs the SM issue peak
+                rate = alu * st["elems_per_launch"] / sec
+                peak_i = 148 * 128 * 1.965e9
+                r["alu_issue"] = {"thread_instr_per_elem": alu, "achieved_tinstr_per_s": float(f"{rate:.4g}"),
+                                  "peak_tinstr_per_s": float(f"{peak_i:.4g}"), "frac": round(rate / peak_i, 4)}
         t = traffic.get(cls)
         r["traffic"] = round(t) if t else None
         r["kernel"] = st["kernel"]

@@ -299,7 +299,8 @@ class BatchedEngine:
         if e0 is not None:
             nbytes = 8 * m * nel + (8 * n * nel if add is not None else 0)
             nbytes += 8 * (d.fan * n_out if nl is not None else n * nel)
-            self._record("chain", e0, self._event(), nbytes, "k_chain_nonlin" if nl is not None else "k_chain_plain")
+            self._record("chain", e0, self._event(), nbytes, "k_chain_nonlin" if nl is not None else "k_chain_plain",
+                         elems=nel)
         self.kernel_launches += 1
         return Y
 
@@ -326,9 +327,9 @@ class BatchedEngine:
     def disable_profiling(self):
         self._prof = None
 
-    def _record(self, cls, e0, e1, work, kernel):
+    def _record(self, cls, e0, e1, work, kernel, elems=0):
         if self._prof is not None:
-            self._prof.setdefault(cls, []).append((e0, e1, work, kernel))
+            self._prof.setdefault(cls, []).append((e0, e1, work, kernel, elems))
 
     @staticmethod
     def _event():
@@ -340,12 +341,14 @@ class BatchedEngine:
         torch.cuda.synchronize()
         out = {}
         for cls, rec in (self._prof or {}).items():
-            ms = [a.elapsed_time(b) for a, b, _, _ in rec]
-            work = [w for _, _, w, _ in rec]
+            ms = [r[0].elapsed_time(r[1]) for r in rec]
+            work = [r[2] for r in rec]
+            elems = [r[4] for r in rec]
             nl = len(rec)
             out[cls] = {"launches_per_step": nl / max(steps, 1), "ms_per_step": sum(ms) / max(steps, 1),
                         "ms_per_launch": sum(ms) / nl if nl else 0.0, "work_per_launch": sum(work) / nl if nl else 0.0,
-                        "kernel": ",".join(sorted({k for _, _, _, k in rec}))}
+                        "elems_per_launch": sum(elems) / nl if nl else 0.0,
+                        "kernel": ",".join(sorted({r[3] for r in rec}))}
         return out
 
     def limb_products(self):
