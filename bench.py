@@ -514,9 +514,18 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # SSN_SHARED_GPU=1: every rank on cuda:0 over gloo (functional check of the multi-rank
+    # timing / reduction logic on a single-GPU box; never used for reported numbers)
+    shared = os.environ.get("SSN_SHARED_GPU") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    red_dev = "cpu" if shared else "cuda"
     kind, k, n, verify, dflt_batch = WORKLOADS[args.workload]
     B = args.batch or dflt_batch
     model = build_model(kind)
@@ -557,7 +566,7 @@ def main():
     def max_over_ranks(v):
         if world == 1:
             return v
-        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        t = torch.tensor([v], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
