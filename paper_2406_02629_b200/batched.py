@@ -24,6 +24,7 @@ they equal the reference / plaintext exactly (tests/test_gpu_batched.py).
 """
 
 import ctypes
+import os
 import time
 
 import numpy as np
@@ -84,6 +85,8 @@ class BatchedEngine:
         self._chain_member = {i: start for start, ch in self.chains.items() for i in ch[1:]}
         self._rt_all = _lib.u64_array([R[i][t] for t in range(n) for i in range(self.m)])
         self._plan_implicit_convs(implicit)
+        # chain kernels emit the next conv's limb planes (else ssn_planes_cn does, per conv)
+        self.chain_planes = os.environ.get("SSN_CHAIN_PLANES", "1") != "0"
         self._ext_host = _lib.u64_array(self.ext) if self.ext else None
 
     # ------------------------------------------------------------------ setup
@@ -279,7 +282,7 @@ class BatchedEngine:
         d.fault_rank = self.fault[1] if (self.fault is not None and self.fault[0] == chain[0]) else -1
         shift_rows = 0
         ps = self._plane_src.get(chain[-1])
-        if ps is not None and nl is not None and tuple(last.out_shape) == tuple(ps[3:]):
+        if ps is not None and nl is not None and self.chain_planes and tuple(last.out_shape) == tuple(ps[3:]):
             _, Wp, copies, C2, H2, W2 = ps
             buf = self._plane_buffer(chain[-1])
             # the chain writes the unshifted copy (index 1 of 3 for mode 2); ssn_planes_shift

@@ -50,12 +50,29 @@ struct STables {
     uint32_t pw[N][K - 1];   // id_t^(e+1), e < k-1 (small, non-negative)
 };
 
+// Division of a 32-bit numerator by a launch-constant 32-bit divisor: q = umulhi64(x, ceil(2^64/d))
+// is exact for all x < 2^32 (Granlund-Montgomery with a 64-bit magic), ~3 IMADs instead of the
+// ~20-instruction integer-division sequence.
+struct FastDiv {
+    u64 m;
+    uint32_t d;
+};
+static inline FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f;
+    f.d = d;
+    f.m = d == 1 ? 0 : (u64)((((unsigned __int128)1) << 64) / d + 1);
+    return f;
+}
+__device__ __forceinline__ uint32_t fdiv(uint32_t x, const FastDiv &f) {
+    return f.d == 1 ? x : (uint32_t)__umul64hi((u64)x, f.m);
+}
+
 struct ChainArgs {
     const u64 *acc;
     u64 acc_ps;
     const u64 *bias;
     u64 bias_ps;
-    uint32_t bias_div, bias_mod;
+    FastDiv bias_div, bias_mod, f_chw, f_hw, f_ow;
     const u64 *other;
     u64 other_ps;
     u64 *out;
@@ -222,7 +239,8 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
     const u64 comp = em ? PP - em : 0;
     coeffs<K>(ca, a.sseed, a.sstream + 2, i);
     coeffs<K>(cc, a.sseed, a.sstream + 3, i);
-    const uint32_t ch = (i / a.bias_div) % a.bias_mod;
+    const uint32_t bq = fdiv(i, a.bias_div);
+    const uint32_t ch = bq - fdiv(bq, a.bias_mod) * a.bias_mod.d;
     // ---- step 2 (RESHARE_BACK): front fr applies R^T; step 3: out rank t reconstructs,
     //      + zero share (rerand) + bias share, then + alpha share (TRUNC_MASKED)
     // Rolled loop over the out ranks (the unrolled form pushed the kernel past the instruction
@@ -338,9 +356,9 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 4) k_chain_nonlin(ChainArgs a, 
                 bt = 1 + ssn_rand_range(a.sseed, a.sstream + 4, o, 0, a.bmax);     // window-constant beta
                 uint32_t base_in = o;
                 if (pooled) {
-                    const uint32_t img = o / chw, rem = o - img * chw;
-                    const uint32_t ci = rem / hw, rr = rem - ci * hw;
-                    const uint32_t y0 = rr / ow, x0 = rr - y0 * ow;
+                    const uint32_t img = fdiv(o, a.f_chw), rem = o - img * chw;
+                    const uint32_t ci = fdiv(rem, a.f_hw), rr = rem - ci * hw;
+                    const uint32_t y0 = fdiv(rr, a.f_ow), x0 = rr - y0 * ow;
                     base_in = ((img * a.c + ci) * a.h + y0 * a.kh) * a.w + x0 * a.kw;
                 }
                 i64 acc = a.pool_kind == 1 ? INT64_MIN : 0;
@@ -386,9 +404,9 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 4) k_chain_nonlin(ChainArgs a, 
                 uint8_t *pb = nullptr;
                 int xq = 0;
                 if (a.planes) {
-                    const uint32_t img = o / chw, rem = o - img * chw;
-                    const uint32_t ci = rem / hw, pix = rem - ci * hw;
-                    const uint32_t y = pix / ow;
+                    const uint32_t img = fdiv(o, a.f_chw), rem = o - img * chw;
+                    const uint32_t ci = fdiv(rem, a.f_hw), pix = rem - ci * hw;
+                    const uint32_t y = fdiv(pix, a.f_ow);
                     xq = (int)(pix - y * ow);
                     pb = a.planes + (u64)ci * a.pl_cs + (u64)img * a.pl_is + (u64)y * a.pl_wp;
                 }
@@ -473,8 +491,14 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
     a.acc_ps = d->acc_pstride;
     a.bias = d->bias;
     a.bias_ps = d->bias_pstride;
-    a.bias_div = (uint32_t)d->bias_div;
-    a.bias_mod = (uint32_t)d->bias_mod;
+    a.bias_div = make_fastdiv((uint32_t)d->bias_div);
+    a.bias_mod = make_fastdiv((uint32_t)d->bias_mod);
+    if (d->nonlin) {
+        const uint32_t ohh = (uint32_t)(d->h / d->kh), oww = (uint32_t)(d->w / d->kw);
+        a.f_chw = make_fastdiv((uint32_t)d->c * ohh * oww);
+        a.f_hw = make_fastdiv(ohh * oww);
+        a.f_ow = make_fastdiv(oww);
+    }
     a.other = d->other;
     a.other_ps = d->other_pstride;
     a.out = d->out;
