@@ -214,6 +214,9 @@ typedef struct ssn_chain_desc {
     uint8_t *planes;
     uint64_t plane_pstride, plane_lstride, plane_cstride, plane_istride;
     int plane_wp, plane_copies, plane_nparty;
+    /* optional (nonlin chains): scratch [n][nel] -> run as two kernels (reshare/truncation/add
+     * into scratch, then the masked nonlinearity); same results */
+    uint64_t *scratch;
 } ssn_chain_desc;
 
 int ssn_layer_chain(const ssn_chain_desc *desc, void *stream);

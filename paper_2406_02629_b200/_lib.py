@@ -104,6 +104,7 @@ class ChainDesc(ctypes.Structure):
         ("planes", _P),
         ("plane_pstride", _U64), ("plane_lstride", _U64), ("plane_cstride", _U64), ("plane_istride", _U64),
         ("plane_wp", _I32), ("plane_copies", _I32), ("plane_nparty", _I32),
+        ("scratch", _P),
     ]
 
 _lib = None

@@ -87,6 +87,8 @@ class BatchedEngine:
         self._plan_implicit_convs(implicit)
         # chain kernels emit the next conv's limb planes (else ssn_planes_cn does, per conv)
         self.chain_planes = os.environ.get("SSN_CHAIN_PLANES", "1") != "0"
+        # nonlinear chains as two kernels (reshare/truncation, then nonlinearity)
+        self.split_chain = os.environ.get("SSN_SPLIT_CHAIN", "1") != "0"
         self._ext_host = _lib.u64_array(self.ext) if self.ext else None
 
     # ------------------------------------------------------------------ setup
@@ -295,6 +297,10 @@ class BatchedEngine:
             d.plane_wp, d.plane_copies, d.plane_nparty = Wp, 1, m
             self._planes_ready.add(chain[-1])
             shift_rows = m * gemm_mod.limbs(p) * C2 * B * H2 if copies == 3 else 0
+        scratch = None
+        if nl is not None and self.split_chain:
+            scratch = torch.empty((n, nel), dtype=torch.int64, device=self.dev)
+            d.scratch = scratch.data_ptr()
         e0 = self._event() if self._prof is not None else None
         _lib.call("ssn_layer_chain", ctypes.byref(d), _lib.stream_ptr())
         if d.planes and shift_rows:

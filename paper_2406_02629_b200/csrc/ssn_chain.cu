@@ -333,7 +333,10 @@ __device__ __noinline__ void emit_planes(uint8_t *row, u64 v, int xq, int copies
 // pass.  No block barrier: warps never wait for each other.
 constexpr int WPT = 8;
 
-template <int K, int N>
+// SPLIT: the reshare/truncation/add part already ran (k_chain_plain into a.acc = its n-party
+// output) and this kernel only runs the masked nonlinearity, reading each party's share.
+// Two kernels of half the code each run faster than one that overflows the instruction cache.
+template <int K, int N, bool SPLIT>
 __global__ void __launch_bounds__(CHAIN_THREADS, 4) k_chain_nonlin(ChainArgs a, const __grid_constant__ STables<K, N> tb,
                                                                 SsnField f) {
     constexpr int M = 2 * K - 1;
@@ -368,7 +371,12 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 4) k_chain_nonlin(ChainArgs a, 
                     for (int wx = 0; wx < a.kw; wx++) {
                         const uint32_t i = base_in + wy * a.w + wx;
                         u64 x[N];
-                        chain_elem<K, N>(a, tb, i, x, bad);
+                        if (SPLIT) {
+#pragma unroll
+                            for (int t = 0; t < M; t++) x[t] = a.acc[(u64)t * a.acc_ps + i];
+                        } else {
+                            chain_elem<K, N>(a, tb, i, x, bad);
+                        }
                         // participants mask with their beta shares (NONLIN_MASKED); elite rec over m
                         u64 cb[K - 1];
                         coeffs<K>(cb, a.sseed, a.sstream + 5, i);
@@ -552,7 +560,22 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
         u64 blocks = (n_out + CHAIN_THREADS * WPT - 1) / (CHAIN_THREADS * WPT);
         if (blocks > 148ull * 16) blocks = 148ull * 16;
         if (blocks < 1) blocks = 1;
-        k_chain_nonlin<K, N><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a, tb, f);
+        if (d->scratch) {
+            // split: reshare + truncation (+ add) into scratch [n][nel], then the nonlinearity
+            ChainArgs a1 = a;
+            a1.out = d->scratch;
+            a1.out_ps = a.nel;
+            a1.planes = nullptr;
+            u64 b1 = (a.nel + PLAIN_THREADS - 1) / PLAIN_THREADS;
+            if (b1 > 148ull * 16) b1 = 148ull * 16;
+            k_chain_plain<K, N><<<(unsigned)b1, PLAIN_THREADS, 0, st>>>(a1, tb, f);
+            ChainArgs a2 = a;
+            a2.acc = d->scratch;
+            a2.acc_ps = a.nel;
+            k_chain_nonlin<K, N, true><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a2, tb, f);
+        } else {
+            k_chain_nonlin<K, N, false><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a, tb, f);
+        }
     }
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
