@@ -197,6 +197,37 @@ __device__ __forceinline__ void coeffs(u64 (&c)[K - 1], u64 seed, u64 stream, u6
     }
 }
 
+// Dense use of Philox output: NC calls give 128*NC random bits, sliced into 45-bit field
+// coefficients (and one 64-bit word for a bounded draw) instead of one call per 2 coefficients.
+template <int NC>
+struct Reservoir {
+    uint32_t w[4 * NC + 2];
+};
+template <int NC>
+__device__ __forceinline__ void fill(Reservoir<NC> &r, u64 seed, u64 stream, u64 i, uint32_t tag) {
+#pragma unroll
+    for (int c = 0; c < NC; c++) {
+        const ssn_u4 v = ssn_philox_at(seed, stream, i, tag + c);
+        r.w[4 * c] = v.x;
+        r.w[4 * c + 1] = v.y;
+        r.w[4 * c + 2] = v.z;
+        r.w[4 * c + 3] = v.w;
+    }
+    r.w[4 * NC] = r.w[4 * NC + 1] = 0;
+}
+// bits [bit, bit + 64) of the reservoir; `bit` is a compile-time constant after unrolling, so
+// the word indices resolve to registers
+template <int NC>
+__device__ __forceinline__ u64 take64(const Reservoir<NC> &r, int bit) {
+    const int wi = bit >> 5, sh = bit & 31;
+    const u64 lo = ((u64)r.w[wi + 1] << 32) | r.w[wi];
+    return sh == 0 ? lo : (lo >> sh) | ((u64)r.w[wi + 2] << (64 - sh));
+}
+template <int NC>
+__device__ __forceinline__ u64 take45(const Reservoir<NC> &r, int bit) {
+    return take64<NC>(r, bit) & PMASK;
+}
+
 // elite truncation of the reconstructed masked value (ssn_trunc_value, specialised)
 __device__ __forceinline__ u64 trunc_val(u64 v, const ChainArgs &a) {
     const i64 shifted = (i64)addm(v, a.neglo_mod) + a.lo;
@@ -219,11 +250,16 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
 #pragma unroll
     for (int j = 0; j < M; j++) acc[j] = a.acc[(u64)j * a.acc_ps + i];
     // ---- reshare step 1 (RESHARE_OUT): participant j sub-shares its local product to the front
+    // (the participants' M*(K-1) polynomial coefficients sliced from one Philox reservoir)
+    constexpr int NCR = (45 * M * (K - 1) + 127) / 128;
+    Reservoir<NCR> rr;
+    fill<NCR>(rr, a.pseed, a.pstream, i, 0x900u);
     u64 sub[K][M];
 #pragma unroll
     for (int j = 0; j < M; j++) {
         u64 c[K - 1];
-        coeffs<K>(c, a.pseed, a.pstream + j, i);
+#pragma unroll
+        for (int e = 0; e < K - 1; e++) c[e] = take45<NCR>(rr, 45 * (j * (K - 1) + e));
 #pragma unroll
         for (int fr = 0; fr < K; fr++) sub[fr][j] = share_at<K, N>(acc[j], c, tb, fr);
     }
@@ -231,14 +267,22 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
 #pragma unroll
     for (int fr = 0; fr < K; fr++) subsum[fr] = xsum_of<M>(sub[fr]);
     // source: zero shares (gen_zero_shares) and the truncation masks (gen_additive_mask)
+    // (zero, alpha and comp coefficients + the 64 bits of e from one source reservoir)
+    constexpr int NCS = (45 * 3 * (K - 1) + 64 + 127) / 128;
+    Reservoir<NCS> rs;
+    fill<NCS>(rs, a.sseed, a.sstream, i, 0x900u);
     u64 z[K - 1], ca[K - 1], cc[K - 1];
-    coeffs<K>(z, a.sseed, a.sstream + 0, i);
-    const u64 e = 1 + ssn_rand_range(a.sseed, a.sstream + 1, i, 0, a.emax);
+#pragma unroll
+    for (int e = 0; e < K - 1; e++) {
+        z[e] = take45<NCS>(rs, 45 * e);
+        ca[e] = take45<NCS>(rs, 45 * (K - 1 + e));
+        cc[e] = take45<NCS>(rs, 45 * (2 * (K - 1) + e));
+    }
+    // e = 1 + U[0, emax) by multiply-shift of 64 random bits (bias <= emax / 2^64 <= 2^-32)
+    const u64 e = 1 + __umul64hi(take64<NCS>(rs, 45 * 3 * (K - 1)), a.emax);
     const u64 em = red64(e);
     const u64 alpha = mulm(em, a.stepm);
     const u64 comp = em ? PP - em : 0;
-    coeffs<K>(ca, a.sseed, a.sstream + 2, i);
-    coeffs<K>(cc, a.sseed, a.sstream + 3, i);
     const uint32_t bq = fdiv(i, a.bias_div);
     const uint32_t ch = bq - fdiv(bq, a.bias_mod) * a.bias_mod.d;
     // ---- step 2 (RESHARE_BACK): front fr applies R^T; step 3: out rank t reconstructs,
