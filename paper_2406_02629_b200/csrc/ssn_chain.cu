@@ -153,10 +153,12 @@ __device__ __forceinline__ u64 lin_s(const u64 (&x)[M], u64 xsum, const SRow<M> 
         lo += (u64)(uint32_t)x[j] * r.nn[j];
         hi += (uint32_t)(x[j] >> 32) * r.nn[j];
     }
-    const u64 pos = lo + ((u64)hi << 32);                 // < 2^64
-    const u64 neg = mul_small(xsum, r.off);               // < 2^62
-    const u64 v = lz(pos) + (4 * PP - lz(neg));           // < 2^48
-    return r.one ? lz(v) : mulm(v, r.dinv);
+    // pos < M * 2^60 <= 7 * 2^60 < 2^63 and neg < 2^62 < 2^18 * p, so pos + 2^18 p - neg is a
+    // non-negative u64 below 2^64: ONE fold for the whole signed combination
+    const u64 pos = lo + ((u64)hi << 32);
+    const u64 neg = mul_small(xsum, r.off);
+    const u64 v = lz(pos + (PP << 18) - neg);            // < 2^46
+    return r.one ? v : mulm(v, r.dinv);
 }
 template <int M>
 __device__ __forceinline__ u64 xsum_of(const u64 (&x)[M]) {
