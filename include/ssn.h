@@ -217,9 +217,16 @@ typedef struct ssn_chain_desc {
     /* optional (nonlin chains): scratch [n][nel] -> run as two kernels (reshare/truncation/add
      * into scratch, then the masked nonlinearity); same results */
     uint64_t *scratch;
+    /* optional (nonlin chains): the trusted source's beta^-1 from a table inv_table[b] =
+     * b^-1 mod p, b < inv_table_len (must exceed bmax) instead of batch inversion */
+    const uint64_t *inv_table;
+    uint64_t inv_table_len;
 } ssn_chain_desc;
 
 int ssn_layer_chain(const ssn_chain_desc *desc, void *stream);
+/* table[b] = b^-1 mod p for b in [1, n), table[0] = 0 (batch inversion, p = 2^45 - 55):
+ * gen_multiplicative_mask's beta^-1 (S/masks.py:67-90) for beta <= 2^28 by lookup. */
+int ssn_inv_table(uint64_t *table, uint64_t n, uint64_t p, void *stream);
 /* 1 if ssn_layer_chain supports (k, n, ids, p): a pseudo-Mersenne prime within 2^-24 of a
  * power of two (masked uniform draws) and small-rational protocol constants; else 0. */
 int ssn_chain_supported(int k, int n, const uint64_t *ids, uint64_t p);

@@ -77,6 +77,7 @@ _SIGS = {
     "ssn_planes_shift": [_P, _U64, _I32, _P],
     "ssn_planes_cn": [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _U64, _I32, _P],
     "ssn_chain_supported": [_I32, _I32, _P, _U64],
+    "ssn_inv_table": [_P, _U64, _U64, _P],
 }
 
 
@@ -105,6 +106,7 @@ class ChainDesc(ctypes.Structure):
         ("plane_pstride", _U64), ("plane_lstride", _U64), ("plane_cstride", _U64), ("plane_istride", _U64),
         ("plane_wp", _I32), ("plane_copies", _I32), ("plane_nparty", _I32),
         ("scratch", _P),
+        ("inv_table", _P), ("inv_table_len", _U64),
     ]
 
 _lib = None

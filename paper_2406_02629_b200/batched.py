@@ -197,6 +197,24 @@ class BatchedEngine:
             self._record("gemm", e0, self._event(), m * B * H * Wd * O * K, f"k_gemm_p45w<{mode}>")
         return out
 
+    # ------------------------------------------------------------------ beta^-1 table
+    _INV_TABLES = {}                       # device -> table (shared by every engine)
+    INV_TABLE_MAX = 1 << 28                # gen_multiplicative_mask caps beta at 2^28 (S/masks.py:57-64)
+
+    def _inv_table(self, bmax):
+        """The trusted source's beta^-1 by lookup: table[b] = b^-1 mod p for b <= bmax, built
+        once per device by batch inversion (2 GiB for the 2^28 cap).  Opt-in (SSN_INV_TABLE=1):
+        measured no faster than the in-kernel per-warp batch inversion, which is the default."""
+        if os.environ.get("SSN_INV_TABLE", "0") != "1" or self.p != (1 << 45) - 55 or bmax > self.INV_TABLE_MAX:
+            return None
+        tab = self._INV_TABLES.get(self.dev)
+        if tab is None or tab.numel() <= bmax:
+            n = self.INV_TABLE_MAX + 1
+            tab = torch.empty(n, dtype=torch.int64, device=self.dev)
+            _lib.call("ssn_inv_table", _lib.ptr(tab), n, self.p, _lib.stream_ptr())
+            self._INV_TABLES[self.dev] = tab
+        return tab
+
     # ------------------------------------------------------------------ fused chains
     CHAIN_SCHEMES = ((2, 3), (3, 5), (4, 7))
 
@@ -297,6 +315,10 @@ class BatchedEngine:
             d.plane_wp, d.plane_copies, d.plane_nparty = Wp, 1, m
             self._planes_ready.add(chain[-1])
             shift_rows = m * gemm_mod.limbs(p) * C2 * B * H2 if copies == 3 else 0
+        if nl is not None:
+            tab = self._inv_table(d.bmax)
+            if tab is not None:
+                d.inv_table, d.inv_table_len = tab.data_ptr(), tab.numel()
         scratch = None
         if nl is not None and self.split_chain:
             scratch = torch.empty((n, nel), dtype=torch.int64, device=self.dev)

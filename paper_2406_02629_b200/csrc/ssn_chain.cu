@@ -92,6 +92,7 @@ struct ChainArgs {
     uint8_t *planes;
     u64 pl_ps, pl_ls, pl_cs, pl_is;
     int pl_wp, pl_copies, pl_nparty;
+    const u64 *inv_table;   // optional: inv_table[b] = b^-1 mod p for b in [1, bmax]
 };
 
 constexpr int CHAIN_THREADS = 128;
@@ -439,19 +440,31 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 4) k_chain_nonlin(ChainArgs a, 
             }
             plain[q] = pl;
             beta[q] = bt;
-            pre[q] = run;                       // product of this thread's earlier betas
-            run = mulm(run, bt);
+            if (a.inv_table) {
+                pre[q] = a.inv_table[bt];           // source's beta^-1 from the inverse table
+            } else {
+                pre[q] = run;                       // product of this thread's earlier betas
+                run = mulm(run, bt);
+            }
         }
-        // source: beta^-1 for every window of the warp from one inversion
-        const u64 wpre = warp_excl_prefix(run, lane);
-        const u64 wsuf = warp_excl_suffix(run, lane);
-        const u64 total = __shfl_sync(0xffffffffu, mulm(wpre, run), 31);
-        u64 inv = mulm(mulm(invm(total), wpre), wsuf);      // = run^-1
+        // source: beta^-1 for every window of the warp from one inversion (no table)
+        u64 inv = 0;
+        if (!a.inv_table) {
+            const u64 wpre = warp_excl_prefix(run, lane);
+            const u64 wsuf = warp_excl_suffix(run, lane);
+            const u64 total = __shfl_sync(0xffffffffu, mulm(wpre, run), 31);
+            inv = mulm(mulm(invm(total), wpre), wsuf);      // = run^-1
+        }
 #pragma unroll 1
         for (int q = WPT - 1; q >= 0; q--) {
             const uint32_t o = base + q * CHAIN_THREADS + threadIdx.x;
-            const u64 binv = mulm(inv, pre[q]);
-            inv = mulm(inv, beta[q]);
+            u64 binv;
+            if (a.inv_table) {
+                binv = pre[q];
+            } else {
+                binv = mulm(inv, pre[q]);
+                inv = mulm(inv, beta[q]);
+            }
             if (o < n_out) {
                 u64 cbi[K - 1];
                 coeffs<K>(cbi, a.sseed, a.sstream + 6, o);
@@ -595,6 +608,7 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
     a.pl_wp = d->plane_wp;
     a.pl_copies = d->plane_copies;
     a.pl_nparty = d->plane_nparty;
+    a.inv_table = (d->nonlin && d->inv_table && d->inv_table_len > d->bmax) ? d->inv_table : nullptr;
     if (a.planes && (!d->nonlin || a.pl_copies < 1 || a.pl_nparty < 1 || a.pl_nparty > N)) return SSN_ERR_ARG;
     if (a.senders > a.nout) return SSN_ERR_ARG;
     if (!d->nonlin) {
@@ -634,6 +648,42 @@ int supported(const u64 *ids, u64 p) {
 }
 
 }  // namespace
+
+namespace {
+// inverse table of [0, n): 1024 consecutive entries per thread by Montgomery's batch trick
+// (one Fermat inversion per thread), table[0] = 0
+__global__ void k_inv_table(u64 *__restrict__ t, u64 n) {
+    constexpr int G = 64;
+    const u64 start = (blockIdx.x * (u64)blockDim.x + threadIdx.x) * G;
+    if (start >= n) return;
+    u64 pre[G];
+    u64 run = 1;
+    for (int g = 0; g < G; g++) {
+        const u64 b = start + g;
+        pre[g] = run;
+        if (b > 0 && b < n) run = mulm(run, b);
+    }
+    u64 inv = canon(invm(canon(run)));
+    for (int g = G - 1; g >= 0; g--) {
+        const u64 b = start + g;
+        if (b >= n) continue;
+        if (b == 0) {
+            t[b] = 0;
+            continue;
+        }
+        t[b] = canon(mulm(inv, pre[g]));
+        inv = mulm(inv, b);
+    }
+}
+}  // namespace
+
+extern "C" int ssn_inv_table(uint64_t *table, uint64_t n, uint64_t p, void *stream) {
+    if (!table || n == 0 || n > (1ull << 32)) return SSN_ERR_ARG;
+    if (p != PP) return SSN_ERR_UNSUPPORTED;
+    const u64 threads = (n + 63) / 64;
+    k_inv_table<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(table, n);
+    return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
+}
 
 extern "C" int ssn_chain_supported(int k, int n, const uint64_t *ids, uint64_t p) {
     if (!ids) return 0;

@@ -182,3 +182,18 @@ def test_device_rng_masks_are_valid_sharings(ssn):
         z = gen_zero_shares((100,), s, rng)
         assert np.all(host(s.rec(z[:k])) == 0)
         assert len({int(v) for v in host(z[0].values)}) > 90
+
+
+def test_inverse_table():
+    """ssn_inv_table: table[b] * b == 1 (mod p) on samples of [1, 2^20), table[0] == 0."""
+    import torch
+    from paper_2406_02629_b200 import _lib
+    p = (1 << 45) - 55
+    n = 1 << 20
+    t = torch.empty(n, dtype=torch.int64, device="cuda")
+    _lib.call("ssn_inv_table", _lib.ptr(t), n, p, _lib.stream_ptr())
+    tab = t.cpu().numpy()
+    assert tab[0] == 0
+    rng = np.random.default_rng(5)
+    for b in list(rng.integers(1, n, size=200)) + [1, 2, n - 1, 63, 64, 65]:
+        assert int(tab[b]) * int(b) % p == 1, b
