@@ -201,8 +201,9 @@ def load_traffic():
 
 
 # executed thread instructions per element of the fused chain kernels (ncu
-# smsp__inst_executed x 32 / elements, ResNet-152 5PC, profiles/r01/README.md)
-CHAIN_ALU = {"chain": 3970}
+# smsp__inst_executed x 32 / elements over a ResNet-152 5PC step, profiles/r01/README.md:
+# k_chain_plain 2298 + k_chain_nonlin 1425 per nonlinear element)
+CHAIN_ALU = {"chain": 3630}
 
 
 def roofline(kstats, eng, dev_ms, bf16, hbm, src):
