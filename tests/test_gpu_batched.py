@@ -143,3 +143,22 @@ def test_lenet28_config1(ssn, k, n):
     assert np.array_equal(got.output, want[0])
     eng = BatchedEngine(model, scheme, batch=4, seed=3)
     assert np.array_equal(eng.run(xb), want)
+
+
+@pytest.mark.parametrize("split,planes,table", [(False, True, False), (True, False, False), (True, True, True)])
+def test_chain_variants_agree(ssn, split, planes, table, monkeypatch):
+    """The fused chain's variants -- one kernel vs reshare/nonlinearity split, limb planes from
+    the chain vs ssn_planes_cn, beta^-1 by per-warp batch inversion vs the inverse table --
+    all reproduce the plaintext (ResNet-50 bottlenecks at 64x64, 5 parties, verification)."""
+    from paper_2406_02629_b200 import resnet
+    from paper_2406_02629_b200.batched import BatchedEngine
+    monkeypatch.setenv("SSN_SPLIT_CHAIN", "1" if split else "0")
+    monkeypatch.setenv("SSN_CHAIN_PLANES", "1" if planes else "0")
+    monkeypatch.setenv("SSN_INV_TABLE", "1" if table else "0")
+    net = resnet.imagenet_resnet(50, image=64)
+    scheme = ssn.SssScheme(ssn.PrimeField(), 3, 5)
+    xb = net.random_inputs(seed=4, batch=2)
+    want, _ = resnet.plaintext_forward(net, xb)
+    eng = BatchedEngine(net, scheme, batch=2, seed=6, verify=True)
+    assert eng.split_chain == split and eng.chain_planes == planes
+    assert np.array_equal(eng.run(xb), want)
