@@ -16,10 +16,16 @@
 // TRUNC_MASKED, SHARE_DIST, NONLIN_MASKED, NONLIN_PLAIN) is computed exactly as the
 // reference computes it, and the hand-off between parties is a register move instead of an
 // HBM round trip.  The trusted source's masks (zero shares, alpha/comp, beta/beta^-1,
-// S/masks.py) are drawn in the same thread from the source's Philox lane; beta^-1 for the 32
-// windows of a warp comes from one Fermat inversion plus warp-shuffle prefix/suffix
-// products (Montgomery's batch trick across lanes).  HBM traffic per element: 8*m bytes of
-// GEMM output in, 8*n bytes of shares out (+8*n for a residual add).
+// S/masks.py) are drawn in the same thread from the source's Philox lane (coefficients
+// sliced densely from Philox reservoirs); beta^-1 for the 256 windows of a warp comes from one
+// Fermat inversion plus warp-shuffle prefix/suffix products (Montgomery's batch trick).  HBM
+// traffic per element: 8*m bytes of GEMM output in, 8*n bytes of shares out (+8*n for a
+// residual add, +6*m bytes of limb planes for the next implicit-GEMM conv).
+//
+// Kernels: k_chain_plain (reshare .. truncation [.. add]) and k_chain_nonlin (.. masked
+// nonlinearity).  A nonlinear chain normally runs as k_chain_plain into a scratch buffer
+// followed by k_chain_nonlin<SPLIT> -- two kernels of half the code each beat one kernel that
+// overflows the instruction cache (profiles/r01/README.md).
 //
 // The kernels are specialised to keep their SASS small (they are instruction-fetch bound
 // otherwise): the field must be pseudo-Mersenne with masked uniform draws (the default
