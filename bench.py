@@ -581,8 +581,10 @@ def main():
     l0 = _lib.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    h0 = time.perf_counter()
     for _ in range(args.steps):
         eng.run_device(x_dev)
+    host_ms = (time.perf_counter() - h0) * 1e3 / args.steps     # host enqueue time per step
     e1.record(stream)
     sync_all()
     launches = (_lib.launch_count() - l0) // args.steps
@@ -635,6 +637,7 @@ def main():
         "e2e": {"value": round(e2e, 3), "unit": "images/s",
                 "h2d_bytes_per_step": int(x_host.numel() * 8), "d2h_bytes_per_step": int(out_host.numel() * 8)},
         "gpu_launches": int(launches),
+        "host_enqueue_ms_per_step": round(host_ms, 3),
         "roofline": roof,
         "roofline_by_kernel": by_kernel,
         "cpu_baseline": cpu,
