@@ -573,6 +573,10 @@ def main():
 
     for _ in range(args.warmup):
         eng.run_device(x_dev)
+    # verification runs in every step's kernels; its host-side failure check is deferred to the
+    # end of the timed region (no per-step sync)
+    for e in getattr(eng, "engines", [eng]):
+        e.defer_verify = True
     # ---- device-resident timed region (value) ----
     sampler = ClockSampler(local)
     sampler.start()
@@ -581,12 +585,20 @@ def main():
     l0 = _lib.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
-    h0 = time.perf_counter()
     for _ in range(args.steps):
         eng.run_device(x_dev)
-    host_ms = (time.perf_counter() - h0) * 1e3 / args.steps     # host enqueue time per step
     e1.record(stream)
     sync_all()
+    # host enqueue cost of one step with an empty launch queue (CUDA-graph rationale: it must
+    # stay below the device time for the GPU never to starve)
+    h0 = time.perf_counter()
+    eng.run_device(x_dev)
+    host_ms = (time.perf_counter() - h0) * 1e3
+    torch.cuda.synchronize()
+    verify_failures = 0
+    for e in getattr(eng, "engines", [eng]):
+        if e.verify:
+            verify_failures += int(e.fail.item())
     launches = (_lib.launch_count() - l0) // args.steps
     dev_ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     kstats = eng.profile_summary(args.steps)
@@ -638,6 +650,7 @@ def main():
                 "h2d_bytes_per_step": int(x_host.numel() * 8), "d2h_bytes_per_step": int(out_host.numel() * 8)},
         "gpu_launches": int(launches),
         "host_enqueue_ms_per_step": round(host_ms, 3),
+        "verification_failures": verify_failures if verify else None,
         "roofline": roof,
         "roofline_by_kernel": by_kernel,
         "cpu_baseline": cpu,

@@ -82,6 +82,7 @@ class BatchedEngine:
         self.fault = None
         self.fuse = fuse
         self.chains = self._plan_chains() if fuse else {}
+        self._chain_cache = {}
         self._chain_member = {i: start for start, ch in self.chains.items() for i in ch[1:]}
         self._rt_all = _lib.u64_array([R[i][t] for t in range(n) for i in range(self.m)])
         self._plan_implicit_convs(implicit)
@@ -253,12 +254,11 @@ class BatchedEngine:
             chains[idx] = chain
         return chains
 
-    def _chain(self, chain, vals, src_rng, party_rng):
-        """One fused launch: reshare + rerand + bias + truncation [+ add] [+ nonlinear]."""
+    def _chain_static(self, chain):
+        """The launch-invariant part of a chain's descriptor (geometry, mask bounds, bias,
+        constants, plane buffer), built once per chain: host time per launch matters."""
         B, n, k, m, p = self.batch, self.n, self.k, self.m, self.p
-        lin = self.ops[chain[0]]
-        acc = self._gemm(chain[0], lin, vals[self._srcs(chain[0])[0]])
-        tr = self.ops[chain[1]]
+        lin, tr = self.ops[chain[0]], self.ops[chain[1]]
         add = next((self.ops[i] for i in chain[2:] if self.ops[i].kind == "add"), None)
         nl = next((self.ops[i] for i in chain[2:] if self.ops[i].kind == "nonlinear"), None)
         last = self.ops[chain[-1]]
@@ -266,15 +266,15 @@ class BatchedEngine:
         ohw = _count(lin.out_shape[1:]) if len(lin.out_shape) > 1 else 1
         nel = B * _count(lin.out_shape)
         n_out = B * _count(last.out_shape)
-        Y = torch.empty((n, B) + tuple(last.out_shape), dtype=torch.int64, device=self.dev)
         d = _lib.ChainDesc()
-        d.acc, d.acc_pstride = acc.data_ptr(), nel
+        d.acc_pstride = nel
         bias = self.W[lin.weight + ".b"]
         d.bias, d.bias_pstride, d.bias_div, d.bias_mod = bias.data_ptr(), O, ohw, O
+        other = None
         if add is not None:
             other = [s for s in self._srcs(chain[2]) if s != chain[1]][0]
-            d.other, d.other_pstride = vals[other].data_ptr(), nel
-        d.out, d.out_pstride = Y.data_ptr(), n_out
+            d.other_pstride = nel
+        d.out_pstride = n_out
         d.nel = nel
         d.nout = n if lin.passive_out else k
         d.value_bound, d.r, d.d = tr.value_bound, tr.r, tr.divisor
@@ -293,14 +293,14 @@ class BatchedEngine:
             d.nb, d.c, d.h, d.w, d.kh, d.kw = B, c, h, w, kh, kw
             d.fan = n if nl.passive_out else k
             d.bmax = multiplicative_mask_bound(self.scheme.field, nl.value_bound)
-        d.party_seed, d.party_stream = party_rng.seed, party_rng.next_stream(m + 1)
-        d.src_seed, d.src_stream = src_rng.seed, src_rng.next_stream(7)
+            tab = self._inv_table(d.bmax)
+            if tab is not None:
+                d.inv_table, d.inv_table_len = tab.data_ptr(), tab.numel()
         d.k, d.n = k, n
         d.ids, d.rt = ctypes.addressof(self.ids_all), ctypes.addressof(self._rt_all)
         d.ext = ctypes.addressof(self._ext_host) if self._ext_host is not None else None
         d.p = p
-        d.fault_rank = self.fault[1] if (self.fault is not None and self.fault[0] == chain[0]) else -1
-        shift_rows = 0
+        shift = None
         ps = self._plane_src.get(chain[-1])
         if ps is not None and nl is not None and self.chain_planes and tuple(last.out_shape) == tuple(ps[3:]):
             _, Wp, copies, C2, H2, W2 = ps
@@ -313,25 +313,44 @@ class BatchedEngine:
             d.plane_lstride = C2 * B * H2 * Wp
             d.plane_pstride = gemm_mod.limbs(p) * C2 * B * H2 * Wp
             d.plane_wp, d.plane_copies, d.plane_nparty = Wp, 1, m
-            self._planes_ready.add(chain[-1])
-            shift_rows = m * gemm_mod.limbs(p) * C2 * B * H2 if copies == 3 else 0
-        if nl is not None:
-            tab = self._inv_table(d.bmax)
-            if tab is not None:
-                d.inv_table, d.inv_table_len = tab.data_ptr(), tab.numel()
+            if copies == 3:
+                shift = (buf.data_ptr(), m * gemm_mod.limbs(p) * C2 * B * H2, Wp)
+        nbytes = 8 * m * nel + (8 * n * nel if add is not None else 0)
+        nbytes += 8 * (d.fan * n_out if nl is not None else n * nel)
+        return {"d": d, "lin": lin, "last": last, "other": other, "nl": nl is not None, "nel": nel,
+                "shift": shift, "planes": bool(d.planes), "nbytes": nbytes}
+
+    def _chain(self, chain, vals, src_rng, party_rng):
+        """One fused launch: reshare + rerand + bias + truncation [+ add] [+ nonlinear]."""
+        B, n, m = self.batch, self.n, self.m
+        st = self._chain_cache.get(chain[0])
+        if st is None:
+            st = self._chain_cache[chain[0]] = self._chain_static(chain)
+        d = st["d"]
+        acc = self._gemm(chain[0], st["lin"], vals[self._srcs(chain[0])[0]])
+        Y = torch.empty((n, B) + tuple(st["last"].out_shape), dtype=torch.int64, device=self.dev)
+        d.acc = acc.data_ptr()
+        if st["other"] is not None:
+            d.other = vals[st["other"]].data_ptr()
+        d.out = Y.data_ptr()
+        d.party_seed, d.party_stream = party_rng.seed, party_rng.next_stream(m + 1)
+        d.src_seed, d.src_stream = src_rng.seed, src_rng.next_stream(7)
+        d.fault_rank = self.fault[1] if (self.fault is not None and self.fault[0] == chain[0]) else -1
         scratch = None
-        if nl is not None and self.split_chain:
-            scratch = torch.empty((n, nel), dtype=torch.int64, device=self.dev)
+        if st["nl"] and self.split_chain:
+            scratch = torch.empty((n, st["nel"]), dtype=torch.int64, device=self.dev)
             d.scratch = scratch.data_ptr()
+        else:
+            d.scratch = None
+        if st["planes"]:
+            self._planes_ready.add(chain[-1])
         e0 = self._event() if self._prof is not None else None
         _lib.call("ssn_layer_chain", ctypes.byref(d), _lib.stream_ptr())
-        if d.planes and shift_rows:
-            _lib.call("ssn_planes_shift", buf.data_ptr(), shift_rows, d.plane_wp, _lib.stream_ptr())
+        if st["shift"] is not None:
+            _lib.call("ssn_planes_shift", *st["shift"], _lib.stream_ptr())
         if e0 is not None:
-            nbytes = 8 * m * nel + (8 * n * nel if add is not None else 0)
-            nbytes += 8 * (d.fan * n_out if nl is not None else n * nel)
-            self._record("chain", e0, self._event(), nbytes, "k_chain_nonlin" if nl is not None else "k_chain_plain",
-                         elems=nel)
+            self._record("chain", e0, self._event(), st["nbytes"],
+                         "k_chain_nonlin" if st["nl"] else "k_chain_plain", elems=st["nel"])
         self.kernel_launches += 1
         return Y
 
@@ -644,9 +663,18 @@ class BatchedEngine:
         out = torch.empty_like(v)
         _lib.call("ssn_decode_signed", _lib.ptr(v), _lib.ptr(out), N, p, _lib.stream_ptr())
         self.kernel_launches += 2
-        if self.verify:
+        if self.verify and not self.defer_verify:
             self._check_failures()
         return out.reshape((B,) + tuple(op.out_shape))
+
+    # defer_verify: the Reed-Solomon checks still run inside every step's kernels, but the host
+    # reads the device failure counter only in check_verification() -- no per-step sync, so the
+    # host enqueues step i+1 while the GPU runs step i
+    defer_verify = False
+
+    def check_verification(self):
+        """Raise VerificationError if any deferred check failed since the last call."""
+        self._check_failures()
 
     def _check_failures(self):
         bad = int(self.fail.item())

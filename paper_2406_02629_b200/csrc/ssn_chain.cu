@@ -32,6 +32,7 @@
 // p = 2^45 - 55, S/field.py:21) and every protocol constant must be a small rational (true
 // for the default party ids 1..n).  ssn_chain_supported() tells the host; other schemes use
 // the unfused kernels of ssn_elementwise.cu.
+#include <cstring>
 #include "ssn.h"
 #include "ssn_field.cuh"
 #include "ssn_lincomb.cuh"
@@ -556,8 +557,34 @@ int build_tables(STables<K, N> &tb, const u64 *ids, const u64 *rt, const u64 *ex
 template <int K, int N>
 int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
     const u64 p = d->p;
-    STables<K, N> tb;
-    if (!build_tables<K, N>(tb, d->ids, d->rt, d->ext, p)) return SSN_ERR_UNSUPPORTED;
+    // the protocol constants depend only on (ids, R, RS rows, p): rebuilt (rational
+    // reconstruction, inverses) only when they change -- host time per launch matters, a
+    // ResNet-152 step makes ~300 launches
+    constexpr int M = 2 * K - 1;
+    struct Key {
+        u64 ids[N], rt[N * M], ext[N * K], p;
+        int has_ext;
+    };
+    static thread_local Key last_key;
+    static thread_local STables<K, N> last_tb;
+    static thread_local bool have = false;
+    Key key;
+    memset(&key, 0, sizeof(key));
+    for (int t = 0; t < N; t++) key.ids[t] = d->ids[t];
+    for (int t = 0; t < N * M; t++) key.rt[t] = d->rt[t];
+    key.has_ext = d->ext != nullptr;
+    if (d->ext)
+        for (int t = 0; t < (N - K) * K; t++) key.ext[t] = d->ext[t];
+    key.p = p;
+    if (!have || memcmp(&key, &last_key, sizeof(key)) != 0) {
+        if (!build_tables<K, N>(last_tb, d->ids, d->rt, d->ext, p)) {
+            have = false;
+            return SSN_ERR_UNSUPPORTED;
+        }
+        last_key = key;
+        have = true;
+    }
+    const STables<K, N> &tb = last_tb;
     const SsnField f = ssn_make_field(p);
     ChainArgs a;
     a.acc = d->acc;
