@@ -162,3 +162,16 @@ def test_chain_variants_agree(ssn, split, planes, table, monkeypatch):
     eng = BatchedEngine(net, scheme, batch=2, seed=6, verify=True)
     assert eng.split_chain == split and eng.chain_planes == planes
     assert np.array_equal(eng.run(xb), want)
+
+
+def test_resnet152_5pc_full_size_matches_plaintext(ssn):
+    """The headline configuration at full size (ResNet-152, 224x224, 5 parties, t=2,
+    verification on): decoded logits equal the exact integer plaintext, no RS failures."""
+    from paper_2406_02629_b200 import resnet
+    from paper_2406_02629_b200.batched import BatchedEngine
+    net = resnet.imagenet_resnet(152)
+    xb = net.random_inputs(seed=8, batch=2)
+    eng = BatchedEngine(net, ssn.SssScheme(ssn.PrimeField(), 3, 5), batch=2, seed=13, verify=True)
+    want, _ = resnet.plaintext_forward(net, xb, device="cuda")
+    assert np.array_equal(eng.run(xb), want)
+    assert int(eng.fail.item()) == 0
