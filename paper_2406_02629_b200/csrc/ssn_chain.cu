@@ -489,9 +489,18 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 4) k_chain_nonlin(ChainArgs a, 
                     if (t < a.fan) {
                         const u64 v = canon(mulm(plain[q], share_raw<K, N>(binv, cbi, tb, t)));
                         a.out[(u64)t * a.out_ps + o] = v;
-                        if (pb != nullptr && t < a.pl_nparty)          // limb planes for the next conv
-                            emit_planes(pb + (u64)t * a.pl_ps, v, xq, a.pl_copies, a.pl_nparty * a.pl_ps,
-                                        a.pl_ls, a.pl_wp);
+                        if (pb != nullptr && t < a.pl_nparty) {        // limb planes for the next conv
+                            if (SPLIT && a.pl_copies == 1) {
+                                // inline single copy: offsets t*ps + l*ls are warp-uniform
+                                uint8_t *dst = pb + xq;
+#pragma unroll
+                                for (int l = 0; l < 6; l++)
+                                    dst[(u64)t * a.pl_ps + (u64)l * a.pl_ls] = (uint8_t)(v >> (8 * l));
+                            } else {
+                                emit_planes(pb + (u64)t * a.pl_ps, v, xq, a.pl_copies, a.pl_nparty * a.pl_ps,
+                                            a.pl_ls, a.pl_wp);
+                            }
+                        }
                     }
             }
         }
