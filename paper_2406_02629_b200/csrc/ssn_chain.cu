@@ -297,10 +297,10 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
     const uint32_t ch = bq - fdiv(bq, a.bias_mod) * a.bias_mod.d;
     // ---- step 2 (RESHARE_BACK): front fr applies R^T; step 3: out rank t reconstructs,
     //      + zero share (rerand) + bias share, then + alpha share (TRUNC_MASKED)
-    // Rolled loop over the out ranks (the unrolled form pushed the kernel past the instruction
-    // cache); masked[] then lives in local memory (L1), tb.rt[t] is an indexed constant load.
+    // Unrolled over the out ranks: with the nonlinearity split into its own kernel, k_chain_plain
+    // stays within the instruction cache and the unrolled form keeps masked[] in registers.
     u64 masked[N];
-#pragma unroll 1
+#pragma unroll
     for (int t = 0; t < N; t++) {
         if (t < a.senders) {
             u64 back[K];
