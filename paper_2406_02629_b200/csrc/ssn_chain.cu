@@ -104,7 +104,6 @@ struct ChainArgs {
 
 constexpr int CHAIN_THREADS = 128;
 constexpr int PLAIN_THREADS = 128;
-constexpr int CHAIN_WARPS = CHAIN_THREADS / 32;
 
 // ---- arithmetic in the default field p = 2^45 - 55 (S/field.py:21) with compile-time fold
 constexpr int PS = 45;
