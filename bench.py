@@ -200,10 +200,9 @@ def load_traffic():
         return {}
 
 
-# executed thread instructions per element of the fused chain kernels (ncu
-# smsp__inst_executed x 32 / elements over a ResNet-152 5PC step, profiles/r01/README.md:
-# k_chain_plain 2298 + k_chain_nonlin 1425 per nonlinear element)
-CHAIN_ALU = {"chain": 3630}
+# executed thread instructions per chain element, by (k, n) (ncu smsp__inst_executed x 32 /
+# elements over a ResNet-152 5PC step, profiles/r01/README.md); other schemes: not calibrated
+CHAIN_ALU = {(3, 5): 3316}
 
 
 def roofline(kstats, eng, dev_ms, bf16, hbm, src):
@@ -231,13 +230,14 @@ def roofline(kstats, eng, dev_ms, bf16, hbm, src):
             r = {"bound": "hbm", "achieved": round(achieved, 1), "peak": round(hbm, 1), "unit": "GB/s",
                  "frac": round(achieved / hbm, 4),
                  "note": "algorithmic bytes per launch (DESIGN.md section 3) / CUDA-event launch time"}
-            alu = CHAIN_ALU.get(cls)
+            alu = CHAIN_ALU.get((eng.k, eng.n)) if cls == "chain" else None
             if alu and st.get("elems_per_launch"):
                 # the fused protocol chain is integer-ALU bound: executed thread instructions per
                 # element (ncu, profiles/r01/README.md) x elements / time vs the SM issue peak
                 rate = alu * st["elems_per_launch"] / sec
                 peak_i = 148 * 128 * 1.965e9
-                r["alu_issue"] = {"thread_instr_per_elem": alu, "achieved_tinstr_per_s": float(f"{rate:.4g}"),
+                r["alu_issue"] = {"thread_instr_per_elem": alu, "calibration": "ResNet-152 5PC ncu count",
+                                  "achieved_tinstr_per_s": float(f"{rate:.4g}"),
                                   "peak_tinstr_per_s": float(f"{peak_i:.4g}"), "frac": round(rate / peak_i, 4)}
         t = traffic.get(cls)
         r["traffic"] = round(t) if t else None
