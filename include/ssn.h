@@ -221,6 +221,9 @@ typedef struct ssn_chain_desc {
      * b^-1 mod p, b < inv_table_len (must exceed bmax) instead of batch inversion */
     const uint64_t *inv_table;
     uint64_t inv_table_len;
+    /* 1: only the masked nonlinearity (sss_nonlinear) of the n parties' input shares in acc
+     * (a nonlinear op outside a linear chain, e.g. the global pool); reshare fields unused */
+    int nonlin_only;
 } ssn_chain_desc;
 
 int ssn_layer_chain(const ssn_chain_desc *desc, void *stream);

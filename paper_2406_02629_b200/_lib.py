@@ -107,6 +107,7 @@ class ChainDesc(ctypes.Structure):
         ("plane_wp", _I32), ("plane_copies", _I32), ("plane_nparty", _I32),
         ("scratch", _P),
         ("inv_table", _P), ("inv_table_len", _U64),
+        ("nonlin_only", _I32),
     ]
 
 _lib = None

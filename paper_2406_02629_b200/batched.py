@@ -481,7 +481,8 @@ class BatchedEngine:
             elif op.kind == "truncation":
                 y = self._truncation(idx, op, xin, masked_for.get(src, False), src_rng, party_rng)
             elif op.kind == "nonlinear":
-                y = self._nonlinear(idx, op, xin, src_rng)
+                y = (self._nonlinear_fused(idx, op, xin, src_rng) if self.chains
+                     else self._nonlinear(idx, op, xin, src_rng))
             elif op.kind == "add":
                 other = vals[op.src2]
                 nn = _count(op.out_shape) * B
@@ -619,6 +620,39 @@ class BatchedEngine:
                   _lib.ptr(self.fail) if self.verify else None, N, p, _lib.stream_ptr())
         Y = torch.empty((n, B) + tuple(op.out_shape), dtype=torch.int64, device=self.dev)
         self._ew(0, FR, Cm, Y, n * N)
+        self.kernel_launches += 1
+        return Y
+
+    def _nonlinear_fused(self, idx, op, X, src_rng):
+        """A nonlinear op outside a linear chain (e.g. the global pool) as ONE launch of the
+        chain kernel's masked-nonlinearity stage (mask, elite rec/ReLU/pool, beta^-1 output)."""
+        B, n, k, m, p = self.batch, self.n, self.k, self.m, self.p
+        n_in, n_out = B * _count(op.in_shape), B * _count(op.out_shape)
+        if op.pool_kind is not None:
+            (c, h, w), (kh, kw) = op.in_shape, op.pool
+            kind = 1 if op.pool_kind == "max" else 2
+        elif len(op.in_shape) == 3:
+            (c, h, w), kh, kw, kind = op.in_shape, 1, 1, 0
+        else:
+            c, h, w, kh, kw, kind = _count(op.in_shape), 1, 1, 1, 1, 0
+        Y = torch.empty((n, B) + tuple(op.out_shape), dtype=torch.int64, device=self.dev)
+        d = _lib.ChainDesc()
+        d.acc, d.acc_pstride = X.data_ptr(), n_in
+        d.out, d.out_pstride = Y.data_ptr(), n_out
+        d.nel = n_in
+        d.nonlin, d.nonlin_only, d.relu, d.pool_kind = 1, 1, int(bool(op.relu)), kind
+        d.nb, d.c, d.h, d.w, d.kh, d.kw = B, c, h, w, kh, kw
+        d.fan = n if op.passive_out else k
+        d.bmax = multiplicative_mask_bound(self.scheme.field, op.value_bound)
+        d.nout, d.r, d.d, d.emax = n, 1, 1, 1
+        d.bias_div, d.bias_mod = 1, 1
+        d.src_seed, d.src_stream = src_rng.seed, src_rng.next_stream(7)
+        d.k, d.n = k, n
+        d.ids, d.rt = ctypes.addressof(self.ids_all), ctypes.addressof(self._rt_all)
+        d.ext = ctypes.addressof(self._ext_host) if self._ext_host is not None else None
+        d.p = p
+        d.fault_rank = -1
+        _lib.call("ssn_layer_chain", ctypes.byref(d), _lib.stream_ptr())
         self.kernel_launches += 1
         return Y
 

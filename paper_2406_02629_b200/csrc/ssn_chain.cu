@@ -661,7 +661,10 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
         u64 blocks = (n_out + CHAIN_THREADS * WPT - 1) / (CHAIN_THREADS * WPT);
         if (blocks > 148ull * 16) blocks = 148ull * 16;
         if (blocks < 1) blocks = 1;
-        if (d->scratch) {
+        if (d->nonlin_only) {
+            // a standalone masked nonlinearity: acc holds the n parties' input shares
+            k_chain_nonlin<K, N, true><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a, tb, f);
+        } else if (d->scratch) {
             // split: reshare + truncation (+ add) into scratch [n][nel], then the nonlinearity
             ChainArgs a1 = a;
             a1.out = d->scratch;
@@ -735,8 +738,10 @@ extern "C" int ssn_chain_supported(int k, int n, const uint64_t *ids, uint64_t p
 }
 
 extern "C" int ssn_layer_chain(const ssn_chain_desc *d, void *stream) {
-    if (!d || !d->acc || !d->bias || !d->out || !d->ids || !d->rt) return SSN_ERR_ARG;
-    if (d->r < 1 || d->d < 1 || d->emax < 1 || d->nout < d->k || d->nout > d->n) return SSN_ERR_ARG;
+    if (!d || !d->acc || !d->out || !d->ids || !d->rt) return SSN_ERR_ARG;
+    if (d->nonlin_only && !d->nonlin) return SSN_ERR_ARG;
+    if (!d->nonlin_only && (!d->bias || d->r < 1 || d->d < 1 || d->emax < 1 || d->nout < d->k || d->nout > d->n))
+        return SSN_ERR_ARG;
     if (d->verify && (!d->ext || d->nout != d->n)) return SSN_ERR_ARG;
     if (d->nel >= (1ull << 32) || d->bias_div < 1 || d->bias_mod < 1 || d->bias_div >= (1ull << 32) ||
         d->bias_mod >= (1ull << 32))
