@@ -431,6 +431,9 @@ def run_party_placement(args):
     scheme = SssScheme(PrimeField(), k, n)
     g = rank // (n + 1)
     eng = PartyShardedEngine(model, scheme, batch=B, seed=7 + g, verify=verify, group=g) if g < groups else None
+    # a collective before the first point-to-point call creates the NCCL communicator on every
+    # rank (batch_isend_irecv as the first call of a group must otherwise involve all ranks)
+    dist.barrier()
     xb = (model.random_inputs(seed=100 + g, batch=B) if hasattr(model, "random_inputs")
           else np.stack([__import__("paper_2406_02629_b200.model", fromlist=["random_input"])
                          .random_input(100 + g, model, index=i)[0] for i in range(B)]))
