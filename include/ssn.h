@@ -36,6 +36,10 @@ extern "C" {
 
 int ssn_version(void);
 
+/* Kernels this library has launched in this process (every entry point counts each of its
+ * launches; bench.py reports the per-step difference as gpu_launches). */
+unsigned long long ssn_kernel_launches(void);
+
 /* out[i] = a[i] OP b[bidx(i)], bidx(i) = (i / b_div) % b_mod + (i / b_div2) * b_mul2.
  * op: 0 add, 1 sub, 2 mul, 3 neg (b unused).
  * Replaces share_add/share_sub/share_mul (S/sss.py:238-276), PrimeField.add/sub/mul/neg

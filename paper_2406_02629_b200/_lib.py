@@ -49,6 +49,7 @@ _U64, _I64, _I32, _P = ctypes.c_uint64, ctypes.c_int64, ctypes.c_int, ctypes.c_v
 
 _SIGS = {
     "ssn_version": [],
+    "ssn_kernel_launches": [],
     "ssn_ewise": [_I32, _P, _P, _P, _U64, _U64, _U64, _U64, _U64, _U64, _P],
     "ssn_gen": [_P, _U64, _P, _U64, _U64, _U64, _I32, _P, _I32, _P, _U64, _U64, _U64, _I32, _U64, _P],
     "ssn_rec": [_P, _U64, _U64, _P, _I32, _P, _U64, _U64, _I32, _U64, _P],
@@ -128,23 +129,20 @@ def load(require_cuda=True):
         for name, args in _SIGS.items():
             fn = getattr(L, name)
             fn.argtypes = args
-            fn.restype = ctypes.c_int
+            fn.restype = ctypes.c_uint64 if name == "ssn_kernel_launches" else ctypes.c_int
         _lib = L
     if require_cuda and not torch.cuda.is_available():
         raise SsnUnavailable("no CUDA device: the SSNet B200 path has no CPU fallback")
     return _lib
 
 
-_launches = [0]
-
-
 def launch_count():
-    """Number of kernel-launching C-ABI calls made by this process (one kernel each)."""
-    return _launches[0]
+    """Kernels launched by libssn_b200 in this process (the library's own counter, incremented
+    at every launch site; an entry point may launch more than one kernel)."""
+    return int(load(require_cuda=False).ssn_kernel_launches())
 
 
 def call(name, *args):
-    _launches[0] += 1
     rc = getattr(load(), name)(*args)
     if rc != 0:
         if rc == SSN_ERR_ARG:

@@ -655,6 +655,7 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
     if (!d->nonlin) {
         u64 blocks = (a.nel + PLAIN_THREADS - 1) / PLAIN_THREADS;
         if (blocks > 148ull * 16) blocks = 148ull * 16;
+        SSN_COUNT_LAUNCH();
         k_chain_plain<K, N><<<(unsigned)blocks, PLAIN_THREADS, 0, st>>>(a, tb, f);
     } else {
         const u64 n_out = (u64)d->nb * d->c * (d->h / d->kh) * (d->w / d->kw);
@@ -663,6 +664,7 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
         if (blocks < 1) blocks = 1;
         if (d->nonlin_only) {
             // a standalone masked nonlinearity: acc holds the n parties' input shares
+            SSN_COUNT_LAUNCH();
             k_chain_nonlin<K, N, true><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a, tb, f);
         } else if (d->scratch) {
             // split: reshare + truncation (+ add) into scratch [n][nel], then the nonlinearity
@@ -672,12 +674,15 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
             a1.planes = nullptr;
             u64 b1 = (a.nel + PLAIN_THREADS - 1) / PLAIN_THREADS;
             if (b1 > 148ull * 16) b1 = 148ull * 16;
+            SSN_COUNT_LAUNCH();
             k_chain_plain<K, N><<<(unsigned)b1, PLAIN_THREADS, 0, st>>>(a1, tb, f);
             ChainArgs a2 = a;
             a2.acc = d->scratch;
             a2.acc_ps = a.nel;
+            SSN_COUNT_LAUNCH();
             k_chain_nonlin<K, N, true><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a2, tb, f);
         } else {
+            SSN_COUNT_LAUNCH();
             k_chain_nonlin<K, N, false><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a, tb, f);
         }
     }
@@ -725,6 +730,7 @@ extern "C" int ssn_inv_table(uint64_t *table, uint64_t n, uint64_t p, void *stre
     if (!table || n == 0 || n > (1ull << 32)) return SSN_ERR_ARG;
     if (p != PP) return SSN_ERR_UNSUPPORTED;
     const u64 threads = (n + 63) / 64;
+    SSN_COUNT_LAUNCH();
     k_inv_table<<<(unsigned)((threads + 255) / 256), 256, 0, (cudaStream_t)stream>>>(table, n);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }

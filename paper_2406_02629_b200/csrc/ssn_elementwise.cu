@@ -73,6 +73,7 @@ extern "C" int ssn_ewise(int op, const u64 *a, const u64 *b, u64 *out, u64 n, u6
     else if (b_mul2 == 0 && b_mod == 1) mode = 1;
     else if (b_mul2 == 0 && b_div == 1 && n % b_mod == 0 && n / b_mod <= 65535) mode = 2;
     dim3 grid = mode == 2 ? ssn_grid2(b_mod, (int)(n / b_mod)) : dim3(ssn_blocks(n));
+    SSN_COUNT_LAUNCH();
     k_ewise<<<grid, 256, 0, (cudaStream_t)stream>>>(op, mode, a, b, out, n, b_div, b_mod, b_div2, b_mul2,
                                                     ssn_make_field(p));
     return ssn_check_launch();
@@ -100,6 +101,7 @@ extern "C" int ssn_gen(const u64 *secret, u64 secret_bstride, const u64 *coeffs,
     if (km1 < 0 || km1 > SSN_MAXK || nids < 1 || nids > SSN_MAXJ || nbatch < 1) return SSN_ERR_ARG;
     if (n == 0) return 0;
     PowTable pw = make_pows(ids, nids, km1, p);
+    SSN_COUNT_LAUNCH();
     k_gen<<<ssn_grid2(n, nbatch), 256, 0, (cudaStream_t)strm>>>(secret, secret_bstride, coeffs, coeff_bstride,
                                                                   seed, stream, km1, pw, nids, out, out_bstride,
                                                                   out_tstride, n, nbatch, ssn_make_field(p));
@@ -125,6 +127,7 @@ extern "C" int ssn_rec(const u64 *pts, u64 pts_bstride, u64 pts_jstride, const u
     if (m < 1 || m > SSN_MAXJ || nbatch < 1) return SSN_ERR_ARG;
     if (n == 0) return 0;
     Weights W = make_weights(w, m, p);
+    SSN_COUNT_LAUNCH();
     k_rec<<<ssn_grid2(n, nbatch), 256, 0, (cudaStream_t)strm>>>(pts, pts_bstride, pts_jstride, W, m, out,
                                                                   out_bstride, n, nbatch, ssn_make_field(p));
     return ssn_check_launch();
@@ -160,6 +163,7 @@ extern "C" int ssn_reduce_apply(const u64 *pts, u64 pts_bstride, u64 pts_jstride
         int ok = make_row(R.r[t], row, m, p);
         if (t < nout) R.small = R.small && ok;
     }
+    SSN_COUNT_LAUNCH();
     k_reduce_apply<<<ssn_grid2(n, nbatch), 256, 0, (cudaStream_t)strm>>>(pts, pts_bstride, pts_jstride, R, m, nout,
                                                                            out, out_bstride, out_tstride, n, nbatch,
                                                                            ssn_make_field(p));
@@ -197,6 +201,7 @@ extern "C" int ssn_reshare_finish(const u64 *pts, u64 pts_bstride, u64 pts_jstri
     if (k < 1 || k > SSN_MAXP || nbatch < 1 || bias_div == 0 || bias_mod == 0) return SSN_ERR_ARG;
     if (n == 0) return 0;
     Weights W = make_weights(w, k, p);
+    SSN_COUNT_LAUNCH();
     k_reshare_finish<<<ssn_grid2(n, nbatch), 256, 0, (cudaStream_t)strm>>>(
         pts, pts_bstride, pts_jstride, W, k, zero, zero_bstride, bias, bias_bstride, bias_div, bias_mod, alpha,
         alpha_bstride, out, out_bstride, n, nbatch, ssn_make_field(p));
@@ -259,6 +264,7 @@ extern "C" int ssn_trunc_elite(const u64 *pts, u64 pts_jstride, int npts, int k,
         rshift = 0;
         while ((1ll << rshift) < r) rshift++;
     }
+    SSN_COUNT_LAUNCH();
     k_trunc_elite<<<ssn_blocks(n), 256, 0, (cudaStream_t)strm>>>(pts, pts_jstride, npts, k, W, E, lo, neglo_mod, r,
                                                                  rshift, d, coeffs, seed, stream, km1, pw, nids, out,
                                                                  out_tstride, fail, n, ssn_make_field(p));
@@ -310,6 +316,7 @@ extern "C" int ssn_nonlin_elite(const u64 *pts, u64 pts_jstride, int m, const u6
     const u64 n_out = (u64)nb * c * (h / kh) * (wd / kw);
     if (n_out == 0) return 0;
     if (n_out >= (1ull << 32)) return SSN_ERR_UNSUPPORTED;
+    SSN_COUNT_LAUNCH();
     k_nonlin_elite<<<ssn_blocks(n_out), 256, 0, (cudaStream_t)strm>>>(pts, pts_jstride, m, W, relu, pool_kind, c, h,
                                                                       wd, kh, kw, plain, n_out, ssn_make_field(p));
     return ssn_check_launch();
@@ -327,6 +334,7 @@ __global__ void k_encode(const i64 *__restrict__ x, u64 *__restrict__ out, u64 n
 }
 extern "C" int ssn_encode_signed(const i64 *x, u64 *out, u64 n, unsigned long long *overflow, u64 p, void *strm) {
     if (n == 0) return 0;
+    SSN_COUNT_LAUNCH();
     k_encode<<<ssn_blocks(n), 256, 0, (cudaStream_t)strm>>>(x, out, n, ssn_make_field(p), overflow);
     return ssn_check_launch();
 }
@@ -339,6 +347,7 @@ __global__ void k_decode(const u64 *__restrict__ v, i64 *__restrict__ out, u64 n
 }
 extern "C" int ssn_decode_signed(const u64 *v, i64 *out, u64 n, u64 p, void *strm) {
     if (n == 0) return 0;
+    SSN_COUNT_LAUNCH();
     k_decode<<<ssn_blocks(n), 256, 0, (cudaStream_t)strm>>>(v, out, n, ssn_make_field(p));
     return ssn_check_launch();
 }
@@ -349,6 +358,7 @@ __global__ void k_inv(const u64 *__restrict__ a, u64 *__restrict__ out, u64 n, S
 }
 extern "C" int ssn_inv(const u64 *a, u64 *out, u64 n, u64 p, void *strm) {
     if (n == 0) return 0;
+    SSN_COUNT_LAUNCH();
     k_inv<<<ssn_blocks(n), 256, 0, (cudaStream_t)strm>>>(a, out, n, ssn_make_field(p));
     return ssn_check_launch();
 }
@@ -360,6 +370,7 @@ __global__ void k_rand(u64 *__restrict__ out, u64 n, u64 lo, u64 range, u64 seed
 extern "C" int ssn_rand(u64 *out, u64 n, u64 lo, u64 range, u64 seed, u64 stream, void *strm) {
     if (range == 0) return SSN_ERR_ARG;
     if (n == 0) return 0;
+    SSN_COUNT_LAUNCH();
     k_rand<<<ssn_blocks(n), 256, 0, (cudaStream_t)strm>>>(out, n, lo, range, seed, stream);
     return ssn_check_launch();
 }
@@ -392,6 +403,7 @@ extern "C" int ssn_mask_trunc(u64 n, u64 step, u64 emax, u64 seed, u64 stream, i
     if (emax < 1 || km1 < 0 || km1 > SSN_MAXK || nids < 1 || nids > SSN_MAXJ) return SSN_ERR_ARG;
     if (n == 0) return 0;
     PowTable pw = make_pows(ids, nids, km1, p);
+    SSN_COUNT_LAUNCH();
     k_mask_trunc<<<ssn_blocks(n), 256, 0, (cudaStream_t)strm>>>(n, step, emax, seed, stream, km1, pw, nids, alpha,
                                                                 comp, out_tstride, ssn_make_field(p));
     return ssn_check_launch();
@@ -470,6 +482,7 @@ extern "C" int ssn_mask_beta(int nb, int c, int h, int wd, int kh, int kw, u64 b
     u64 blocks = (n_out + 256 * SSN_WPT - 1) / (256 * SSN_WPT);
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
+    SSN_COUNT_LAUNCH();
     k_mask_beta<<<(unsigned)blocks, 256, 0, (cudaStream_t)strm>>>(c, h, wd, kh, kw, n_out, bmax, seed, stream, km1,
                                                                   pw, nids, beta, beta_tstride, binv, binv_tstride,
                                                                   ssn_make_field(p));
@@ -489,8 +502,10 @@ extern "C" int ssn_pool_expand(const u64 *blk, u64 *out, int nb, int c, int h, i
     if (kh < 1 || kw < 1 || h % kh || wd % kw) return SSN_ERR_ARG;
     const u64 n = (u64)nb * c * h * wd;
     if (n == 0) return 0;
+    SSN_COUNT_LAUNCH();
     k_pool_expand<<<ssn_blocks(n), 256, 0, (cudaStream_t)strm>>>(blk, out, c, h, wd, kh, kw, n);
     return ssn_check_launch();
 }
 
 extern "C" int ssn_version(void) { return SSN_ABI_VERSION; }
+extern "C" unsigned long long ssn_kernel_launches(void) { return ssn_launch_counter(); }

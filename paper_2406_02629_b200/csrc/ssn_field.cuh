@@ -143,6 +143,14 @@ __device__ __forceinline__ u64 ssn_rand_range(u64 seed, u64 stream, u64 i, u32 j
     return ssn_bounded(((u64)r.x << 32) | r.y, r.z, range);
 }
 
+// Process-wide count of kernels this library launched (ssn_kernel_launches()); one shared
+// instance across translation units (inline function, static local).
+inline unsigned long long &ssn_launch_counter() {
+    static unsigned long long c = 0;
+    return c;
+}
+#define SSN_COUNT_LAUNCH() (++ssn_launch_counter())
+
 // Two uniform field elements (coefficients 2*jp and 2*jp+1) from one Philox call when p is
 // within 2^-24 of a power of two (masked 64-bit words; the default prime is 2^-39 close);
 // otherwise the bounded 96-bit method, one call each.

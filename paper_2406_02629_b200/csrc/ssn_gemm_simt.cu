@@ -133,6 +133,7 @@ extern "C" int ssn_conv_simt(const u64 *w, u64 w_pstride, const u64 *x, u64 x_ps
     dim3 grid((unsigned)((N + TN - 1) / TN), (unsigned)((O + TM - 1) / TM), (unsigned)nparty);
     SsnField f = ssn_make_field(p);
     u64 r64 = (u64)((((unsigned __int128)1) << 64) % p);
+    SSN_COUNT_LAUNCH();
     k_gemm_simt<true><<<grid, 256, 0, (cudaStream_t)strm>>>(w, w_pstride, x, x_pstride, out, out_pstride, O, K, N,
                                                             ohw, g, f, r64, fold_period(p));
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
@@ -146,6 +147,7 @@ extern "C" int ssn_dense_simt(const u64 *w, u64 w_pstride, const u64 *x, u64 x_p
     dim3 grid((unsigned)((nimg + TN - 1) / TN), (unsigned)((O + TM - 1) / TM), (unsigned)nparty);
     SsnField f = ssn_make_field(p);
     u64 r64 = (u64)((((unsigned __int128)1) << 64) % p);
+    SSN_COUNT_LAUNCH();
     k_gemm_simt<false><<<grid, 256, 0, (cudaStream_t)strm>>>(w, w_pstride, x, x_pstride, out, out_pstride, O, K,
                                                              (u64)nimg, 1, g, f, r64, fold_period(p));
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;

@@ -688,6 +688,7 @@ int launch_tc(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int 
     SsnField f = ssn_make_field(p);
     u64 r64 = (u64)((((unsigned __int128)1) << 64) % p);
     dim3 grid((O + BN - 1) / BN, (M + BM - 1) / BM, nparty);
+    SSN_COUNT_LAUNCH();
     k_gemm_tc<L><<<grid, 128, smem, st>>>(ma, mb, out, out_pstride, ohw, O, M, (Kpad + BK - 1) / BK, f, r64, cd);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
@@ -722,6 +723,7 @@ int launch_p45(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
     const int grid = (int)(ntiles < nsm ? ntiles : nsm);
+    SSN_COUNT_LAUNCH();
     if (variant)
         wide::k_gemm_p45w<0><<<grid, wide::THREADS_W, wide::SMEM_W, st>>>(
             ma, mb, out, out_pstride, (uint32_t)ohw, O, M, (Kpad + BK - 1) / BK, ntm, ntn, (int)ntiles, wide::ConvGeom{});
@@ -799,6 +801,7 @@ int launch_cn(const uint8_t *a, int mode, int nimg, int C, int H, int W, int Wp,
     if (ntiles >= (1ll << 31)) return SSN_ERR_UNSUPPORTED;
     const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
     const uint32_t ohw = (uint32_t)(H * W);
+    SSN_COUNT_LAUNCH();
     if (mode == 1)
         wide::k_gemm_p45w<1><<<grid, wide::THREADS_W, wide::SMEM_W, st>>>(ma, mb, out, out_pstride, ohw, O, M, taps * geo.cblocks,
                                                                        ntm, ntn, (int)ntiles, geo);
@@ -965,6 +968,7 @@ extern "C" int ssn_planes_shift(uint8_t *planes, uint64_t rows, int Wp, void *st
     const u64 total = rows * (Wp / 16);
     u64 blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
+    SSN_COUNT_LAUNCH();
     k_planes_shift<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(planes, rows, Wp);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
@@ -976,6 +980,7 @@ extern "C" int ssn_planes_cn(const u64 *x, int nparty, int nimg, int C, int H, i
     const u64 total = (u64)nparty * nimg * C * H * W;
     u64 blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
+    SSN_COUNT_LAUNCH();
     k_planes_cn<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, nimg, C, H, W, Wp, L, planes, x_pstride, total,
                                                                      copies, nparty);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
@@ -988,6 +993,7 @@ extern "C" int ssn_limb_split(const u64 *x, u64 rows, u64 K, u64 Kpad, int L, ui
     if (total == 0) return 0;
     u64 blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
+    SSN_COUNT_LAUNCH();
     k_limb_split<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, rows, K, Kpad, L, planes, x_pstride, total);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
@@ -1001,6 +1007,7 @@ extern "C" int ssn_im2col_limbs(const u64 *x, int nparty, int nimg, int C, int H
     const u64 rows = (u64)nimg * OH * OW;
     if (rows >= (1ull << 32)) return SSN_ERR_UNSUPPORTED;
     dim3 grid((unsigned)((Kpad + IC_K - 1) / IC_K), (unsigned)((rows + IC_ROWS - 1) / IC_ROWS), (unsigned)nparty);
+    SSN_COUNT_LAUNCH();
     k_im2col_limbs<<<grid, IC_THREADS, 0, (cudaStream_t)stream>>>(x, C, H, W, kh, kw, stride, pad, OH, OW, L,
                                                                   (uint32_t)rows, K, (int)Kpad, planes, x_pstride);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
