@@ -390,7 +390,7 @@ constexpr int WPT = 8;
 // output) and this kernel only runs the masked nonlinearity, reading each party's share.
 // Two kernels of half the code each run faster than one that overflows the instruction cache.
 template <int K, int N, bool SPLIT>
-__global__ void __launch_bounds__(CHAIN_THREADS, 4) k_chain_nonlin(ChainArgs a, const __grid_constant__ STables<K, N> tb,
+__global__ void __launch_bounds__(CHAIN_THREADS, 6) k_chain_nonlin(ChainArgs a, const __grid_constant__ STables<K, N> tb,
                                                                 SsnField f) {
     constexpr int M = 2 * K - 1;
     unsigned long long bad = 0;

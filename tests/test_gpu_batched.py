@@ -44,6 +44,29 @@ def test_reference_model_batched_matches_plaintext(ssn):
                 assert np.array_equal(eng.run(xb), want)
 
 
+@pytest.mark.parametrize("verify", [False, True])
+def test_lnt_ordering_batched_matches_plaintext(ssn, verify):
+    """ordering="lnt" (nonlinear before truncation, S/layers.py:164-184) through the batched
+    engine, fused and unfused: decoded outputs equal the integer plaintext of that schedule."""
+    from paper_2406_02629_b200.batched import BatchedEngine
+    model, _ = ssn.build_reference_model(7, pool="max")
+    weights = {name: qt.values for name, qt in model.weights.items()}
+    F = ssn.PrimeField()
+    for k, n in ((2, 3), (3, 5)):
+        scheme = ssn.SssScheme(F, k, n)
+        B = 6
+        xb = np.stack([ssn.random_input(7, model, index=i)[0] for i in range(B)])
+        for fuse in (False, True):
+            eng = BatchedEngine(model, scheme, batch=B, seed=5, fuse=fuse, ordering="lnt", verify=verify)
+            ops = [op.meta() for op in eng.ops]
+            assert [o["kind"] for o in ops] != [o.kind for o in BatchedEngine(
+                model, scheme, batch=B, seed=5, fuse=False).ops]          # the schedule did change
+            want, _ = _plain_batch(ops, xb, weights)
+            assert np.array_equal(eng.run(xb), want)
+            if verify:
+                assert int(eng.fail.item()) == 0
+
+
 def test_avg_pool_chain_model(ssn):
     from paper_2406_02629_b200.batched import BatchedEngine
     model, _ = ssn.build_reference_model(7, pool="avg")
