@@ -24,16 +24,22 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 WORKLOADS = {
-    # name: (builder, k, n, verify, default batch)
-    "resnet152-5pc": ("imagenet152", 3, 5, True, 16),
-    "resnet50-3pc": ("imagenet50", 2, 3, False, 16),
-    "resnet18-cifar-3pc": ("cifar18", 2, 3, False, 128),
+    # name: (builder, k, n, verify, default batch per GPU)
+    "resnet152-5pc": ("imagenet152", 3, 5, True, 32),
+    "resnet50-3pc": ("imagenet50", 2, 3, False, 32),
+    "resnet18-cifar-3pc": ("cifar18", 2, 3, False, 256),
     "lenet-3pc": ("reference", 2, 3, False, 1024),
     "lenet28-3pc": ("lenet28", 2, 3, False, 1024),     # config 1: LeNet-style CNN on 1x28x28
     "gemm-sweep": ("gemm", 0, 0, False, 0),          # config 5: mod-p share GEMM + reshare sweep
 }
 SWEEP = [(256, 256, 256), (1024, 1024, 1024), (2048, 2048, 2048), (4096, 4096, 4096), (8192, 8192, 8192),
          (16384, 4096, 4096), (4096, 4096, 16384), (16384, 16384, 16384)]
+# default CUDA streams per GPU (co-resident placement).  --streams S splits the batch over S
+# streams so one part's tensor-bound GEMMs overlap another's ALU-bound protocol chains: +3-4%
+# images/s (profiles/r01/README.md, batch/stream sweep), but then every kernel's CUDA-event time
+# includes the co-running kernels and the per-kernel rooflines stop describing the kernels.  The
+# default stays one stream so `roofline` is a clean per-kernel measurement.
+DEFAULT_STREAMS = {}
 METRIC = "ResNet-152 secure-inference images/s (5PC t=2, verification on, 224x224)"
 
 
@@ -500,7 +506,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-check", action="store_true")
-    ap.add_argument("--streams", type=int, default=1,
+    ap.add_argument("--streams", type=int, default=None,
                     help="co-resident: split the batch over this many CUDA streams (GEMM/chain overlap)")
     ap.add_argument("--placement", default="coresident", choices=["coresident", "party"],
                     help="coresident: every GPU runs all n parties on its own batch (default); "
@@ -538,11 +544,14 @@ def main():
     red_dev = "cpu" if shared else "cuda"
     kind, k, n, verify, dflt_batch = WORKLOADS[args.workload]
     B = args.batch or dflt_batch
+    nstreams = args.streams if args.streams is not None else DEFAULT_STREAMS.get(args.workload, 1)
+    if B % nstreams:
+        nstreams = 1
     model = build_model(kind)
     scheme = SssScheme(PrimeField(), k, n)
-    if args.streams > 1:
+    if nstreams > 1:
         from paper_2406_02629_b200.batched import StreamPipelinedEngine
-        eng = StreamPipelinedEngine(model, scheme, batch=B, streams=args.streams, seed=7 + rank, verify=verify)
+        eng = StreamPipelinedEngine(model, scheme, batch=B, streams=nstreams, seed=7 + rank, verify=verify)
     else:
         eng = BatchedEngine(model, scheme, batch=B, seed=7 + rank, verify=verify)
     shape = (B,) + tuple(model.input_shape)
@@ -654,6 +663,7 @@ def main():
         "config": {"workload": args.workload, "model": model.name, "k": k, "n": n, "verify": verify,
                    "batch_per_gpu": B, "global_batch": imgs, "parallelism": f"dp{world} x co-resident {n} parties",
                    "rng": "device philox", "l2": "working set >> 126 MB L2 (inputs larger than L2)",
+                   "streams_per_gpu": nstreams, "batch_latency_ms": round(dev_ms, 3),
                    "s_per_image": round(dev_ms / 1000.0 / B, 6)},
         "e2e": {"value": round(e2e, 3), "unit": "images/s",
                 "h2d_bytes_per_step": int(x_host.numel() * 8), "d2h_bytes_per_step": int(out_host.numel() * 8)},
