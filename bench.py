@@ -206,9 +206,10 @@ def load_traffic():
         return {}
 
 
-# executed thread instructions per chain element, by (k, n) (ncu smsp__inst_executed x 32 /
-# elements over a ResNet-152 5PC step, profiles/r01/README.md); other schemes: not calibrated
-CHAIN_ALU = {(3, 5): 3316}
+# executed thread instructions per chain element, by (k, n): ncu smsp__thread_inst_executed over
+# the chain kernels of one step / the step's chain elements (tools/chain_alu.py, the ncu lists in
+# profiles/r01/alu/: ResNet-152 5PC and ResNet-50 3PC); other schemes: not calibrated
+CHAIN_ALU = {(3, 5): 3328, (2, 3): 1573}
 
 
 def roofline(kstats, eng, dev_ms, bf16, hbm, src):
@@ -242,7 +243,7 @@ def roofline(kstats, eng, dev_ms, bf16, hbm, src):
                 # element (ncu, profiles/r01/README.md) x elements / time vs the SM issue peak
                 rate = alu * st["elems_per_launch"] / sec
                 peak_i = 148 * 128 * 1.965e9
-                r["alu_issue"] = {"thread_instr_per_elem": alu, "calibration": "ResNet-152 5PC ncu count",
+                r["alu_issue"] = {"thread_instr_per_elem": alu, "calibration": "ncu count, tools/chain_alu.py",
                                   "achieved_tinstr_per_s": float(f"{rate:.4g}"),
                                   "peak_tinstr_per_s": float(f"{peak_i:.4g}"), "frac": round(rate / peak_i, 4)}
         t = traffic.get(cls)

@@ -1,0 +1,35 @@
+"""Calibrate bench.py's CHAIN_ALU: executed thread instructions per chain element for one
+workload.  Run one warm step under ncu first:
+  ncu --metrics smsp__thread_inst_executed.sum --profile-from-start off -k regex:k_chain \
+      --csv --log-file chain.csv python tools/profile_step.py WORKLOAD BATCH
+then: python tools/chain_alu.py WORKLOAD BATCH chain.csv  (needs the GPU for the element count)."""
+import csv
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2406_02629_b200.batched import BatchedEngine  # noqa: E402
+from paper_2406_02629_b200.field import PrimeField  # noqa: E402
+from paper_2406_02629_b200.sss import SssScheme  # noqa: E402
+
+wl, B, path = sys.argv[1], int(sys.argv[2]), sys.argv[3]
+kind, k, n, verify, _ = bench.WORKLOADS[wl]
+model = bench.build_model(kind)
+eng = BatchedEngine(model, SssScheme(PrimeField(), k, n), batch=B, seed=7, verify=verify)
+x = torch.as_tensor(model.random_inputs(seed=1, batch=B), device="cuda")
+eng.run_device(x)
+eng.enable_profiling()
+eng.run_device(x)
+stats = eng.profile_summary(1)
+eng.disable_profiling()
+elems = stats["chain"]["elems_per_launch"] * stats["chain"]["launches_per_step"]
+rows = list(csv.reader(open(path)))
+h = next(i for i, r in enumerate(rows) if "Metric Value" in r)
+vi, ni = rows[h].index("Metric Value"), rows[h].index("Metric Name")
+inst = sum(float(r[vi].replace(",", "")) for r in rows[h + 1:]
+           if len(r) > vi and r[ni] == "smsp__thread_inst_executed.sum")
+print(f"{wl} B={B} (k,n)=({k},{n}): {inst:.4g} thread instructions / {elems:.4g} chain elements = "
+      f"{inst / elems:.0f} per element")
