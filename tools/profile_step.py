@@ -1,5 +1,5 @@
 """Run one warm step of the batched engine inside a cudaProfilerStart/Stop range (for ncu
---profile-from-start off).  Usage: python tools/profile_step.py [workload] [batch]"""
+--profile-from-start off).  Usage: python tools/profile_step.py [workload] [batch (default: bench.py's)]"""
 import os
 import sys
 
@@ -12,8 +12,8 @@ from paper_2406_02629_b200.field import PrimeField  # noqa: E402
 from paper_2406_02629_b200.sss import SssScheme  # noqa: E402
 
 wl = sys.argv[1] if len(sys.argv) > 1 else "resnet152-5pc"
-B = int(sys.argv[2]) if len(sys.argv) > 2 else 16
-kind, k, n, verify, _ = bench.WORKLOADS[wl]
+kind, k, n, verify, dflt = bench.WORKLOADS[wl]
+B = int(sys.argv[2]) if len(sys.argv) > 2 else dflt
 model = bench.build_model(kind)
 eng = BatchedEngine(model, SssScheme(PrimeField(), k, n), batch=B, seed=7, verify=verify)
 x = torch.as_tensor(model.random_inputs(seed=1, batch=B), device="cuda")
