@@ -318,8 +318,8 @@ def run_reference(args):
 
 def run_gemm_sweep(args):
     """Config 5: one party's mod-p share GEMM C = A.B^T over uniform field elements (u8 limb
-    planes, tcgen05) for M,N,K in SWEEP, plus the co-resident (3,5) reshare chain on the GEMM
-    output.  Every rank runs the sweep on its own GPU (weak scaling, no collective); value =
+    planes, tcgen05) for M,N,K in SWEEP, plus the reshare microbenchmark (reshare_microbench:
+    co-resident R^T apply against HBM, and at >= 2 GPUs one all-pairs NCCL hop against NVLink).  Every rank runs the sweep on its own GPU (weak scaling, no collective); value =
     summed field Gop/s of the largest shape.  Exactness: a 256^3 slice against the CUDA-core
     reference GEMM (ssn_dense_simt)."""
     import torch
@@ -387,6 +387,7 @@ def run_gemm_sweep(args):
         del A, Bp, out
     top = rows[-1]
     value = top["field_gops"]
+    reshare = reshare_microbench(args, torch, dist, _lib, p, hbm, world, rank)
     if world > 1:
         t = torch.tensor([value], dtype=torch.float64, device="cuda")
         dist.all_reduce(t)
@@ -401,10 +402,113 @@ def run_gemm_sweep(args):
                 "roofline": {"bound": "tensor", "achieved": top["int8_tops"], "peak": round(peak, 1),
                              "unit": "TFLOP/s", "frac": top["frac_int8"], "traffic": None,
                              "note": f"peak = 2 x {src} dense bf16"},
-                "gpu_launches": int(launches), "exact_vs_cuda_core_gemm": exact, "sweep": rows}
+                "gpu_launches": int(launches), "exact_vs_cuda_core_gemm": exact, "sweep": rows,
+                "reshare": reshare}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+NVLINK_GBPS = 900.0          # NVLink 5 per direction per GPU (B200_PROFILING.md / datasheet)
+
+
+def reshare_microbench(args, torch, dist, _lib, p, hbm, world, rank):
+    """Config 5's reshare half.  (a) Co-resident: step 2 of reshare_degree_reduce
+    (S/protocol.py:165-185) on a 4096^2 GEMM output of the (3,5) scheme -- each of the k front
+    ranks applies R^T to the m = 5 participants' sub-shares (ssn_reduce_apply), algorithmic bytes
+    8*(m + n) per element per front rank, against HBM.  (b) Party-per-GPU (world >= 2): one
+    reshare hop's traffic, every rank sending a 4096^2-element share buffer to every other rank
+    at once (NCCL send/recv in one group), max-over-ranks time, per-rank egress against NVLink."""
+    from paper_2406_02629_b200.field import PrimeField
+    from paper_2406_02629_b200.sss import SssScheme
+    k, n = 3, 5
+    m = 2 * k - 1
+    sch = SssScheme(PrimeField(), k, n)
+    R = sch.reducing_matrix()
+    rt = _lib.u64_array([R[j][t] for t in range(n) for j in range(m)])
+    E = 4096 * 4096
+    sub = torch.empty((k, m, E), dtype=torch.int64, device="cuda")
+    _lib.call("ssn_rand", _lib.ptr(sub), sub.numel(), 0, p, 99 + rank, 7, _lib.stream_ptr())
+    back = torch.empty((k, n, E), dtype=torch.int64, device="cuda")
+
+    def apply():
+        _lib.call("ssn_reduce_apply", _lib.ptr(sub), m * E, E, m, rt, n, _lib.ptr(back), n * E, E, E, k, p,
+                  _lib.stream_ptr())
+    for _ in range(max(1, args.warmup)):
+        apply()
+    reps = max(1, args.steps)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        apply()
+    e1.record()
+    torch.cuda.synchronize()
+    sec = e0.elapsed_time(e1) / reps / 1e3
+    gbs = 8.0 * (m + n) * E * k / sec / 1e9
+    out = {"coresident_reduce_apply": {"scheme": [k, n], "elements": E, "front_ranks": k,
+                                       "ms": round(sec * 1e3, 3), "achieved_GBps": round(gbs, 1),
+                                       "peak_GBps": round(hbm, 1), "frac_hbm": round(gbs / hbm, 4),
+                                       "bytes_per_elem_per_front": 8 * (m + n)}}
+
+    def timed(fn, nbytes):
+        for _ in range(max(1, args.warmup)):
+            fn()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize()
+        t_s = e0.elapsed_time(e1) / reps / 1e3
+        return {"ms": round(t_s * 1e3, 3), "achieved_GBps": round(nbytes / t_s / 1e9, 1),
+                "frac_hbm": round(nbytes / t_s / 1e9 / hbm, 4)}
+    # step 1 / SHARE_DIST: gen of n shares from a secret, Philox coefficients in registers
+    ids = _lib.u64_array(list(sch.party_ids))
+    sec_in = sub[0, 0]
+    gen_out = back[0]
+    out["gen"] = dict(timed(lambda: _lib.call("ssn_gen", _lib.ptr(sec_in), E, None, 0, 5, 11, k - 1, ids, n,
+                                              _lib.ptr(gen_out), n * E, E, E, 1, p, _lib.stream_ptr()),
+                            8.0 * (1 + n) * E), bytes_per_elem=8 * (1 + n), ids=n)
+    # step 3 / elite reconstruction: rec over the k front ranks
+    wf = _lib.u64_array(list(sch.lagrange_weights(sch.front_ids)))
+    rec_out = back[1, 0]
+    out["rec"] = dict(timed(lambda: _lib.call("ssn_rec", _lib.ptr(sub[0]), 0, E, wf, k, _lib.ptr(rec_out), 0, E, 1, p,
+                                              _lib.stream_ptr()), 8.0 * (k + 1) * E), bytes_per_elem=8 * (k + 1))
+    del sub, back
+    if world < 2:
+        out["exchange"] = {"unavailable": "party-per-GPU exchange needs >= 2 GPUs"}
+        return out
+    Ex = 4096 * 4096
+    send = [torch.empty(Ex, dtype=torch.int64, device="cuda") for _ in range(world)]
+    recv = [torch.empty(Ex, dtype=torch.int64, device="cuda") for _ in range(world)]
+
+    def hop():
+        ops = []
+        for peer in range(world):
+            if peer != rank:
+                ops.append(dist.P2POp(dist.isend, send[peer], peer))
+                ops.append(dist.P2POp(dist.irecv, recv[peer], peer))
+        for w in dist.batch_isend_irecv(ops):
+            w.wait()
+    dist.barrier()
+    for _ in range(max(1, args.warmup)):
+        hop()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record()
+    for _ in range(reps):
+        hop()
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / reps], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    sec = float(t.item()) / 1e3
+    egress = 8.0 * Ex * (world - 1) / sec / 1e9
+    out["exchange"] = {"ranks": world, "elements_per_peer": Ex, "ms": round(sec * 1e3, 3),
+                       "egress_GBps_per_rank": round(egress, 1), "peak_GBps": NVLINK_GBPS,
+                       "frac_nvlink": round(egress / NVLINK_GBPS, 4)}
+    return out
 
 
 def run_party_placement(args):

@@ -17,6 +17,7 @@
 #include "ssn_field.cuh"
 #include "ssn.h"
 #include "ssn_lincomb.cuh"
+#include "ssn_p45.cuh"
 
 static int ssn_blocks(u64 n, int threads = 256) {
     u64 b = (n + threads - 1) / threads;
@@ -79,6 +80,101 @@ extern "C" int ssn_ewise(int op, const u64 *a, const u64 *b, u64 *out, u64 n, u6
     return ssn_check_launch();
 }
 
+// ------------------------------------------------------------------ p = 2^45 - 55 fast paths
+// rec / R-apply / reshare step 3 with compile-time row lengths and the chain kernels' arithmetic
+// (ssn_p45.cuh): non-negative small-rational rows, ONE pseudo-Mersenne fold per row, no sign
+// branches.  Same canonical outputs as the generic kernels; taken when every row is small.
+template <int M, int NO>
+struct P45Rows {
+    ssn45::SRow<M> r[NO];
+};
+
+template <int M>
+__global__ void k_rec_p45(const u64 *__restrict__ pts, u64 p_b, u64 p_j, P45Rows<M, 1> w, u64 *__restrict__ out,
+                          u64 o_b, u64 n) {
+    const u64 b = blockIdx.y;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u64 *base = pts + b * p_b + i;
+        u64 x[M];
+#pragma unroll
+        for (int j = 0; j < M; j++) x[j] = base[j * p_j];
+        out[b * o_b + i] = ssn45::canon(ssn45::lin<M>(x, w.r[0]));
+    }
+}
+
+template <int M, int NO>
+__global__ void k_reduce_apply_p45(const u64 *__restrict__ pts, u64 p_b, u64 p_j, P45Rows<M, NO> R,
+                                   u64 *__restrict__ out, u64 o_b, u64 o_t, u64 n) {
+    const u64 b = blockIdx.y;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u64 *base = pts + b * p_b + i;
+        u64 v[M];
+#pragma unroll
+        for (int j = 0; j < M; j++) v[j] = base[j * p_j];
+        const u64 vs = ssn45::xsum_of<M>(v);
+#pragma unroll
+        for (int t = 0; t < NO; t++) out[b * o_b + t * o_t + i] = ssn45::canon(ssn45::lin_s<M>(v, vs, R.r[t]));
+    }
+}
+
+template <int K>
+__global__ void k_reshare_finish_p45(const u64 *__restrict__ pts, u64 p_b, u64 p_j, P45Rows<K, 1> w,
+                                     const u64 *__restrict__ zero, u64 z_b, const u64 *__restrict__ bias, u64 bi_b,
+                                     u64 bias_div, u64 bias_mod, const u64 *__restrict__ alpha, u64 a_b,
+                                     u64 *__restrict__ out, u64 o_b, u64 n) {
+    const u64 b = blockIdx.y;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u64 *base = pts + b * p_b + i;
+        u64 x[K];
+#pragma unroll
+        for (int j = 0; j < K; j++) x[j] = base[j * p_j];
+        u64 acc = ssn45::lin<K>(x, w.r[0]);                      // lazy, < 2^46
+        if (zero) acc += zero[b * z_b + i];
+        if (bias) {
+            const u64 ch = n < (1ull << 32) ? (u64)(((uint32_t)i / (uint32_t)bias_div) % (uint32_t)bias_mod)
+                                            : (i / bias_div) % bias_mod;
+            acc += bias[b * bi_b + ch];
+        }
+        if (alpha) acc += alpha[b * a_b + i];
+        out[b * o_b + i] = ssn45::canon(acc);                      // < 2^46 + 3 * 2^45
+    }
+}
+
+// gen with compile-time (k-1, |ids|): the same coefficients as k_gen (host-fed, or the same
+// Philox draws), shares s + sum_j c_j id^(j+1) with small id powers, one fold each
+template <int KM1, int NIDS>
+struct P45Pows {
+    uint32_t pw[NIDS][KM1 > 0 ? KM1 : 1];
+};
+
+template <int KM1, int NIDS>
+__global__ void k_gen_p45(const u64 *__restrict__ secret, u64 s_b, const u64 *__restrict__ coeffs, u64 c_b, u64 seed,
+                          u64 stream, P45Pows<KM1, NIDS> pw, u64 *__restrict__ out, u64 o_b, u64 o_t, u64 n,
+                          SsnField f) {
+    const u64 b = blockIdx.y;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        const u64 s = secret ? secret[b * s_b + i] : 0;
+        u64 c[SSN_MAXK];
+        load_coeffs(c, coeffs ? coeffs + b * c_b : nullptr, n, i, KM1, seed, stream + b, f);
+#pragma unroll
+        for (int t = 0; t < NIDS; t++) {
+            u64 acc = s;                                           // < p + 2^45 * sum id^j < 2^64
+#pragma unroll
+            for (int j = 0; j < KM1; j++) acc += mul_small(c[j], pw.pw[t][j]);
+            out[b * o_b + t * o_t + i] = ssn45::canon(acc);
+        }
+    }
+}
+
+// rows[t*m + j] -> small-rational p45 rows; 0 if any row has no small form
+template <int M, int NO>
+static int p45_rows(P45Rows<M, NO> &R, const u64 *rows, u64 p) {
+    if (p != ssn45::PP) return 0;
+    for (int t = 0; t < NO; t++)
+        if (!ssn45::make_srow<M>(R.r[t], rows + (u64)t * M, M, p)) return 0;
+    return 1;
+}
+
 // ------------------------------------------------------------------ gen
 // out[b][t][i] = secret[b][i] + sum_j c_j[b][i] * ids[t]^(j+1)
 __global__ void k_gen(const u64 *__restrict__ secret, u64 s_b, const u64 *__restrict__ coeffs, u64 c_b, u64 seed,
@@ -101,6 +197,22 @@ extern "C" int ssn_gen(const u64 *secret, u64 secret_bstride, const u64 *coeffs,
     if (km1 < 0 || km1 > SSN_MAXK || nids < 1 || nids > SSN_MAXJ || nbatch < 1) return SSN_ERR_ARG;
     if (n == 0) return 0;
     PowTable pw = make_pows(ids, nids, km1, p);
+#define SSN_GEN_P45(KK, NN)                                                                               \
+    if (km1 == KK && nids == NN && pw.small && p == ssn45::PP) {                                          \
+        P45Pows<KK, NN> q;                                                                                \
+        for (int t = 0; t < NN; t++)                                                                      \
+            for (int j = 0; j < KK; j++) q.pw[t][j] = (uint32_t)pw.r[t].n[j];                             \
+        SSN_COUNT_LAUNCH();                                                                               \
+        k_gen_p45<KK, NN><<<ssn_grid2(n, nbatch), 256, 0, (cudaStream_t)strm>>>(                           \
+            secret, secret_bstride, coeffs, coeff_bstride, seed, stream, q, out, out_bstride, out_tstride, n, \
+            ssn_make_field(p));                                                                           \
+        return ssn_check_launch();                                                                        \
+    }
+    SSN_GEN_P45(1, 2)
+    SSN_GEN_P45(1, 3)
+    SSN_GEN_P45(2, 3)
+    SSN_GEN_P45(2, 5)
+#undef SSN_GEN_P45
     SSN_COUNT_LAUNCH();
     k_gen<<<ssn_grid2(n, nbatch), 256, 0, (cudaStream_t)strm>>>(secret, secret_bstride, coeffs, coeff_bstride,
                                                                   seed, stream, km1, pw, nids, out, out_bstride,
@@ -126,6 +238,20 @@ extern "C" int ssn_rec(const u64 *pts, u64 pts_bstride, u64 pts_jstride, const u
                        u64 out_bstride, u64 n, int nbatch, u64 p, void *strm) {
     if (m < 1 || m > SSN_MAXJ || nbatch < 1) return SSN_ERR_ARG;
     if (n == 0) return 0;
+#define SSN_REC_P45(MM)                                                                                   \
+    if (m == MM) {                                                                                        \
+        P45Rows<MM, 1> R;                                                                                 \
+        if (p45_rows<MM, 1>(R, w, p)) {                                                                   \
+            SSN_COUNT_LAUNCH();                                                                           \
+            k_rec_p45<MM><<<ssn_grid2(n, nbatch), 256, 0, (cudaStream_t)strm>>>(pts, pts_bstride, pts_jstride, \
+                                                                              R, out, out_bstride, n);      \
+            return ssn_check_launch();                                                                    \
+        }                                                                                                 \
+    }
+    SSN_REC_P45(2)
+    SSN_REC_P45(3)
+    SSN_REC_P45(5)
+#undef SSN_REC_P45
     Weights W = make_weights(w, m, p);
     SSN_COUNT_LAUNCH();
     k_rec<<<ssn_grid2(n, nbatch), 256, 0, (cudaStream_t)strm>>>(pts, pts_bstride, pts_jstride, W, m, out,
@@ -154,6 +280,21 @@ extern "C" int ssn_reduce_apply(const u64 *pts, u64 pts_bstride, u64 pts_jstride
                                 u64 *out, u64 out_bstride, u64 out_tstride, u64 n, int nbatch, u64 p, void *strm) {
     if (m < 1 || m > SSN_MAXP || nout < 1 || nout > SSN_MAXJ || nbatch < 1) return SSN_ERR_ARG;
     if (n == 0) return 0;
+#define SSN_RA_P45(MM, NN)                                                                                \
+    if (m == MM && nout == NN) {                                                                          \
+        P45Rows<MM, NN> Q;                                                                                \
+        if (p45_rows<MM, NN>(Q, rt, p)) {                                                                 \
+            SSN_COUNT_LAUNCH();                                                                           \
+            k_reduce_apply_p45<MM, NN><<<ssn_grid2(n, nbatch), 256, 0, (cudaStream_t)strm>>>(              \
+                pts, pts_bstride, pts_jstride, Q, out, out_bstride, out_tstride, n);                       \
+            return ssn_check_launch();                                                                    \
+        }                                                                                                 \
+    }
+    SSN_RA_P45(3, 2)
+    SSN_RA_P45(3, 3)
+    SSN_RA_P45(5, 3)
+    SSN_RA_P45(5, 5)
+#undef SSN_RA_P45
     RTable R;
     R.small = 1;
     for (int t = 0; t < SSN_MAXJ; t++) {
@@ -200,6 +341,20 @@ extern "C" int ssn_reshare_finish(const u64 *pts, u64 pts_bstride, u64 pts_jstri
                                   u64 out_bstride, u64 n, int nbatch, u64 p, void *strm) {
     if (k < 1 || k > SSN_MAXP || nbatch < 1 || bias_div == 0 || bias_mod == 0) return SSN_ERR_ARG;
     if (n == 0) return 0;
+#define SSN_RF_P45(KK)                                                                                    \
+    if (k == KK) {                                                                                        \
+        P45Rows<KK, 1> Q;                                                                                 \
+        if (p45_rows<KK, 1>(Q, w, p)) {                                                                   \
+            SSN_COUNT_LAUNCH();                                                                           \
+            k_reshare_finish_p45<KK><<<ssn_grid2(n, nbatch), 256, 0, (cudaStream_t)strm>>>(                \
+                pts, pts_bstride, pts_jstride, Q, zero, zero_bstride, bias, bias_bstride, bias_div, bias_mod, \
+                alpha, alpha_bstride, out, out_bstride, n);                                               \
+            return ssn_check_launch();                                                                    \
+        }                                                                                                 \
+    }
+    SSN_RF_P45(2)
+    SSN_RF_P45(3)
+#undef SSN_RF_P45
     Weights W = make_weights(w, k, p);
     SSN_COUNT_LAUNCH();
     k_reshare_finish<<<ssn_grid2(n, nbatch), 256, 0, (cudaStream_t)strm>>>(
