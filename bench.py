@@ -475,6 +475,23 @@ def reshare_microbench(args, torch, dist, _lib, p, hbm, world, rank):
     rec_out = back[1, 0]
     out["rec"] = dict(timed(lambda: _lib.call("ssn_rec", _lib.ptr(sub[0]), 0, E, wf, k, _lib.ptr(rec_out), 0, E, 1, p,
                                               _lib.stream_ptr()), 8.0 * (k + 1) * E), bytes_per_elem=8 * (k + 1))
+    # truncation elite (S/layers.py:295-315): rec over the fronts, RS check of the n-k extra masked
+    # shares, window decode / floor / round, fresh (k, n) shares
+    from paper_2406_02629_b200.protocol import extrapolation_coeffs
+    ext = _lib.u64_array([v for row in extrapolation_coeffs(sch, sch.front_ids, sch.party_ids[k:]) for v in row])
+    fail = torch.zeros(1, dtype=torch.int64, device="cuda")
+    masked = back[0]
+    tr_out = sub[1]
+    out["trunc_elite"] = dict(timed(lambda: _lib.call(
+        "ssn_trunc_elite", _lib.ptr(masked), E, n, k, wf, ext, 1 << 40, 1 << 12, 1, None, 5, 13, k - 1, ids, n,
+        _lib.ptr(tr_out), E, _lib.ptr(fail), E, p, _lib.stream_ptr()), 8.0 * (n + n) * E),
+        bytes_per_elem=8 * (n + n), rs_checks=n - k)
+    # nonlinear elite (S/layers.py:345-364): rec over the 2k-1 participants, decode, ReLU, encode
+    wp = _lib.u64_array(list(sch.lagrange_weights(sch.participating_ids)))
+    plain = sub[2, 0]
+    out["nonlin_elite"] = dict(timed(lambda: _lib.call(
+        "ssn_nonlin_elite", _lib.ptr(back[1]), E, m, wp, 1, 0, 1, 1, 4096, 4096, 1, 1, _lib.ptr(plain), p,
+        _lib.stream_ptr()), 8.0 * (m + 1) * E), bytes_per_elem=8 * (m + 1))
     del sub, back
     if world < 2:
         out["exchange"] = {"unavailable": "party-per-GPU exchange needs >= 2 GPUs"}

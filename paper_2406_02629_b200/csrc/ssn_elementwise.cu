@@ -393,6 +393,43 @@ __global__ void k_trunc_elite(const u64 *__restrict__ pts, u64 p_j, int npts, in
     if (fail && bad_local) atomicAdd(fail, bad_local);
 }
 
+// p45 truncation elite: compile-time k, extra RS points NX and output ids NIDS (0: the truncated
+// value only); same coefficient draws and canonical outputs as k_trunc_elite
+template <int K, int NX, int NIDS>
+__global__ void k_trunc_elite_p45(const u64 *__restrict__ pts, u64 p_j, P45Rows<K, 1> w,
+                                  P45Rows<K, (NX > 0 ? NX : 1)> ext, i64 lo, u64 neglo_mod, i64 r, int rshift, i64 d,
+                                  const u64 *__restrict__ coeffs, u64 seed, u64 stream,
+                                  P45Pows<K - 1, (NIDS > 0 ? NIDS : 1)> pw, u64 *__restrict__ out, u64 o_t,
+                                  unsigned long long *__restrict__ fail, u64 n, SsnField f) {
+    unsigned long long bad_local = 0;
+    for (u64 i = blockIdx.x * (u64)blockDim.x + threadIdx.x; i < n; i += (u64)gridDim.x * blockDim.x) {
+        u64 s[K + NX];
+#pragma unroll
+        for (int j = 0; j < K + NX; j++) s[j] = pts[j * p_j + i];
+        u64 front[K];
+#pragma unroll
+        for (int j = 0; j < K; j++) front[j] = s[j];
+        const u64 v = ssn45::canon(ssn45::lin<K>(front, w.r[0]));
+#pragma unroll
+        for (int q = 0; q < NX; q++) bad_local += (ssn45::canon(ssn45::lin<K>(front, ext.r[q])) != s[K + q]);
+        const u64 tm = ssn_trunc_value(v, lo, neglo_mod, r, rshift, d, f);
+        if (NIDS == 0) {
+            out[i] = tm;
+            continue;
+        }
+        u64 c[SSN_MAXK];
+        load_coeffs(c, coeffs, n, i, K - 1, seed, stream, f);
+#pragma unroll
+        for (int t = 0; t < NIDS; t++) {
+            u64 acc = tm;
+#pragma unroll
+            for (int j = 0; j < K - 1; j++) acc += mul_small(c[j], pw.pw[t][j]);
+            out[t * o_t + i] = ssn45::canon(acc);
+        }
+    }
+    if (fail && bad_local) atomicAdd(fail, bad_local);
+}
+
 extern "C" int ssn_trunc_elite(const u64 *pts, u64 pts_jstride, int npts, int k, const u64 *w, const u64 *ext,
                                i64 value_bound, i64 r, i64 d, const u64 *coeffs, u64 seed, u64 stream, int km1,
                                const u64 *ids, int nids, u64 *out, u64 out_tstride, unsigned long long *fail, u64 n,
@@ -419,6 +456,32 @@ extern "C" int ssn_trunc_elite(const u64 *pts, u64 pts_jstride, int npts, int k,
         rshift = 0;
         while ((1ll << rshift) < r) rshift++;
     }
+#define SSN_TE_P45(KK, XX, NN)                                                                            \
+    if (k == KK && npts - k == XX && nids == NN && km1 == KK - 1 && p == ssn45::PP && pw.small) {          \
+        P45Rows<KK, 1> qw;                                                                                \
+        P45Rows<KK, (XX > 0 ? XX : 1)> qe;                                                                \
+        P45Pows<KK - 1, (NN > 0 ? NN : 1)> qp;                                                            \
+        int ok = p45_rows<KK, 1>(qw, w, p);                                                               \
+        for (int e = 0; e < XX && ok; e++) ok = ssn45::make_srow<KK>(qe.r[e], ext + (u64)e * KK, KK, p);  \
+        for (int t = 0; t < NN; t++)                                                                      \
+            for (int j = 0; j < KK - 1; j++) qp.pw[t][j] = (uint32_t)pw.r[t].n[j];                        \
+        if (ok) {                                                                                         \
+            SSN_COUNT_LAUNCH();                                                                           \
+            k_trunc_elite_p45<KK, XX, NN><<<ssn_blocks(n), 256, 0, (cudaStream_t)strm>>>(                  \
+                pts, pts_jstride, qw, qe, lo, neglo_mod, r, rshift, d, coeffs, seed, stream, qp, out,      \
+                out_tstride, fail, n, ssn_make_field(p));                                                 \
+            return ssn_check_launch();                                                                    \
+        }                                                                                                 \
+    }
+    SSN_TE_P45(2, 0, 0)
+    SSN_TE_P45(2, 0, 3)
+    SSN_TE_P45(2, 1, 0)
+    SSN_TE_P45(2, 1, 3)
+    SSN_TE_P45(3, 0, 0)
+    SSN_TE_P45(3, 0, 5)
+    SSN_TE_P45(3, 2, 0)
+    SSN_TE_P45(3, 2, 5)
+#undef SSN_TE_P45
     SSN_COUNT_LAUNCH();
     k_trunc_elite<<<ssn_blocks(n), 256, 0, (cudaStream_t)strm>>>(pts, pts_jstride, npts, k, W, E, lo, neglo_mod, r,
                                                                  rshift, d, coeffs, seed, stream, km1, pw, nids, out,
@@ -462,6 +525,38 @@ __global__ void k_nonlin_elite(const u64 *__restrict__ pts, u64 p_j, int m, Weig
     }
 }
 
+template <int M>
+__global__ void k_nonlin_elite_p45(const u64 *__restrict__ pts, u64 p_j, P45Rows<M, 1> w, int relu, int pool_kind,
+                                   int c, int h, int wd, int kh, int kw, u64 *__restrict__ plain, u64 n_out) {
+    const int oh = h / kh, ow = wd / kw;
+    for (u64 o = blockIdx.x * (u64)blockDim.x + threadIdx.x; o < n_out; o += (u64)gridDim.x * blockDim.x) {
+        u64 base_in;
+        if (pool_kind == 0) {
+            base_in = o;
+        } else {
+            const uint32_t o32 = (uint32_t)o, chw = (uint32_t)(c * oh * ow), hw = (uint32_t)(oh * ow);
+            const uint32_t img = o32 / chw, rem = o32 - img * chw;
+            const uint32_t ci = rem / hw, rr = rem - ci * hw;
+            const uint32_t y = rr / (uint32_t)ow, x = rr - y * (uint32_t)ow;
+            base_in = (((u64)img * c + ci) * (u64)h + (u64)(y * kh)) * wd + (u64)(x * kw);
+        }
+        i64 acc = pool_kind == 1 ? INT64_MIN : 0;
+        for (int a = 0; a < kh; a++)
+            for (int bq = 0; bq < kw; bq++) {
+                const u64 i = base_in + (u64)a * wd + bq;
+                u64 x[M];
+#pragma unroll
+                for (int j = 0; j < M; j++) x[j] = pts[j * p_j + i];
+                const u64 v = ssn45::canon(ssn45::lin<M>(x, w.r[0]));
+                i64 sv = v > ssn45::PHALF ? (i64)v - (i64)ssn45::PP : (i64)v;
+                if (relu && sv <= 0) sv = 0;
+                if (pool_kind == 1) acc = sv > acc ? sv : acc;
+                else acc += sv;
+            }
+        plain[o] = acc < 0 ? (u64)((i64)ssn45::PP + acc) : (u64)acc;
+    }
+}
+
 extern "C" int ssn_nonlin_elite(const u64 *pts, u64 pts_jstride, int m, const u64 *w, int relu, int pool_kind,
                                 int nb, int c, int h, int wd, int kh, int kw, u64 *plain, u64 p, void *strm) {
     if (m < 1 || m > SSN_MAXP || pool_kind < 0 || pool_kind > 2 || kh < 1 || kw < 1 || h % kh || wd % kw)
@@ -471,6 +566,19 @@ extern "C" int ssn_nonlin_elite(const u64 *pts, u64 pts_jstride, int m, const u6
     const u64 n_out = (u64)nb * c * (h / kh) * (wd / kw);
     if (n_out == 0) return 0;
     if (n_out >= (1ull << 32)) return SSN_ERR_UNSUPPORTED;
+#define SSN_NE_P45(MM)                                                                                    \
+    if (m == MM) {                                                                                        \
+        P45Rows<MM, 1> q;                                                                                 \
+        if (p45_rows<MM, 1>(q, w, p)) {                                                                   \
+            SSN_COUNT_LAUNCH();                                                                           \
+            k_nonlin_elite_p45<MM><<<ssn_blocks(n_out), 256, 0, (cudaStream_t)strm>>>(                     \
+                pts, pts_jstride, q, relu, pool_kind, c, h, wd, kh, kw, plain, n_out);                    \
+            return ssn_check_launch();                                                                    \
+        }                                                                                                 \
+    }
+    SSN_NE_P45(3)
+    SSN_NE_P45(5)
+#undef SSN_NE_P45
     SSN_COUNT_LAUNCH();
     k_nonlin_elite<<<ssn_blocks(n_out), 256, 0, (cudaStream_t)strm>>>(pts, pts_jstride, m, W, relu, pool_kind, c, h,
                                                                       wd, kh, kw, plain, n_out, ssn_make_field(p));
