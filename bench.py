@@ -773,7 +773,7 @@ def main():
     online, offline = eng.comm_per_image()
     roof, by_kernel = roofline(kstats, eng, dev_ms, bf16, hbm, src)
     cpu = None
-    if not args.no_cpu_baseline:
+    if not args.no_cpu_baseline and world == 1:          # the CPU baseline is an N=1 figure
         try:
             cpu = cpu_baseline_sample(model, k, n, verify, budget_s=args.cpu_budget)
         except Exception as exc:       # reported, never silently replaced
