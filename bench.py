@@ -695,6 +695,10 @@ def main():
             from paper_2406_02629_b200.model import plaintext_infer
             want = np.stack([plaintext_infer(model, xb[i]) for i in range(B)])
         outputs_match = bool(np.array_equal(got, want))
+        if world > 1:                       # every rank's batch must match, not just rank 0's
+            t = torch.tensor([float(outputs_match)], dtype=torch.float64, device=red_dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN)
+            outputs_match = bool(t.item() == 1.0)
 
     stream = torch.cuda.current_stream()
 
@@ -744,6 +748,10 @@ def main():
     for e in getattr(eng, "engines", [eng]):
         if e.verify:
             verify_failures += int(e.fail.item())
+    if world > 1:
+        t = torch.tensor([float(verify_failures)], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(t)
+        verify_failures = int(t.item())
     # ---- end-to-end through the public API with host buffers (e2e) ----
     out_host = torch.empty((B,) + eng.out_shape(), dtype=torch.int64).pin_memory()
     sync_all()
