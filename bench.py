@@ -134,6 +134,7 @@ def cpu_baseline_sample(model, k, n, verify, budget_s=20.0):
     from oracle import sim
     from paper_2406_02629_b200.layers import ScheduledOp, _flag_passive
     oracle.build()
+    cores = oracle.set_threads(0)            # all host cores (torchrun exports OMP_NUM_THREADS=1)
     if not hasattr(model, "nodes"):          # chain models (ModelGraph): the whole network is the sample
         weights = {name: qt.values for name, qt in model.weights.items()}
         from paper_2406_02629_b200.layers import plan_schedule
@@ -147,7 +148,7 @@ def cpu_baseline_sample(model, k, n, verify, budget_s=20.0):
             sim.simulate([op.meta() for op in ops], sim.Scheme(k, n), 7, x, weights, verify=verify)
             reps += 1
         dt = (time.perf_counter() - t0) / reps
-        return {"value": 1.0 / dt, "unit": "images/s", "cores": os.cpu_count(), "kind": "port",
+        return {"value": 1.0 / dt, "unit": "images/s", "cores": cores, "kind": "port",
                 "sample": f"oracle/sim.py full {n}PC protocol, 1 image x {reps}", "s_per_image": dt}
     weights = model.weight_values()
     total_macs = model.macs()
@@ -185,7 +186,7 @@ def cpu_baseline_sample(model, k, n, verify, budget_s=20.0):
     sim.simulate([op.meta() for op in sub], sim.Scheme(k, n), 7, x, weights, verify=verify)
     dt = time.perf_counter() - t0
     s_per_img = dt * total_macs / blk_macs
-    return {"value": 1.0 / s_per_img, "unit": "images/s", "cores": os.cpu_count(), "kind": "port",
+    return {"value": 1.0 / s_per_img, "unit": "images/s", "cores": cores, "kind": "port",
             "sample": (f"oracle/sim.py lockstep {n}PC protocol (C arithmetic, OpenMP) on residual block {blk} "
                        f"({len(sub) - 1} ops, {blk_macs / 1e9:.3f} of {total_macs / 1e9:.2f} GMAC) for 1 image: "
                        f"{dt:.1f} s, extrapolated by field-MAC share"),
@@ -266,6 +267,7 @@ def gemm_reference(args):
     extrapolated to the sweep's largest shape by MAC count."""
     import oracle
     oracle.build()
+    cores = oracle.set_threads(0)
     rng = np.random.default_rng(0)
     p = oracle.DEFAULT_PRIME
     S = 512
@@ -283,7 +285,7 @@ def gemm_reference(args):
             "ms_per_step": round(2.0 * M * N * K / (v * 1e9) * 1e3, 1), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic (uniform field elements)",
             "config": {"workload": "gemm-sweep"},
-            "cpu_baseline": {"value": round(v, 3), "unit": "Gop/s", "cores": os.cpu_count(), "kind": "port",
+            "cpu_baseline": {"value": round(v, 3), "unit": "Gop/s", "cores": cores, "kind": "port",
                              "sample": f"oracle C exact mod-p GEMM {S}^3 (u128 accumulate, OpenMP); rate is "
                                        "size-independent, ms_per_step extrapolated to the largest shape"},
             "e2e": {"value": round(v, 3), "unit": "Gop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

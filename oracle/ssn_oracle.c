@@ -121,6 +121,13 @@ void ssn_o_reduce_apply(const u64 *stack, const u64 *Rt, int m, int nout, u64 *o
 
 /* sss_linear's local product (S/layers.py:245-255): C(M,N) = A(M,K) @ B(K,N) mod p,
  * exact, with a u128 accumulator reduced every 2^12 terms (products < 2^114). */
+/* OpenMP team size for every later parallel region (torchrun exports OMP_NUM_THREADS=1 to
+ * each rank; the CPU baseline should use all host cores); returns the effective size */
+int ssn_o_set_threads(int threads) {
+    if (threads > 0) omp_set_num_threads(threads);
+    return omp_get_max_threads();
+}
+
 void ssn_o_gemm(const u64 *A, const u64 *B, u64 *C, int M, int N, int K, u64 p, int threads) {
 #ifdef _OPENMP
     if (threads > 0) omp_set_num_threads(threads);
