@@ -51,8 +51,11 @@ def gemm_kernel_name(p, L, rows):
 def use_tc(p, rows, K, O):
     # the persistent p45 kernel zero-fills (TMA out-of-range) a partial 128-row tile, so small
     # row counts (e.g. the classifier's batch rows) still run on the tensor cores
-    min_rows = 16 if p == (1 << 45) - 55 else TC_MIN_ROWS
-    return rows >= min_rows and O >= 16 and K >= 32 and tc_supported(p, K)
+    if p == (1 << 45) - 55:
+        # p45 kernel: TMA zero-fills partial 128-row tiles, 32-channel tiles and the K tail, so
+        # any shape runs exactly -- e.g. LeNet's 1-channel 5x5 conv (K = 25, O = 6)
+        return rows >= 1 and O >= 1 and K >= 1 and tc_supported(p, K)
+    return rows >= TC_MIN_ROWS and O >= 16 and K >= 32 and tc_supported(p, K)
 
 
 def _ev():

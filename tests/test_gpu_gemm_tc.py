@@ -72,6 +72,8 @@ def test_random_dense_shapes(g, rows, O, K):
     (16, 15, 17, 48, 3, 2, 1, 2, 3),
     (3, 56, 56, 64, 7, 2, 3, 1, 1),
     (256, 7, 7, 128, 3, 1, 1, 4, 5),
+    (1, 28, 28, 6, 5, 1, 2, 3, 3),              # LeNet-28 conv1: K = 25, O = 6
+    (6, 14, 14, 16, 5, 1, 0, 2, 3),             # LeNet-28 conv2: K = 150
 ])
 def test_conv_tc_vs_simt(g, C, H, W, O, k, s, pad, nimg, nparty):
     rng = np.random.default_rng(C * H + O)
@@ -117,7 +119,8 @@ def test_implicit_conv_planes_vs_im2col(kh, C, H, W, O):
     assert torch.equal(out, want)
 
 
-@pytest.mark.parametrize("rows,K,O", [(16, 2048, 1000), (40, 512, 64), (1, 256, 32)])
+@pytest.mark.parametrize("rows,K,O", [(16, 2048, 1000), (40, 512, 64), (1, 256, 32), (300, 25, 6), (7, 84, 10),
+                                      (129, 1, 3)])
 def test_small_row_dense_on_tensor_cores(rows, K, O):
     """Partial 128-row tiles (TMA zero fill beyond the rows) stay exact: classifier-sized GEMMs."""
     from paper_2406_02629_b200 import gemm as G

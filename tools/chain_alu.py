@@ -19,7 +19,13 @@ wl, B, path = sys.argv[1], int(sys.argv[2]), sys.argv[3]
 kind, k, n, verify, _ = bench.WORKLOADS[wl]
 model = bench.build_model(kind)
 eng = BatchedEngine(model, SssScheme(PrimeField(), k, n), batch=B, seed=7, verify=verify)
-x = torch.as_tensor(model.random_inputs(seed=1, batch=B), device="cuda")
+if hasattr(model, "random_inputs"):
+    xb = model.random_inputs(seed=1, batch=B)
+else:                                        # ModelGraph (LeNet-style chain models)
+    import numpy as np
+    from paper_2406_02629_b200.model import random_input
+    xb = np.stack([random_input(1, model, index=i)[0] for i in range(B)])
+x = torch.as_tensor(xb, device="cuda")
 eng.run_device(x)
 eng.enable_profiling()
 eng.run_device(x)

@@ -16,7 +16,13 @@ kind, k, n, verify, dflt = bench.WORKLOADS[wl]
 B = int(sys.argv[2]) if len(sys.argv) > 2 else dflt
 model = bench.build_model(kind)
 eng = BatchedEngine(model, SssScheme(PrimeField(), k, n), batch=B, seed=7, verify=verify)
-x = torch.as_tensor(model.random_inputs(seed=1, batch=B), device="cuda")
+if hasattr(model, "random_inputs"):
+    xb = model.random_inputs(seed=1, batch=B)
+else:                                        # ModelGraph (LeNet-style chain models)
+    import numpy as np
+    from paper_2406_02629_b200.model import random_input
+    xb = np.stack([random_input(1, model, index=i)[0] for i in range(B)])
+x = torch.as_tensor(xb, device="cuda")
 eng.run_device(x)
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
