@@ -28,8 +28,8 @@ WORKLOADS = {
     "resnet152-5pc": ("imagenet152", 3, 5, True, 32),
     "resnet50-3pc": ("imagenet50", 2, 3, False, 32),
     "resnet18-cifar-3pc": ("cifar18", 2, 3, False, 256),
-    "lenet-3pc": ("reference", 2, 3, False, 1024),
-    "lenet28-3pc": ("lenet28", 2, 3, False, 1024),     # config 1: LeNet-style CNN on 1x28x28
+    "lenet-3pc": ("reference", 2, 3, False, 16384),
+    "lenet28-3pc": ("lenet28", 2, 3, False, 8192),     # config 1: LeNet-style CNN on 1x28x28
     "gemm-sweep": ("gemm", 0, 0, False, 0),          # config 5: mod-p share GEMM + reshare sweep
 }
 SWEEP = [(256, 256, 256), (1024, 1024, 1024), (2048, 2048, 2048), (4096, 4096, 4096), (8192, 8192, 8192),

@@ -144,7 +144,7 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(done + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, party = blockIdx.z;
+    const int n0 = blockIdx.y * BN, m0 = blockIdx.x * BM, party = blockIdx.z;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; s++) {
@@ -687,7 +687,8 @@ int launch_tc(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int 
     }
     SsnField f = ssn_make_field(p);
     u64 r64 = (u64)((((unsigned __int128)1) << 64) % p);
-    dim3 grid((O + BN - 1) / BN, (M + BM - 1) / BM, nparty);
+    if ((O + BN - 1) / BN > 65535 || nparty > 65535) return SSN_ERR_UNSUPPORTED;
+    dim3 grid((M + BM - 1) / BM, (O + BN - 1) / BN, nparty);          // row tiles on x (no 65535 cap)
     SSN_COUNT_LAUNCH();
     k_gemm_tc<L><<<grid, 128, smem, st>>>(ma, mb, out, out_pstride, ohw, O, M, (Kpad + BK - 1) / BK, f, r64, cd);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
@@ -846,8 +847,8 @@ __global__ void __launch_bounds__(IC_THREADS) k_im2col_limbs(const u64 *__restri
                                                               uint8_t *__restrict__ planes, u64 x_pstride) {
     __shared__ u64 sv[IC_ROWS][IC_K + 1];
     const int party = blockIdx.z;
-    const uint32_t r0 = blockIdx.y * IC_ROWS;
-    const int k0 = blockIdx.x * IC_K;
+    const uint32_t r0 = blockIdx.x * IC_ROWS;     // row tiles on x (up to 2^31 - 1 blocks)
+    const int k0 = blockIdx.y * IC_K;
     const int t = threadIdx.x;
     const u64 *xp = x + (u64)party * x_pstride;
     const uint32_t ohw = (uint32_t)(OH * OW);
@@ -1006,7 +1007,8 @@ extern "C" int ssn_im2col_limbs(const u64 *x, int nparty, int nimg, int C, int H
     if ((u64)K > Kpad || OH < 1 || OW < 1) return SSN_ERR_ARG;
     const u64 rows = (u64)nimg * OH * OW;
     if (rows >= (1ull << 32)) return SSN_ERR_UNSUPPORTED;
-    dim3 grid((unsigned)((Kpad + IC_K - 1) / IC_K), (unsigned)((rows + IC_ROWS - 1) / IC_ROWS), (unsigned)nparty);
+    if ((Kpad + IC_K - 1) / IC_K > 65535 || nparty > 65535) return SSN_ERR_UNSUPPORTED;
+    dim3 grid((unsigned)((rows + IC_ROWS - 1) / IC_ROWS), (unsigned)((Kpad + IC_K - 1) / IC_K), (unsigned)nparty);
     SSN_COUNT_LAUNCH();
     k_im2col_limbs<<<grid, IC_THREADS, 0, (cudaStream_t)stream>>>(x, C, H, W, kh, kw, stride, pad, OH, OW, L,
                                                                   (uint32_t)rows, K, (int)Kpad, planes, x_pstride);
