@@ -152,7 +152,7 @@ int ssn_gemm_tc(const uint8_t *a_planes, const uint8_t *b_planes, int nparty, in
 /* Implicit-GEMM convolution on the tensor cores from CHANNEL-MAJOR limb planes (the A operand
  * is M-major: TMA loads 128 consecutive output pixels x 64 channels per limb; p = 2^45 - 55):
  *  mode 1 (1x1, stride 1, pad 0): a_planes [party][L][C][nimg*H*W];
- *  mode 2 (3x3, stride 1, pad 1): a_planes [3][party][L][C][nimg][H][Wp], Wp > W, Wp % 16 == 0:
+ *  mode 2 (3x3, stride 1, pad 1): a_planes [3][party][L][C][nimg][H][Wp], Wp >= W, Wp % 16 == 0:
  *    copy dx holds the rows shifted by dx - 1 columns, zero where the shift leaves the image
  *    (that and TMA's out-of-range zero fill for rows are the convolution's zero padding).
  * b_planes [party][L][O][taps*C] with k = tap*C + c (tap = dy*3 + dx; weights (O,C,kh,kw)

@@ -141,7 +141,7 @@ class BatchedEngine:
             if kh == 1 and op.stride == 1 and op.padding == 0 and (B * H * Wd) % 16 == 0:
                 mode = (1, Wd, 1)
             elif kh == 3 and op.stride == 1 and op.padding == 1 and Wd >= self.IMPLICIT_MIN_W:
-                mode = (2, (Wd // 16 + 1) * 16, 3)
+                mode = (2, gemm_mod.conv_row_pitch(Wd), 3)
             else:
                 continue
             src = idx - 1 if op.src is None else op.src

@@ -467,7 +467,7 @@ constexpr int THREADS_W = 320;                          // TMA, MMA, 8 epilogue 
 
 // A operand modes: 0 = K-major limb planes [party][L][rows][Kpad] (explicit im2col / dense);
 // 1 = channel-major planes [party*L][C][B*H*W] of a 1x1 stride-1 conv input (M-major, TMA 3-D);
-// 2 = channel-major row-padded planes [3][party*L][C][B][H*Wp] (Wp > W) of a 3x3 stride-1
+// 2 = channel-major row-padded planes [3][party*L][C][B][H*Wp] (Wp >= W, Wp % 16 == 0) of a 3x3 stride-1
 //     pad-1 conv input, copy dx holding the rows shifted by dx - 1 columns (zero where the shift
 //     leaves the image): implicit GEMM, tap (dy, dx) reads copy dx at a flattened (y, x) offset
 //     of (dy-1)*Wp; out-of-range rows are TMA zero fill -- the convolution's zero padding.
@@ -767,7 +767,7 @@ int launch_cn(const uint8_t *a, int mode, int nimg, int C, int H, int W, int Wp,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     } else {
-        if (Wp <= W || Wp % 16 || ((u64)H * Wp) % 16) return SSN_ERR_UNSUPPORTED;
+        if (Wp < W || Wp % 16 || ((u64)H * Wp) % 16) return SSN_ERR_UNSUPPORTED;
         const cuuint64_t hw = (cuuint64_t)H * Wp;
         cuuint64_t dims[4] = {hw, (cuuint64_t)nimg, (cuuint64_t)C, 3 * PL};
         cuuint64_t strides[3] = {hw, hw * nimg, hw * nimg * C};
@@ -977,7 +977,7 @@ extern "C" int ssn_planes_shift(uint8_t *planes, uint64_t rows, int Wp, void *st
 extern "C" int ssn_planes_cn(const u64 *x, int nparty, int nimg, int C, int H, int W, int Wp, int L, uint8_t *planes,
                              u64 x_pstride, int copies, void *stream) {
     if (nparty < 1 || nimg < 1 || C < 1 || H < 1 || W < 1 || Wp < W || L < 1 || L > MAXL) return SSN_ERR_ARG;
-    if (copies != 1 && (copies != 3 || Wp <= W)) return SSN_ERR_ARG;
+    if (copies != 1 && (copies != 3 || Wp % 16)) return SSN_ERR_ARG;
     const u64 total = (u64)nparty * nimg * C * H * W;
     u64 blocks = (total + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;

@@ -135,6 +135,13 @@ def field_dense(w, x, p, nimg=1, nparty=1, planes=None, force=None, timing=None)
 # Largest K per tensor-core pass: L * Kpad * 255^2 < 2^32 keeps every limb-diagonal int32
 # accumulator exact (L = 6: Kpad <= 11008).  Larger K is split and the partial products are
 # added mod p.
+def conv_row_pitch(W):
+    """Row pitch of the mode-2 (3x3) channel-major planes: W rounded up to 16 bytes (TMA needs
+    16-byte-aligned row shifts; the shifted copies' never-written edge bytes are the zero
+    padding, so no extra pad column is needed)."""
+    return (W + 15) // 16 * 16
+
+
 def max_k_chunk(p):
     L = limbs(p)
     return ((1 << 32) - 1) // (L * 65025) // 64 * 64

@@ -104,7 +104,7 @@ def test_implicit_conv_planes_vs_im2col(kh, C, H, W, O):
     pad = (kh - 1) // 2
     want = G.field_conv(w, x, 1, pad, p, nimg=B, nparty=nparty, force="tc")
     mode = 1 if kh == 1 else 2
-    Wp = W if mode == 1 else (W // 16 + 1) * 16
+    Wp = W if mode == 1 else G.conv_row_pitch(W)
     L = G.limbs(p)
     copies = 1 if mode == 1 else 3
     planes = torch.zeros((copies, nparty, L, C, B, H, Wp), dtype=torch.uint8, device="cuda")
