@@ -116,7 +116,7 @@ class BatchedEngine:
         return out
 
     # ------------------------------------------------------------------ implicit-GEMM convs
-    IMPLICIT_MIN_W = 14          # 3x3 row-padded tiles waste (Wp - W)/Wp; below 14x14 use im2col
+    IMPLICIT_MIN_W = 14          # 3x3 row-padded tiles waste (Wp - W)/Wp; below 14x14 use im2col (8x8 measured slower)
 
     def _plan_implicit_convs(self, enabled):
         """Convs whose A operand is read straight from channel-major limb planes (no im2col):
