@@ -32,6 +32,7 @@
 // p = 2^45 - 55, S/field.py:21) and every protocol constant must be a small rational (true
 // for the default party ids 1..n).  ssn_chain_supported() tells the host; other schemes use
 // the unfused kernels of ssn_elementwise.cu.
+#include <cstdlib>
 #include <cstring>
 #include "ssn.h"
 #include "ssn_field.cuh"
@@ -484,6 +485,27 @@ int build_tables(STables<K, N> &tb, const u64 *ids, const u64 *rt, const u64 *ex
     return ok;
 }
 
+// Grid cap for the grid-stride chain kernels: SSN_CHAIN_WAVES (default 8) x the resident-block
+// capacity of the device (occupancy API, cached per kernel).  Measured on ResNet-152 5PC: 1 wave
+// (persistent) 168.8 img/s, 2: 173.4, 4: 176.5, 8: 178.2, 16: 177.9, 64: 175.4 -- short blocks
+// in several waves balance the SMs better than one long persistent block each.
+template <typename KernT>
+static u64 chain_grid_cap(KernT kern, int threads) {
+    static int cap = 0;
+    if (!cap) {
+        int dev = 0, nsm = 0, per_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0) != cudaSuccess || per_sm < 1)
+            per_sm = 4;
+        const char *e = getenv("SSN_CHAIN_WAVES");
+        int waves = e ? atoi(e) : 8;
+        if (waves < 1) waves = 1;
+        cap = nsm * per_sm * waves;
+    }
+    return (u64)cap;
+}
+
 template <int K, int N>
 int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
     const u64 p = d->p;
@@ -576,13 +598,16 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
     if (a.senders > a.nout) return SSN_ERR_ARG;
     if (!d->nonlin) {
         u64 blocks = (a.nel + PLAIN_THREADS - 1) / PLAIN_THREADS;
-        if (blocks > 148ull * 16) blocks = 148ull * 16;
+        const u64 cap = chain_grid_cap(k_chain_plain<K, N>, PLAIN_THREADS);
+        if (blocks > cap) blocks = cap;
         SSN_COUNT_LAUNCH();
         k_chain_plain<K, N><<<(unsigned)blocks, PLAIN_THREADS, 0, st>>>(a, tb, f);
     } else {
         const u64 n_out = (u64)d->nb * d->c * (d->h / d->kh) * (d->w / d->kw);
         u64 blocks = (n_out + CHAIN_THREADS * WPT - 1) / (CHAIN_THREADS * WPT);
-        if (blocks > 148ull * 16) blocks = 148ull * 16;
+        const u64 cap = d->scratch || d->nonlin_only ? chain_grid_cap(k_chain_nonlin<K, N, true>, CHAIN_THREADS)
+                                                     : chain_grid_cap(k_chain_nonlin<K, N, false>, CHAIN_THREADS);
+        if (blocks > cap) blocks = cap;
         if (blocks < 1) blocks = 1;
         if (d->nonlin_only) {
             // a standalone masked nonlinearity: acc holds the n parties' input shares
@@ -595,7 +620,8 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
             a1.out_ps = a.nel;
             a1.planes = nullptr;
             u64 b1 = (a.nel + PLAIN_THREADS - 1) / PLAIN_THREADS;
-            if (b1 > 148ull * 16) b1 = 148ull * 16;
+            const u64 cap1 = chain_grid_cap(k_chain_plain<K, N>, PLAIN_THREADS);
+            if (b1 > cap1) b1 = cap1;
             SSN_COUNT_LAUNCH();
             k_chain_plain<K, N><<<(unsigned)b1, PLAIN_THREADS, 0, st>>>(a1, tb, f);
             ChainArgs a2 = a;
