@@ -968,7 +968,7 @@ extern "C" int ssn_planes_shift(uint8_t *planes, uint64_t rows, int Wp, void *st
     if (Wp < 16 || Wp % 16 || rows == 0) return SSN_ERR_ARG;
     const u64 total = rows * (Wp / 16);
     u64 blocks = (total + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > 148 * 64) blocks = 148 * 64;
     SSN_COUNT_LAUNCH();
     k_planes_shift<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(planes, rows, Wp);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
@@ -980,7 +980,7 @@ extern "C" int ssn_planes_cn(const u64 *x, int nparty, int nimg, int C, int H, i
     if (copies != 1 && (copies != 3 || Wp % 16)) return SSN_ERR_ARG;
     const u64 total = (u64)nparty * nimg * C * H * W;
     u64 blocks = (total + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > 148 * 64) blocks = 148 * 64;
     SSN_COUNT_LAUNCH();
     k_planes_cn<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, nimg, C, H, W, Wp, L, planes, x_pstride, total,
                                                                      copies, nparty);
@@ -993,7 +993,7 @@ extern "C" int ssn_limb_split(const u64 *x, u64 rows, u64 K, u64 Kpad, int L, ui
     u64 total = (u64)nparty * rows * (Kpad / 8);
     if (total == 0) return 0;
     u64 blocks = (total + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > 148 * 64) blocks = 148 * 64;
     SSN_COUNT_LAUNCH();
     k_limb_split<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, rows, K, Kpad, L, planes, x_pstride, total);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
