@@ -198,3 +198,20 @@ def test_resnet152_5pc_full_size_matches_plaintext(ssn):
     want, _ = resnet.plaintext_forward(net, xb, device="cuda")
     assert np.array_equal(eng.run(xb), want)
     assert int(eng.fail.item()) == 0
+
+
+@pytest.mark.parametrize("streams", [2, 3])
+def test_stream_pipelined_engine_matches_plaintext(ssn, streams):
+    """bench.py --streams S: the batch split over S engines on S CUDA streams (shared weight
+    shares and limb planes) decodes to the same integer plaintext as one engine."""
+    from paper_2406_02629_b200 import resnet
+    from paper_2406_02629_b200.batched import StreamPipelinedEngine
+    net = resnet.tiny_resnet(seed=3)
+    scheme = ssn.SssScheme(ssn.PrimeField(), 3, 5)
+    B = 2 * streams
+    xb = net.random_inputs(seed=9, batch=B)
+    eng = StreamPipelinedEngine(net, scheme, batch=B, streams=streams, seed=4, verify=True)
+    want, _ = resnet.plaintext_forward(net, xb)
+    for _ in range(2):
+        assert np.array_equal(eng.run(xb), want)
+    assert all(int(e.fail.item()) == 0 for e in eng.engines)
