@@ -25,8 +25,8 @@ sys.path.insert(0, ROOT)
 
 WORKLOADS = {
     # name: (builder, k, n, verify, default batch per GPU)
-    "resnet152-5pc": ("imagenet152", 3, 5, True, 32),
-    "resnet50-3pc": ("imagenet50", 2, 3, False, 32),
+    "resnet152-5pc": ("imagenet152", 3, 5, True, 64),
+    "resnet50-3pc": ("imagenet50", 2, 3, False, 64),
     "resnet18-cifar-3pc": ("cifar18", 2, 3, False, 256),
     "lenet-3pc": ("reference", 2, 3, False, 16384),
     "lenet28-3pc": ("lenet28", 2, 3, False, 8192),     # config 1: LeNet-style CNN on 1x28x28
@@ -34,12 +34,11 @@ WORKLOADS = {
 }
 SWEEP = [(256, 256, 256), (1024, 1024, 1024), (2048, 2048, 2048), (4096, 4096, 4096), (8192, 8192, 8192),
          (16384, 4096, 4096), (4096, 4096, 16384), (16384, 16384, 16384)]
-# default CUDA streams per GPU (co-resident placement).  --streams S splits the batch over S
-# streams so one part's tensor-bound GEMMs overlap another's ALU-bound protocol chains: +3-4%
-# images/s (profiles/r01/README.md, batch/stream sweep), but then every kernel's CUDA-event time
-# includes the co-running kernels and the per-kernel rooflines stop describing the kernels.  The
-# default stays one stream so `roofline` is a clean per-kernel measurement.
-DEFAULT_STREAMS = {}
+# default CUDA streams per GPU (co-resident placement).  S streams split the batch so one part's
+# tensor-bound GEMMs overlap another's ALU-bound protocol chains (profiles/r01/README.md,
+# batch/stream sweep).  The first timed step runs the sub-batches back to back: its per-kernel
+# CUDA events give each kernel's own time for the rooflines; the remaining steps overlap.
+DEFAULT_STREAMS = {"resnet152-5pc": 2, "resnet50-3pc": 2, "resnet18-cifar-3pc": 2}
 METRIC = "ResNet-152 secure-inference images/s (5PC t=2, verification on, 224x224)"
 
 
@@ -751,7 +750,12 @@ def main():
             stash = [(e, e._prof) for e in engines]
             for e in engines:
                 e._prof = None
-        eng.run_device(x_dev)
+        if i < prof_steps and nstreams > 1:
+            # the profiled step runs the stream sub-batches back to back, so every kernel's
+            # CUDA-event time is its own (no co-running kernels); the other steps overlap
+            eng.run_device(x_dev, serial=True)
+        else:
+            eng.run_device(x_dev)
     e1.record(stream)
     sync_all()
     if stash is not None:

@@ -739,17 +739,22 @@ class StreamPipelinedEngine:
     def run(self, x_int, timings=None):
         return self.run_device(x_int).cpu().numpy()
 
-    def run_device(self, x_int, timings=None):
+    def run_device(self, x_int, timings=None, serial=False):
+        """serial=True runs the sub-batches back to back (each stream waits for the previous
+        one): same results, no kernel overlap -- bench.py times its per-kernel roofline step so."""
         if not isinstance(x_int, torch.Tensor):
             x_int = torch.as_tensor(np.asarray(x_int, dtype=np.int64))
         x = x_int.to(device=self.engines[0].dev, dtype=torch.int64)
         cur = torch.cuda.current_stream()
         parts = x.chunk(self.nstreams)
         outs = []
+        prev = cur
         for eng, st, xp in zip(self.engines, self.streams, parts):
-            st.wait_stream(cur)
+            st.wait_stream(prev if serial else cur)
             with torch.cuda.stream(st):
                 outs.append(eng.run_device(xp))
+            if serial:
+                prev = st
         for st, o in zip(self.streams, outs):
             cur.wait_stream(st)
             o.record_stream(cur)
