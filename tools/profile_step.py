@@ -13,7 +13,8 @@ from paper_2406_02629_b200.sss import SssScheme  # noqa: E402
 
 wl = sys.argv[1] if len(sys.argv) > 1 else "resnet152-5pc"
 kind, k, n, verify, dflt = bench.WORKLOADS[wl]
-B = int(sys.argv[2]) if len(sys.argv) > 2 else dflt
+# default: one bench engine's batch (the bench splits its batch over DEFAULT_STREAMS engines)
+B = int(sys.argv[2]) if len(sys.argv) > 2 else dflt // bench.DEFAULT_STREAMS.get(wl, 1)
 model = bench.build_model(kind)
 eng = BatchedEngine(model, SssScheme(PrimeField(), k, n), batch=B, seed=7, verify=verify)
 if hasattr(model, "random_inputs"):
