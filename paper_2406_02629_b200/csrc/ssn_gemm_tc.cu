@@ -846,6 +846,8 @@ __global__ void __launch_bounds__(IC_THREADS) k_im2col_limbs(const u64 *__restri
                                                               uint32_t rows, int K, int Kpad,
                                                               uint8_t *__restrict__ planes, u64 x_pstride) {
     __shared__ u64 sv[IC_ROWS][IC_K + 1];
+    __shared__ int64_t s_off[IC_K];               // k -> c*H*W (or -1 past K), tap row/col - pad
+    __shared__ int s_i[IC_K], s_j[IC_K];
     const int party = blockIdx.z;
     const uint32_t r0 = blockIdx.x * IC_ROWS;     // row tiles on x (up to 2^31 - 1 blocks)
     const int k0 = blockIdx.y * IC_K;
@@ -853,6 +855,19 @@ __global__ void __launch_bounds__(IC_THREADS) k_im2col_limbs(const u64 *__restri
     const u64 *xp = x + (u64)party * x_pstride;
     const uint32_t ohw = (uint32_t)(OH * OW);
     const int khw = kh * kw;
+    if (t < IC_K) {                               // the block's 64 k decompositions, once
+        const int k = k0 + t;
+        if (k < K) {
+            const int c = k / khw, rem = k - c * khw;
+            const int i = rem / kw;
+            s_off[t] = (int64_t)c * H * W;
+            s_i[t] = i - pad;
+            s_j[t] = rem - i * kw - pad;
+        } else {
+            s_off[t] = -1;
+        }
+    }
+    __syncthreads();
     {
         const int rr = t & (IC_ROWS - 1);
         const uint32_t r = r0 + rr;
@@ -866,16 +881,14 @@ __global__ void __launch_bounds__(IC_THREADS) k_im2col_limbs(const u64 *__restri
             ox = pix - oy * OW;
         }
         const u64 *ximg = xp + (u64)img * C * H * W;
+        const int oys = oy * stride, oxs = ox * stride;
 #pragma unroll 4
         for (int kk = t / IC_ROWS; kk < IC_K; kk += IC_THREADS / IC_ROWS) {
-            const int k = k0 + kk;
             u64 v = 0;
-            if (rok && k < K) {
-                const int c = k / khw;
-                const int rem = k - c * khw;
-                const int i = rem / kw, j = rem - i * kw;
-                const int sy = oy * stride + i - pad, sx = ox * stride + j - pad;
-                if (sy >= 0 && sy < H && sx >= 0 && sx < W) v = ximg[((u64)c * H + sy) * W + sx];
+            const int64_t off = s_off[kk];
+            if (rok && off >= 0) {
+                const int sy = oys + s_i[kk], sx = oxs + s_j[kk];
+                if (sy >= 0 && sy < H && sx >= 0 && sx < W) v = ximg[off + (int64_t)sy * W + sx];
             }
             sv[rr][kk] = v;
         }
