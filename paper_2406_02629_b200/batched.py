@@ -523,7 +523,7 @@ class BatchedEngine:
         timing = {} if self._prof is not None else None
         K = _count(w.shape[2:])
         ohw = _count(op.out_shape[1:]) if conv else 1
-        tc = gemm_mod.use_tc(p, B * ohw, K, O)
+        tc = gemm_mod.use_tc(p, B * ohw, K, O) and not (conv and gemm_mod.direct_conv(p, O, K))
         planes = None
         if tc:
             planes = self._planes.get(op.weight)

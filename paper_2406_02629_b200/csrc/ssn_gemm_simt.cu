@@ -117,6 +117,55 @@ static int fold_period(u64 p) {
     return (1 << room) / TK * TK;
 }
 
+// Direct conv for few output channels (LeNet's 1->6 and 6->16 5x5 layers): one thread per
+// output pixel computes all O <= OMAX channels, the party's weights broadcast from shared
+// memory (k-major), 128-bit accumulators, one reduction per output.  The tiled kernel above
+// would spend 64 - O of its 64 weight rows on zeros, and the tensor-core path needs an im2col
+// expansion of 6*Kpad bytes per output pixel.
+template <int OMAX>
+__global__ void __launch_bounds__(128) k_conv_direct(const u64 *__restrict__ Wt, u64 w_b, const u64 *__restrict__ X,
+                                                     u64 x_b, u64 *__restrict__ out, u64 o_b, int O, int K, u64 N,
+                                                     ConvGeom g, SsnField f, u64 r64) {
+    extern __shared__ u64 sw[];                       // [K][OMAX]
+    const int party = blockIdx.y;
+    Wt += party * w_b;
+    X += party * x_b;
+    out += party * o_b;
+    for (int e = threadIdx.x; e < K * OMAX; e += blockDim.x) {
+        const int k = e / OMAX, o = e - k * OMAX;
+        sw[e] = o < O ? Wt[(u64)o * K + k] : 0;
+    }
+    __syncthreads();
+    const u64 ohw = (u64)g.OH * g.OW;
+    const u64 chw = (u64)g.C * g.H * g.W;
+    for (u64 n = blockIdx.x * (u64)blockDim.x + threadIdx.x; n < N; n += (u64)gridDim.x * blockDim.x) {
+        const u64 img = n / ohw;
+        const int pix = (int)(n - img * ohw);
+        const int oy = pix / g.OW, ox = pix - (pix / g.OW) * g.OW;
+        u128s acc[OMAX];
+#pragma unroll
+        for (int o = 0; o < OMAX; o++) acc[o] = {0, 0};
+        const u64 *xi = X + img * chw;
+        int k = 0;
+        for (int c = 0; c < g.C; c++)
+            for (int i = 0; i < g.kh; i++) {
+                const int sy = oy * g.stride + i - g.pad;
+                const bool rowok = sy >= 0 && sy < g.H;
+                for (int j = 0; j < g.kw; j++, k++) {
+                    const int sx = ox * g.stride + j - g.pad;
+                    if (!rowok || sx < 0 || sx >= g.W) continue;
+                    const u64 v = xi[((u64)c * g.H + sy) * g.W + sx];
+                    const u64 *wk = sw + k * OMAX;
+#pragma unroll
+                    for (int o = 0; o < OMAX; o++) ssn_mac(acc[o], v, wk[o]);
+                }
+            }
+#pragma unroll
+        for (int o = 0; o < OMAX; o++)
+            if (o < O) out[(img * O + o) * ohw + pix] = ssn_reduce128(acc[o], f, r64);
+    }
+}
+
 // conv: W [parties][O][C*kh*kw], x [parties][nimg][C][H][W] -> out [parties][nimg][O][OH*OW]
 extern "C" int ssn_conv_simt(const u64 *w, u64 w_pstride, const u64 *x, u64 x_pstride, u64 *out, u64 out_pstride,
                              int nparty, int nimg, int O, int C, int H, int W, int kh, int kw, int stride, int pad,
@@ -133,6 +182,19 @@ extern "C" int ssn_conv_simt(const u64 *w, u64 w_pstride, const u64 *x, u64 x_ps
     dim3 grid((unsigned)((N + TN - 1) / TN), (unsigned)((O + TM - 1) / TM), (unsigned)nparty);
     SsnField f = ssn_make_field(p);
     u64 r64 = (u64)((((unsigned __int128)1) << 64) % p);
+    // few output channels and no mid-sum folding needed: the direct kernel
+    if (O <= 16 && (u64)K * 16 * 8 <= 48 * 1024 && fold_period(p) >= K && N < (1ull << 40)) {
+        u64 blocks = (N + 127) / 128;
+        if (blocks > 148ull * 32) blocks = 148ull * 32;
+        SSN_COUNT_LAUNCH();
+        if (O <= 8)
+            k_conv_direct<8><<<dim3((unsigned)blocks, (unsigned)nparty), 128, (size_t)K * 8 * 8, (cudaStream_t)strm>>>(
+                w, w_pstride, x, x_pstride, out, out_pstride, O, K, N, g, f, r64);
+        else
+            k_conv_direct<16><<<dim3((unsigned)blocks, (unsigned)nparty), 128, (size_t)K * 16 * 8, (cudaStream_t)strm>>>(
+                w, w_pstride, x, x_pstride, out, out_pstride, O, K, N, g, f, r64);
+        return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
+    }
     SSN_COUNT_LAUNCH();
     k_gemm_simt<true><<<grid, 256, 0, (cudaStream_t)strm>>>(w, w_pstride, x, x_pstride, out, out_pstride, O, K, N,
                                                             ohw, g, f, r64, fold_period(p));

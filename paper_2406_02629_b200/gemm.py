@@ -64,6 +64,15 @@ def _ev():
     return e
 
 
+def direct_conv(p, O, K):
+    """Few-output-channel convs (LeNet's 1->6 and 6->16 5x5) run faster as the direct CUDA-core
+    kernel inside ssn_conv_simt (all O channels per output pixel, no im2col) than as im2col +
+    tensor-core GEMM with 32-wide channel tiles mostly empty."""
+    # measured: LeNet-28 conv1 (K = 25, O = 6) and the reference model's convs win; conv2
+    # (K = 150, O = 16: 2,400 64-bit MACs per pixel) is faster on the tensor cores
+    return p == (1 << 45) - 55 and O <= 16 and K * O <= 256
+
+
 def field_conv(w, x, stride, padding, p, nimg=1, nparty=1, planes=None, force=None, timing=None):
     """w: (nparty, O, C, kh, kw), x: (nparty, nimg, C, H, W) -> (nparty, nimg, O, OH, OW)
     (leading unit dims squeezed when nparty == nimg == 1).  timing: optional dict that
@@ -77,7 +86,7 @@ def field_conv(w, x, stride, padding, p, nimg=1, nparty=1, planes=None, force=No
     out = torch.empty((nparty, nimg, O, OH, OW) if (nparty > 1 or nimg > 1) else (O, OH, OW),
                       dtype=torch.int64, device=x.device)
     rows = nimg * OH * OW
-    tc = use_tc(p, rows, K, O) if force is None else force == "tc"
+    tc = use_tc(p, rows, K, O) and not direct_conv(p, O, K) if force is None else force == "tc"
     if tc:
         L, Kp = limbs(p), kpad(K)
         if planes is None:
