@@ -109,14 +109,17 @@ int ssn_inv(const uint64_t *a, uint64_t *out, uint64_t n, uint64_t p, void *strm
 int ssn_rand(uint64_t *out, uint64_t n, uint64_t lo, uint64_t range, uint64_t seed, uint64_t stream, void *strm);
 
 /* Trusted source, additive mask (gen_additive_mask, S/masks.py:39-54): e = 1 + U[0, emax),
- * alpha = e*step, comp = -e, both shared at ids: alpha[t][i], comp[t][i]. */
+ * alpha = e*step, comp = -e, both shared at ids: alpha[t][i], comp[t][i].
+ * Consumes THREE Philox streams: e from `stream`, the alpha / comp sharing coefficients from
+ * `stream + 1` / `stream + 2` -- callers reserve all three (DeviceRng.next_stream(3)). */
 int ssn_mask_trunc(uint64_t n, uint64_t step, uint64_t emax, uint64_t seed, uint64_t stream, int km1,
                    const uint64_t *ids, int nids, uint64_t *alpha, uint64_t *comp, uint64_t out_tstride, uint64_t p,
                    void *strm);
 
 /* Trusted source, multiplicative mask (gen_multiplicative_mask, S/masks.py:67-90): beta
  * constant per kh x kw window in [1, bmax], shared per input element; beta^-1 shared per
- * window. Uses Philox streams `stream` and `stream + 1`. */
+ * window.  Consumes THREE Philox streams: beta from `stream`, the beta sharing coefficients from
+ * `stream + 1`, the beta^-1 sharing coefficients from `stream + 2` -- callers reserve all three. */
 int ssn_mask_beta(int nb, int c, int h, int wd, int kh, int kw, uint64_t bmax, uint64_t seed, uint64_t stream,
                   int km1, const uint64_t *ids, int nids, uint64_t *beta, uint64_t beta_tstride, uint64_t *binv,
                   uint64_t binv_tstride, uint64_t p, void *strm);
@@ -228,6 +231,20 @@ typedef struct ssn_chain_desc {
     /* 1: only the masked nonlinearity (sss_nonlinear) of the n parties' input shares in acc
      * (a nonlinear op outside a linear chain, e.g. the global pool); reshare fields unused */
     int nonlin_only;
+    /* 1: reference-stream (host-fed) masks, the parity mode of S/engine.py's purpose lanes:
+     * instead of Philox draws, party t's share of the trusted source's material for element i
+     * is read at image-element ii = i mod h_period (every image of the batch sees the same
+     * bundle, like the reference's runs over input_index, S/engine.py:64-74):
+     *   h_zero  [n][h_period]  zero shares of the linear op (gen_zero_shares, S/masks.py:93-96)
+     *   h_alpha [n][h_period], h_comp [n][h_period]  (gen_additive_mask, S/masks.py:39-54)
+     *   h_tcoef [k-1][h_period] the elite's fresh truncation coefficients (its PURPOSE_PARTY
+     *           stream, S/layers.py:308, drawn after its reshare sub-share draws)
+     *   h_beta  [n][h_period]  beta shares per nonlinear input element (S/masks.py:67-90)
+     *   h_binv  [n][h_period_out] beta^-1 shares per nonlinear output element.
+     * For nonlin_only launches h_period is the nonlinear input size per image. */
+    int host_masks;
+    const uint64_t *h_zero, *h_alpha, *h_comp, *h_tcoef, *h_beta, *h_binv;
+    uint64_t h_period, h_period_out;
 } ssn_chain_desc;
 
 int ssn_layer_chain(const ssn_chain_desc *desc, void *stream);

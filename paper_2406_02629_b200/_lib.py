@@ -109,6 +109,9 @@ class ChainDesc(ctypes.Structure):
         ("scratch", _P),
         ("inv_table", _P), ("inv_table_len", _U64),
         ("nonlin_only", _I32),
+        ("host_masks", _I32),
+        ("h_zero", _P), ("h_alpha", _P), ("h_comp", _P), ("h_tcoef", _P), ("h_beta", _P), ("h_binv", _P),
+        ("h_period", _U64), ("h_period_out", _U64),
     ]
 
 _lib = None

@@ -596,7 +596,7 @@ class BatchedEngine:
         emax = additive_mask_bound(self.scheme.field, step, op.value_bound)
         A = torch.empty((n, N), dtype=torch.int64, device=self.dev)
         Cm = torch.empty((n, N), dtype=torch.int64, device=self.dev)
-        _lib.call("ssn_mask_trunc", N, step, emax, src_rng.seed, src_rng.next_stream(), self.k - 1, self.ids_all, n,
+        _lib.call("ssn_mask_trunc", N, step, emax, src_rng.seed, src_rng.next_stream(3), self.k - 1, self.ids_all, n,
                   _lib.ptr(A), _lib.ptr(Cm), N, p, _lib.stream_ptr())
         self.kernel_launches += 1
         self._mask_cache[idx] = (A, Cm)
@@ -670,7 +670,7 @@ class BatchedEngine:
         bmax = multiplicative_mask_bound(self.scheme.field, op.value_bound)
         BETA = torch.empty((n, n_in), dtype=torch.int64, device=self.dev)
         BINV = torch.empty((n, n_out), dtype=torch.int64, device=self.dev)
-        _lib.call("ssn_mask_beta", B, c, h, w, kh, kw, bmax, src_rng.seed, src_rng.next_stream(2), k - 1,
+        _lib.call("ssn_mask_beta", B, c, h, w, kh, kw, bmax, src_rng.seed, src_rng.next_stream(3), k - 1,
                   self.ids_all, n, _lib.ptr(BETA), n_in, _lib.ptr(BINV), n_out, p, _lib.stream_ptr())
         MASKED = torch.empty((m, n_in), dtype=torch.int64, device=self.dev)
         self._ew(2, X, BETA, MASKED, m * n_in)

@@ -96,6 +96,14 @@ struct ChainArgs {
     u64 pl_ps, pl_ls, pl_cs, pl_is;
     int pl_wp, pl_copies, pl_nparty;
     const u64 *inv_table;   // optional: inv_table[b] = b^-1 mod p for b in [1, bmax]
+    // reference-stream (host-fed) trusted-source material, used by the HF instantiations: the
+    // share of party t of image-element ii = i mod per (every image of the batch gets the SAME
+    // masks, exactly like the reference's runs over input_index, S/engine.py:64-74):
+    //   h_zero / h_alpha / h_comp / h_beta [t*per + ii],  h_tcoef [e*per + ii] (the elite's fresh
+    //   truncation coefficients, PURPOSE_PARTY lane), h_binv [t*per_out + oo]
+    const u64 *h_zero, *h_alpha, *h_comp, *h_tcoef, *h_beta, *h_binv;
+    u64 per, per_out;
+    FastDiv f_per, f_per_out;
 };
 
 constexpr int CHAIN_THREADS = 128;
@@ -189,7 +197,9 @@ __device__ __forceinline__ u64 trunc_val(u64 v, const ChainArgs &a) {
 }
 
 // reshare + rerand + bias + truncation (+ residual add) of element i for all N parties.
-template <int K, int N>
+// HF: the trusted source's masks and the elite's truncation coefficients are host-fed shares
+// (reference-stream parity mode) instead of in-register Philox draws.
+template <int K, int N, bool HF>
 __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, N> &tb, uint32_t i, u64 (&x)[N],
                                            unsigned long long &bad) {
     constexpr int M = 2 * K - 1;
@@ -215,21 +225,27 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
     for (int fr = 0; fr < K; fr++) subsum[fr] = xsum_of<M>(sub[fr]);
     // source: zero shares (gen_zero_shares) and the truncation masks (gen_additive_mask)
     // (zero, alpha and comp coefficients + the 64 bits of e from one source reservoir)
-    constexpr int NCS = (45 * 3 * (K - 1) + 64 + 127) / 128;
-    Reservoir<NCS> rs;
-    fill<NCS>(rs, a.sseed, a.sstream, i, 0x900u);
     u64 z[K - 1], ca[K - 1], cc[K - 1];
+    u64 alpha = 0, comp = 0;
+    uint32_t ii = 0;
+    if constexpr (HF) {
+        ii = i - fdiv(i, a.f_per) * (uint32_t)a.per;
+    } else {
+        constexpr int NCS = (45 * 3 * (K - 1) + 64 + 127) / 128;
+        Reservoir<NCS> rs;
+        fill<NCS>(rs, a.sseed, a.sstream, i, 0x900u);
 #pragma unroll
-    for (int e = 0; e < K - 1; e++) {
-        z[e] = take45<NCS>(rs, 45 * e);
-        ca[e] = take45<NCS>(rs, 45 * (K - 1 + e));
-        cc[e] = take45<NCS>(rs, 45 * (2 * (K - 1) + e));
+        for (int e = 0; e < K - 1; e++) {
+            z[e] = take45<NCS>(rs, 45 * e);
+            ca[e] = take45<NCS>(rs, 45 * (K - 1 + e));
+            cc[e] = take45<NCS>(rs, 45 * (2 * (K - 1) + e));
+        }
+        // e = 1 + U[0, emax) by multiply-shift of 64 random bits (bias <= emax / 2^64 <= 2^-32)
+        const u64 e = 1 + __umul64hi(take64<NCS>(rs, 45 * 3 * (K - 1)), a.emax);
+        const u64 em = red64(e);
+        alpha = mulm(em, a.stepm);
+        comp = em ? PP - em : 0;
     }
-    // e = 1 + U[0, emax) by multiply-shift of 64 random bits (bias <= emax / 2^64 <= 2^-32)
-    const u64 e = 1 + __umul64hi(take64<NCS>(rs, 45 * 3 * (K - 1)), a.emax);
-    const u64 em = red64(e);
-    const u64 alpha = mulm(em, a.stepm);
-    const u64 comp = em ? PP - em : 0;
     const uint32_t bq = fdiv(i, a.bias_div);
     const uint32_t ch = bq - fdiv(bq, a.bias_mod) * a.bias_mod.d;
     // ---- step 2 (RESHARE_BACK): front fr applies R^T; step 3: out rank t reconstructs,
@@ -243,9 +259,12 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
             u64 back[K];
 #pragma unroll
             for (int fr = 0; fr < K; fr++) back[fr] = lin_s<M>(sub[fr], subsum[fr], tb.rt[t]);
-            u64 y = lin<K>(back, tb.wf) + share_raw<K, N>(0, z, tb, t) + a.bias[(u64)t * a.bias_ps + ch];
+            u64 y = lin<K>(back, tb.wf) + a.bias[(u64)t * a.bias_ps + ch];
+            if constexpr (HF) y += a.h_zero[(u64)t * a.per + ii];
+            else y += share_raw<K, N>(0, z, tb, t);
             if (t == a.fault_rank && i == 0) y += 1;                                        // test hook
-            masked[t] = lz(y + share_raw<K, N>(alpha, ca, tb, t));
+            if constexpr (HF) masked[t] = lz(y + a.h_alpha[(u64)t * a.per + ii]);
+            else masked[t] = lz(y + share_raw<K, N>(alpha, ca, tb, t));
         }
     }
     // ---- truncation elite: rec over the front, RS check of the extra points, decode/floor/round
@@ -259,16 +278,23 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
     const u64 tm = trunc_val(v, a);
     // fresh (k, n) shares of the truncated value (SHARE_DIST), + comp at every rank
     u64 g[K - 1];
-    coeffs<K>(g, a.pseed, a.pstream + M, i);
+    if constexpr (HF) {
+#pragma unroll
+        for (int e = 0; e < K - 1; e++) g[e] = a.h_tcoef[(u64)e * a.per + ii];
+    } else {
+        coeffs<K>(g, a.pseed, a.pstream + M, i);
+    }
 #pragma unroll
     for (int t = 0; t < N; t++) {
-        u64 s = share_raw<K, N>(tm, g, tb, t) + share_raw<K, N>(comp, cc, tb, t);
+        u64 s = share_raw<K, N>(tm, g, tb, t);
+        if constexpr (HF) s += a.h_comp[(u64)t * a.per + ii];
+        else s += share_raw<K, N>(comp, cc, tb, t);
         if (a.other) s += a.other[(u64)t * a.other_ps + i];                              // residual add
         x[t] = lz(s);                                                                   // lazy
     }
 }
 
-template <int K, int N>
+template <int K, int N, bool HF>
 __global__ void __launch_bounds__(PLAIN_THREADS, 4) k_chain_plain(ChainArgs a, const __grid_constant__ STables<K, N> tb,
                                                      SsnField f) {
     unsigned long long bad = 0;
@@ -276,7 +302,7 @@ __global__ void __launch_bounds__(PLAIN_THREADS, 4) k_chain_plain(ChainArgs a, c
 #pragma unroll 1
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nel; i += gridDim.x * blockDim.x) {
         u64 x[N];
-        chain_elem<K, N>(a, tb, i, x, bad);
+        chain_elem<K, N, HF>(a, tb, i, x, bad);
 #pragma unroll
         for (int t = 0; t < N; t++) a.out[(u64)t * a.out_ps + i] = canon(x[t]);
     }
@@ -327,7 +353,7 @@ constexpr int WPT = 8;
 // SPLIT: the reshare/truncation/add part already ran (k_chain_plain into a.acc = its n-party
 // output) and this kernel only runs the masked nonlinearity, reading each party's share.
 // Two kernels of half the code each run faster than one that overflows the instruction cache.
-template <int K, int N, bool SPLIT>
+template <int K, int N, bool SPLIT, bool HF>
 __global__ void __launch_bounds__(CHAIN_THREADS, 6) k_chain_nonlin(ChainArgs a, const __grid_constant__ STables<K, N> tb,
                                                                 SsnField f) {
     constexpr int M = 2 * K - 1;
@@ -347,7 +373,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 6) k_chain_nonlin(ChainArgs a, 
             const uint32_t o = base + q * CHAIN_THREADS + threadIdx.x;
             u64 pl = 0, bt = 1;
             if (o < n_out) {
-                bt = 1 + ssn_rand_range(a.sseed, a.sstream + 4, o, 0, a.bmax);     // window-constant beta
+                if constexpr (!HF) bt = 1 + ssn_rand_range(a.sseed, a.sstream + 4, o, 0, a.bmax);  // window-constant beta
                 uint32_t base_in = o;
                 if (pooled) {
                     const uint32_t img = fdiv(o, a.f_chw), rem = o - img * chw;
@@ -366,14 +392,20 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 6) k_chain_nonlin(ChainArgs a, 
 #pragma unroll
                             for (int t = 0; t < M; t++) x[t] = a.acc[(u64)t * a.acc_ps + i];
                         } else {
-                            chain_elem<K, N>(a, tb, i, x, bad);
+                            chain_elem<K, N, HF>(a, tb, i, x, bad);
                         }
                         // participants mask with their beta shares (NONLIN_MASKED); elite rec over m
-                        u64 cb[K - 1];
-                        coeffs<K>(cb, a.sseed, a.sstream + 5, i);
                         u64 mk[M];
+                        if constexpr (HF) {
+                            const uint32_t ii = i - fdiv(i, a.f_per) * (uint32_t)a.per;
 #pragma unroll
-                        for (int j = 0; j < M; j++) mk[j] = mulm(x[j], share_raw<K, N>(bt, cb, tb, j));
+                            for (int j = 0; j < M; j++) mk[j] = mulm(x[j], a.h_beta[(u64)j * a.per + ii]);
+                        } else {
+                            u64 cb[K - 1];
+                            coeffs<K>(cb, a.sseed, a.sstream + 5, i);
+#pragma unroll
+                            for (int j = 0; j < M; j++) mk[j] = mulm(x[j], share_raw<K, N>(bt, cb, tb, j));
+                        }
                         const u64 v = canon(lin<M>(mk, tb.wp));
                         i64 sv = v > PHALF ? (i64)v - (i64)PP : (i64)v;
                         if (a.relu && sv <= 0) sv = 0;
@@ -384,7 +416,9 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 6) k_chain_nonlin(ChainArgs a, 
             }
             plain[q] = pl;
             beta[q] = bt;
-            if (a.inv_table) {
+            if constexpr (HF) {
+                pre[q] = 0;                         // beta^-1 shares are host-fed
+            } else if (a.inv_table) {
                 pre[q] = a.inv_table[bt];           // source's beta^-1 from the inverse table
             } else {
                 pre[q] = run;                       // product of this thread's earlier betas
@@ -393,7 +427,7 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 6) k_chain_nonlin(ChainArgs a, 
         }
         // source: beta^-1 for every window of the warp from one inversion (no table)
         u64 inv = 0;
-        if (!a.inv_table) {
+        if (!HF && !a.inv_table) {
             const u64 wpre = warp_excl_prefix(run, lane);
             const u64 wsuf = warp_excl_suffix(run, lane);
             const u64 total = __shfl_sync(0xffffffffu, mulm(wpre, run), 31);
@@ -402,16 +436,20 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 6) k_chain_nonlin(ChainArgs a, 
 #pragma unroll 1
         for (int q = WPT - 1; q >= 0; q--) {
             const uint32_t o = base + q * CHAIN_THREADS + threadIdx.x;
-            u64 binv;
-            if (a.inv_table) {
-                binv = pre[q];
-            } else {
-                binv = mulm(inv, pre[q]);
-                inv = mulm(inv, beta[q]);
+            u64 binv = 0;
+            if constexpr (!HF) {
+                if (a.inv_table) {
+                    binv = pre[q];
+                } else {
+                    binv = mulm(inv, pre[q]);
+                    inv = mulm(inv, beta[q]);
+                }
             }
             if (o < n_out) {
                 u64 cbi[K - 1];
-                coeffs<K>(cbi, a.sseed, a.sstream + 6, o);
+                uint32_t oo = 0;
+                if constexpr (HF) oo = o - fdiv(o, a.f_per_out) * (uint32_t)a.per_out;
+                else coeffs<K>(cbi, a.sseed, a.sstream + 6, o);
                 uint8_t *pb = nullptr;
                 int xq = 0;
                 if (a.planes) {
@@ -424,7 +462,10 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 6) k_chain_nonlin(ChainArgs a, 
 #pragma unroll
                 for (int t = 0; t < N; t++)
                     if (t < a.fan) {
-                        const u64 v = canon(mulm(plain[q], share_raw<K, N>(binv, cbi, tb, t)));
+                        u64 bis;
+                        if constexpr (HF) bis = a.h_binv[(u64)t * a.per_out + oo];
+                        else bis = share_raw<K, N>(binv, cbi, tb, t);
+                        const u64 v = canon(mulm(plain[q], bis));
                         a.out[(u64)t * a.out_ps + o] = v;
                         if (pb != nullptr && t < a.pl_nparty) {        // limb planes for the next conv
                             if (SPLIT && a.pl_copies == 1) {
@@ -491,19 +532,75 @@ int build_tables(STables<K, N> &tb, const u64 *ids, const u64 *rt, const u64 *ex
 // in several waves balance the SMs better than one long persistent block each.
 template <typename KernT>
 static u64 chain_grid_cap(KernT kern, int threads) {
-    static int cap = 0;
-    if (!cap) {
-        int dev = 0, nsm = 0, per_sm = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0) != cudaSuccess || per_sm < 1)
-            per_sm = 4;
-        const char *e = getenv("SSN_CHAIN_WAVES");
-        int waves = e ? atoi(e) : 8;
-        if (waves < 1) waves = 1;
-        cap = nsm * per_sm * waves;
+    // cached per (kernel, block size, device): the plain / nonlinear / split instantiations share
+    // one function-pointer TYPE but not their occupancy
+    struct Entry {
+        const void *fn;
+        int threads, dev;
+        u64 cap;
+    };
+    static Entry cache[32];
+    static int used = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    for (int e = 0; e < used; e++)
+        if (cache[e].fn == (const void *)kern && cache[e].threads == threads && cache[e].dev == dev)
+            return cache[e].cap;
+    int nsm = 0, per_sm = 0;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0) != cudaSuccess || per_sm < 1)
+        per_sm = 4;
+    const char *env = getenv("SSN_CHAIN_WAVES");
+    int waves = env ? atoi(env) : 8;
+    if (waves < 1) waves = 1;
+    const u64 cap = (u64)nsm * per_sm * waves;
+    if (used < 32) cache[used++] = Entry{(const void *)kern, threads, dev, cap};
+    return cap;
+}
+
+// the kernel launches of one chain (HF: host-fed reference-stream masks)
+template <int K, int N, bool HF>
+int launch_kernels(const ChainArgs &a, const STables<K, N> &tb, const SsnField &f, const ssn_chain_desc *d,
+                   cudaStream_t st) {
+    if (!d->nonlin) {
+        u64 blocks = (a.nel + PLAIN_THREADS - 1) / PLAIN_THREADS;
+        const u64 cap = chain_grid_cap(k_chain_plain<K, N, HF>, PLAIN_THREADS);
+        if (blocks > cap) blocks = cap;
+        SSN_COUNT_LAUNCH();
+        k_chain_plain<K, N, HF><<<(unsigned)blocks, PLAIN_THREADS, 0, st>>>(a, tb, f);
+    } else {
+        const u64 n_out = (u64)d->nb * d->c * (d->h / d->kh) * (d->w / d->kw);
+        u64 blocks = (n_out + CHAIN_THREADS * WPT - 1) / (CHAIN_THREADS * WPT);
+        const u64 cap = d->scratch || d->nonlin_only ? chain_grid_cap(k_chain_nonlin<K, N, true, HF>, CHAIN_THREADS)
+                                                     : chain_grid_cap(k_chain_nonlin<K, N, false, HF>, CHAIN_THREADS);
+        if (blocks > cap) blocks = cap;
+        if (blocks < 1) blocks = 1;
+        if (d->nonlin_only) {
+            // a standalone masked nonlinearity: acc holds the n parties' input shares
+            SSN_COUNT_LAUNCH();
+            k_chain_nonlin<K, N, true, HF><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a, tb, f);
+        } else if (d->scratch) {
+            // split: reshare + truncation (+ add) into scratch [n][nel], then the nonlinearity
+            ChainArgs a1 = a;
+            a1.out = d->scratch;
+            a1.out_ps = a.nel;
+            a1.planes = nullptr;
+            u64 b1 = (a.nel + PLAIN_THREADS - 1) / PLAIN_THREADS;
+            const u64 cap1 = chain_grid_cap(k_chain_plain<K, N, HF>, PLAIN_THREADS);
+            if (b1 > cap1) b1 = cap1;
+            SSN_COUNT_LAUNCH();
+            k_chain_plain<K, N, HF><<<(unsigned)b1, PLAIN_THREADS, 0, st>>>(a1, tb, f);
+            ChainArgs a2 = a;
+            a2.acc = d->scratch;
+            a2.acc_ps = a.nel;
+            SSN_COUNT_LAUNCH();
+            k_chain_nonlin<K, N, true, HF><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a2, tb, f);
+        } else {
+            SSN_COUNT_LAUNCH();
+            k_chain_nonlin<K, N, false, HF><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a, tb, f);
+        }
     }
-    return (u64)cap;
+    return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
 
 template <int K, int N>
@@ -594,47 +691,26 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
     a.pl_copies = d->plane_copies;
     a.pl_nparty = d->plane_nparty;
     a.inv_table = (d->nonlin && d->inv_table && d->inv_table_len > d->bmax) ? d->inv_table : nullptr;
+    const bool hf = d->host_masks != 0;
+    a.h_zero = d->h_zero;
+    a.h_alpha = d->h_alpha;
+    a.h_comp = d->h_comp;
+    a.h_tcoef = d->h_tcoef;
+    a.h_beta = d->h_beta;
+    a.h_binv = d->h_binv;
+    a.per = d->h_period;
+    a.per_out = d->h_period_out;
+    if (hf) {
+        if (a.per < 1 || a.per >= (1ull << 32) || a.nel % a.per) return SSN_ERR_ARG;
+        if (!d->nonlin_only && (!a.h_zero || !a.h_alpha || !a.h_comp || (K > 1 && !a.h_tcoef))) return SSN_ERR_ARG;
+        if (d->nonlin && (!a.h_beta || !a.h_binv || a.per_out < 1 || a.per_out >= (1ull << 32))) return SSN_ERR_ARG;
+        a.f_per = make_fastdiv((uint32_t)a.per);
+        a.f_per_out = make_fastdiv((uint32_t)(a.per_out ? a.per_out : 1));
+        a.inv_table = nullptr;
+    }
     if (a.planes && (!d->nonlin || a.pl_copies < 1 || a.pl_nparty < 1 || a.pl_nparty > N)) return SSN_ERR_ARG;
     if (a.senders > a.nout) return SSN_ERR_ARG;
-    if (!d->nonlin) {
-        u64 blocks = (a.nel + PLAIN_THREADS - 1) / PLAIN_THREADS;
-        const u64 cap = chain_grid_cap(k_chain_plain<K, N>, PLAIN_THREADS);
-        if (blocks > cap) blocks = cap;
-        SSN_COUNT_LAUNCH();
-        k_chain_plain<K, N><<<(unsigned)blocks, PLAIN_THREADS, 0, st>>>(a, tb, f);
-    } else {
-        const u64 n_out = (u64)d->nb * d->c * (d->h / d->kh) * (d->w / d->kw);
-        u64 blocks = (n_out + CHAIN_THREADS * WPT - 1) / (CHAIN_THREADS * WPT);
-        const u64 cap = d->scratch || d->nonlin_only ? chain_grid_cap(k_chain_nonlin<K, N, true>, CHAIN_THREADS)
-                                                     : chain_grid_cap(k_chain_nonlin<K, N, false>, CHAIN_THREADS);
-        if (blocks > cap) blocks = cap;
-        if (blocks < 1) blocks = 1;
-        if (d->nonlin_only) {
-            // a standalone masked nonlinearity: acc holds the n parties' input shares
-            SSN_COUNT_LAUNCH();
-            k_chain_nonlin<K, N, true><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a, tb, f);
-        } else if (d->scratch) {
-            // split: reshare + truncation (+ add) into scratch [n][nel], then the nonlinearity
-            ChainArgs a1 = a;
-            a1.out = d->scratch;
-            a1.out_ps = a.nel;
-            a1.planes = nullptr;
-            u64 b1 = (a.nel + PLAIN_THREADS - 1) / PLAIN_THREADS;
-            const u64 cap1 = chain_grid_cap(k_chain_plain<K, N>, PLAIN_THREADS);
-            if (b1 > cap1) b1 = cap1;
-            SSN_COUNT_LAUNCH();
-            k_chain_plain<K, N><<<(unsigned)b1, PLAIN_THREADS, 0, st>>>(a1, tb, f);
-            ChainArgs a2 = a;
-            a2.acc = d->scratch;
-            a2.acc_ps = a.nel;
-            SSN_COUNT_LAUNCH();
-            k_chain_nonlin<K, N, true><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a2, tb, f);
-        } else {
-            SSN_COUNT_LAUNCH();
-            k_chain_nonlin<K, N, false><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a, tb, f);
-        }
-    }
-    return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
+    return hf ? launch_kernels<K, N, true>(a, tb, f, d, st) : launch_kernels<K, N, false>(a, tb, f, d, st);
 }
 
 template <int K, int N>

@@ -8,10 +8,13 @@ transport implements the same duck-typed seam as DeviceTransport / the reference
 FIFO per (src, dst) channel, phase-checked (ScheduleDivergence on mismatch), with
 CommMetrics fed the reference's element and frame-byte counts.
 
-Backends:
-  * "nccl" -- device tensors go straight over NVLink (ncclSend / ncclRecv);
-  * "gloo" -- tensors are staged through host memory (CPU tests, and several ranks sharing one
-    GPU on a single-GPU box).
+Backends: the seam is one blocking, addressed message at a time, and a party sends to several
+peers before it receives (reshare step 1: fronts 1 and 2 each send to the other first).  NCCL
+pairs a send and a recv between two peers on one stream, so two large ungrouped sends facing
+each other wait on each other forever.  This transport therefore always moves its messages over
+a gloo group (host-staged); under an NCCL default group run_party_dist creates that gloo group
+for it.  The NVLink throughput path is PartyShardedEngine (sharded.py), which issues every
+protocol hop as ONE grouped batch_isend_irecv (ncclGroupStart/ncclSend/ncclRecv/ncclGroupEnd).
 Every message is a fixed 16-word int64 header followed by the payload (u64 share/plaintext
 values, or the u8 bytes of a serialized MaskBundle).
 """
@@ -47,11 +50,16 @@ class DistTransport:
     """Transport for rank `rank` of a torch.distributed world whose ranks ARE the protocol
     ranks.  `device` is where received tensors land (a CUDA device for the product path)."""
 
-    def __init__(self, rank, device, metrics=None, record=False, decode_object=None):
+    def __init__(self, rank, device, metrics=None, record=False, decode_object=None, group=None):
         self.rank = rank
         self.device = torch.device(device)
         self.metrics = metrics
-        self.backend = dist.get_backend()
+        self.group = group
+        self.backend = dist.get_backend(group)
+        if self.backend == "nccl":
+            raise ValueError("DistTransport needs a gloo group: ungrouped NCCL sends between two parties that "
+                             "both send first deadlock (pass group=dist.new_group(backend='gloo'); the NCCL "
+                             "path is PartyShardedEngine)")
         self.record = record
         self.frames = {}             # (src, dst) -> [frame bytes]  (sent frames, when recording)
         self.decode_object = decode_object
@@ -59,16 +67,16 @@ class DistTransport:
 
     # -- wire helpers
     def _comm_device(self):
-        return self.device if self.backend == "nccl" else torch.device("cpu")
+        return torch.device("cpu")
 
     def _send_tensor(self, t, dst):
         # Non-blocking: every party sends to several peers before it receives (e.g. reshare
         # step 1), so a blocking send would deadlock two parties sending to each other.
         # Per-(src, dst) FIFO order is preserved by the backend.
         t = t.contiguous()
-        if self.backend != "nccl" and t.device.type != "cpu":
+        if t.device.type != "cpu":
             t = t.cpu()
-        self._pending.append((dist.isend(t, dst), t))
+        self._pending.append((dist.isend(t, dst, group=self.group), t))
         if len(self._pending) > 64:
             self._reap()
 
@@ -82,7 +90,7 @@ class DistTransport:
 
     def _recv_tensor(self, shape, dtype, src):
         t = torch.empty(shape, dtype=dtype, device=self._comm_device())
-        dist.recv(t, src)
+        dist.recv(t, src, group=self.group)
         return t
 
     def _send(self, dst, hdr, payload, elements, nbytes, frame=None):
@@ -198,7 +206,9 @@ def run_party_dist(model, scheme, seed, input_int, device, ordering="ltn", rng_m
         raise ValueError(f"world size {dist.get_world_size()} != n + 1 = {scheme.n + 1}")
     metrics = metrics if metrics is not None else CommMetrics()
     ops, _ = plan_schedule(model, scheme, ordering, verify=verify)
-    tr = DistTransport(rank, device, metrics, record=record, decode_object=mask_bundle_decoder(scheme, device))
+    group = dist.new_group(backend="gloo") if dist.get_backend() == "nccl" else None   # collective
+    tr = DistTransport(rank, device, metrics, record=record, decode_object=mask_bundle_decoder(scheme, device),
+                       group=group)
     if rank == 0:
         send_bundles(tr, ops, scheme, seed, metrics, rng_mode)
         tr.close()

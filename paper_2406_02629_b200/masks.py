@@ -54,7 +54,7 @@ def gen_additive_mask(shape, r: int, divisor: int, scheme, rng, value_bound: int
         n = int(np.prod(shape)) if shape else 1
         alpha = torch.empty((scheme.n,) + shape, dtype=torch.int64, device=device())
         comp = torch.empty_like(alpha)
-        _lib.call("ssn_mask_trunc", n, step, emax, rng.seed, rng.next_stream(), scheme.k - 1,
+        _lib.call("ssn_mask_trunc", n, step, emax, rng.seed, rng.next_stream(3), scheme.k - 1,
                   _lib.u64_array(scheme.party_ids), scheme.n, _lib.ptr(alpha), _lib.ptr(comp), n, f.p,
                   _lib.stream_ptr())
         return _wrap(alpha, scheme), _wrap(comp, scheme), None
@@ -88,7 +88,7 @@ def gen_multiplicative_mask(shape, scheme, rng, pool=None, value_bound: int = (1
             nb, c, h, w = 1, int(np.prod(shape)) if shape else 1, 1, 1
         beta = torch.empty((scheme.n,) + shape, dtype=torch.int64, device=device())
         binv = torch.empty((scheme.n,) + out_shape, dtype=torch.int64, device=device())
-        _lib.call("ssn_mask_beta", nb, c, h, w, kh, kw, bmax, rng.seed, rng.next_stream(2), scheme.k - 1,
+        _lib.call("ssn_mask_beta", nb, c, h, w, kh, kw, bmax, rng.seed, rng.next_stream(3), scheme.k - 1,
                   _lib.u64_array(scheme.party_ids), scheme.n, _lib.ptr(beta), beta[0].numel(),
                   _lib.ptr(binv), binv[0].numel(), f.p, _lib.stream_ptr())
         return _wrap(beta, scheme), _wrap(binv, scheme), None

@@ -164,7 +164,7 @@ class PartyShardedEngine:
                 emax = additive_mask_bound(self.scheme.field, step, op.value_bound)
                 A = torch.empty((n, N), dtype=torch.int64, device=self.dev)
                 C = torch.empty((n, N), dtype=torch.int64, device=self.dev)
-                _lib.call("ssn_mask_trunc", N, step, emax, rng.seed, rng.next_stream(), k - 1, self.ids_all, n,
+                _lib.call("ssn_mask_trunc", N, step, emax, rng.seed, rng.next_stream(3), k - 1, self.ids_all, n,
                           _lib.ptr(A), _lib.ptr(C), N, p, _lib.stream_ptr())
                 rows = [A, C]
             elif op.kind == "nonlinear":
@@ -173,7 +173,7 @@ class PartyShardedEngine:
                 bmax = multiplicative_mask_bound(self.scheme.field, op.value_bound)
                 BETA = torch.empty((n, n_in), dtype=torch.int64, device=self.dev)
                 BINV = torch.empty((n, n_out), dtype=torch.int64, device=self.dev)
-                _lib.call("ssn_mask_beta", B, c, h, w, kh, kw, bmax, rng.seed, rng.next_stream(2), k - 1,
+                _lib.call("ssn_mask_beta", B, c, h, w, kh, kw, bmax, rng.seed, rng.next_stream(3), k - 1,
                           self.ids_all, n, _lib.ptr(BETA), n_in, _lib.ptr(BINV), n_out, p, _lib.stream_ptr())
                 rows = [BETA, BINV]
             else:
