@@ -19,8 +19,13 @@ Per op (reference in parentheses, paths relative to /root/reference/pkg/src/ssne
   output      rec at the elite + decode (S/protocol.py:289-305)                    ssn_rec, ssn_decode_signed
 Masks come from a device-side trusted source, generated per op just before use
 (S/protocol.py:354-388, S/masks.py): ssn_gen (zero), ssn_mask_trunc, ssn_mask_beta.
-Randomness is device Philox (rng_mode="device"); decoded outputs are RNG-independent, so
-they equal the reference / plaintext exactly (tests/test_gpu_batched.py).
+Randomness: rng_mode="device" (speed mode, the bench) draws everything from device Philox;
+decoded outputs are RNG-independent, so they equal the reference / plaintext exactly.
+rng_mode="host" is the reference-stream parity mode: weight shares (lane 1), input shares
+(lane 3, input_index = image position), the trusted source's bundle (lane 4) and the elite's
+truncation coefficients (lane 5, rank 1) are drawn with the reference's numpy calls and fed to
+the SAME kernels (ssn_chain.cu HF instantiations), so every party's share of every op output
+equals the reference's run of that image bit for bit (tests/test_gpu_parity_batched.py).
 """
 
 import ctypes
@@ -49,9 +54,11 @@ def _count(shape):
 class BatchedEngine:
     def __init__(self, model, scheme, batch, seed=7, rng_mode="device", verify=False, ordering="ltn",
                  profile=False, fuse=True, share_weights_with=None, implicit=True):
-        if rng_mode != "device":
-            raise ValueError("the batched engine draws its randomness on the device (rng_mode='device'); "
-                             "use simulate_inference for reference-stream parity runs")
+        if rng_mode not in ("device", "host"):
+            raise ValueError(f"unknown rng mode {rng_mode!r}")
+        self.host = rng_mode == "host"
+        if self.host and share_weights_with is not None:
+            raise ValueError("reference-stream mode deals its own weight shares")
         self.model = model
         self.scheme = scheme
         self.batch = int(batch)
@@ -77,7 +84,8 @@ class BatchedEngine:
             self.W, self._planes = share_weights_with.W, share_weights_with._planes
         else:
             self._planes = {}
-            self._deal_weights()
+            self._deal_weights_host() if self.host else self._deal_weights()
+        self.hm = self._host_source() if self.host else None
         self.kernel_launches = 0
         self.fault = None
         self.fuse = fuse
@@ -107,6 +115,49 @@ class BatchedEngine:
             _lib.call("ssn_gen", _lib.ptr(enc), 0, None, 0, rng.seed, rng.next_stream(), self.k - 1, self.ids_all,
                       self.n, _lib.ptr(out), 0, nel, nel, 1, self.p, _lib.stream_ptr())
             self.W[name] = out
+
+    def _deal_weights_host(self):
+        """Reference-stream weight shares: lane 1, sorted names (S/engine.py:40-49)."""
+        from .engine import deal_weight_shares
+        values = self.model.weight_values() if hasattr(self.model, "weight_values") else \
+            {name: qt.values for name, qt in self.model.weights.items()}
+        per_rank = deal_weight_shares(values, self.scheme, self.seed, "host")
+        self.W = {name: torch.stack([per_rank[r][name].values for r in range(1, self.n + 1)]).contiguous()
+                  for name in sorted(values)}
+
+    def _host_source(self):
+        """Reference-stream trusted-source material, drawn once (the reference deals the same
+        bundle and the same party streams for every input_index, S/engine.py:64-74,166-171):
+          (idx, name) -> [n][numel]  shares of zero / alpha / comp / beta / beta_inv
+                         (trusted_source_prepare on lane 4, S/protocol.py:354-388);
+          (idx, "tcoef") -> [k-1][numel] the elite's fresh truncation coefficients: rank 1's
+                         PURPOSE_PARTY stream replayed -- each linear op first draws its reshare
+                         sub-share coefficients (S/protocol.py:158, values never matter), each
+                         truncation then its k-1 coefficient tensors (S/layers.py:308)."""
+        from .engine import PURPOSE_MASKS, PURPOSE_PARTY, seeded_rng
+        from .protocol import trusted_source_prepare
+        n, k, p = self.n, self.k, self.p
+        bundles, _ = trusted_source_prepare(self.ops, self.scheme, seeded_rng(self.seed, PURPOSE_MASKS))
+        hm = {key: torch.stack([bundles[r].entries[key].values.reshape(-1) for r in range(1, n + 1)]).contiguous()
+              for key in bundles[1].entries}
+        rng = seeded_rng(self.seed, PURPOSE_PARTY, 1)
+        for idx, op in enumerate(self.ops):
+            if k == 1:
+                break
+            if op.kind == "linear":
+                for _ in range(k - 1):
+                    rng.integers(0, p, size=_count(op.out_shape), dtype=np.int64)
+            elif op.kind == "truncation":
+                draws = np.stack([rng.integers(0, p, size=_count(op.in_shape), dtype=np.int64) for _ in range(k - 1)])
+                hm[(idx, "tcoef")] = torch.as_tensor(draws, device=self.dev).contiguous()
+        return hm
+
+    def _hb(self, idx, name):
+        """Host-fed material of op idx broadcast over the batch: [rows][B * numel] (the
+        unfused kernels index the batch directly)."""
+        t = self.hm[(idx, name)]
+        return t.view(t.shape[0], 1, -1).expand(t.shape[0], self.batch, t.shape[1]).reshape(t.shape[0], -1) \
+            .contiguous()
 
     def _encode(self, v):
         out = torch.empty_like(v)
@@ -300,6 +351,19 @@ class BatchedEngine:
         d.ids, d.rt = ctypes.addressof(self.ids_all), ctypes.addressof(self._rt_all)
         d.ext = ctypes.addressof(self._ext_host) if self._ext_host is not None else None
         d.p = p
+        if self.host:
+            hm = self.hm
+            d.host_masks = 1
+            d.h_zero = hm[(chain[0], "zero")].data_ptr()
+            d.h_alpha = hm[(chain[1], "alpha")].data_ptr()
+            d.h_comp = hm[(chain[1], "comp")].data_ptr()
+            d.h_tcoef = hm[(chain[1], "tcoef")].data_ptr() if k > 1 else None
+            d.h_period = _count(lin.out_shape)
+            if nl is not None:
+                nidx = next(i for i in chain[2:] if self.ops[i].kind == "nonlinear")
+                d.h_beta = hm[(nidx, "beta")].data_ptr()
+                d.h_binv = hm[(nidx, "beta_inv")].data_ptr()
+                d.h_period_out = _count(last.out_shape)
         shift = None
         ps = self._plane_src.get(chain[-1])
         if ps is not None and nl is not None and self.chain_planes and tuple(last.out_shape) == tuple(ps[3:]):
@@ -432,7 +496,11 @@ class BatchedEngine:
         _lib.call("ssn_decode_signed", _lib.ptr(v), _lib.ptr(out), N, self.p, _lib.stream_ptr())
         return out.reshape((self.batch,) + tuple(shape)).cpu().numpy()
 
-    def run_device(self, x_int, timings=None, capture=None):
+    def run_device(self, x_int, timings=None, capture=None, capture_shares=None, input_indices=None):
+        """capture: {idx: decoded op output} (test helper); capture_shares: {idx: [n][B][...]
+        every party's share of each materialised op output (fused chains: the chain's last op;
+        the output op: its input shares)}; input_indices: the reference input_index of each
+        image for the reference-stream input shares (default 0..B-1)."""
         B, n, k, m, p = self.batch, self.n, self.k, self.m, self.p
         run_id = self.runs
         self.runs += 1
@@ -454,12 +522,20 @@ class BatchedEngine:
 
         mark("start")
         # input dealing (S/engine.py:52-54), lane 3
-        enc = self._encode(x)
-        X = torch.empty((n,) + tuple(x.shape), dtype=torch.int64, device=self.dev)
-        irng = DeviceRng(self.seed, 3, run_id)
-        nel = x.numel()
-        _lib.call("ssn_gen", _lib.ptr(enc), 0, None, 0, irng.seed, irng.next_stream(), k - 1, self.ids_all, n,
-                  _lib.ptr(X), 0, nel, nel, 1, p, _lib.stream_ptr())
+        if self.host:
+            from .engine import deal_input_shares
+            idxs = list(range(B)) if input_indices is None else [int(i) for i in input_indices]
+            xh = x.cpu().numpy()
+            X = torch.stack([torch.stack([st.values for st in deal_input_shares(xh[b], self.scheme, self.seed, idxs[b],
+                                                                                  "host")])
+                             for b in range(B)], dim=1).contiguous()
+        else:
+            enc = self._encode(x)
+            X = torch.empty((n,) + tuple(x.shape), dtype=torch.int64, device=self.dev)
+            irng = DeviceRng(self.seed, 3, run_id)
+            nel = x.numel()
+            _lib.call("ssn_gen", _lib.ptr(enc), 0, None, 0, irng.seed, irng.next_stream(), k - 1, self.ids_all, n,
+                      _lib.ptr(X), 0, nel, nel, 1, p, _lib.stream_ptr())
         vals = {-1: X}
         masked_for = {}          # linear idx -> True when its output already carries alpha
         remaining = {i: len(c) for i, c in self.cons.items()}
@@ -489,12 +565,16 @@ class BatchedEngine:
                 y = torch.empty((n, B) + tuple(op.out_shape), dtype=torch.int64, device=self.dev)
                 self._ew(0, xin, other, y, n * nn)
             elif op.kind == "output":
+                if capture_shares is not None:
+                    capture_shares[idx] = xin.clone()
                 result = self._output(op, xin)
                 y = None
             else:
                 raise ValueError(op.kind)
             if y is not None:
                 vals[idx] = y
+                if capture_shares is not None and not masked_for.get(idx, False):   # not: y + next alpha
+                    capture_shares[idx] = y.clone()
             if self.fault is not None and self.fault[0] == idx and y is not None and not self.chains:
                 y[self.fault[1]].view(-1)[0] += 1              # test hook: corrupt one share
             if capture is not None and y is not None and op.kind != "linear" and idx not in self.chains:
@@ -556,9 +636,12 @@ class BatchedEngine:
         N = B * O * ohw
         nout = n if op.passive_out else k
         # source: zero shares for every rank (gen_zero_shares)
-        Z = torch.empty((n, N), dtype=torch.int64, device=self.dev)
-        _lib.call("ssn_gen", None, 0, None, 0, src_rng.seed, src_rng.next_stream(), k - 1, self.ids_all, n,
-                  _lib.ptr(Z), 0, N, N, 1, p, _lib.stream_ptr())
+        if self.host:
+            Z = self._hb(idx, "zero")
+        else:
+            Z = torch.empty((n, N), dtype=torch.int64, device=self.dev)
+            _lib.call("ssn_gen", None, 0, None, 0, src_rng.seed, src_rng.next_stream(), k - 1, self.ids_all, n,
+                      _lib.ptr(Z), 0, N, N, 1, p, _lib.stream_ptr())
         # fuse the next truncation's alpha into step 3 when the truncation is the sole consumer
         nxt = self.cons[idx]
         alpha = None
@@ -594,6 +677,9 @@ class BatchedEngine:
         N = B * _count(op.in_shape)
         step = op.r * op.divisor
         emax = additive_mask_bound(self.scheme.field, step, op.value_bound)
+        if self.host:
+            got = self._mask_cache[idx] = (self._hb(idx, "alpha"), self._hb(idx, "comp"))
+            return got
         A = torch.empty((n, N), dtype=torch.int64, device=self.dev)
         Cm = torch.empty((n, N), dtype=torch.int64, device=self.dev)
         _lib.call("ssn_mask_trunc", N, step, emax, src_rng.seed, src_rng.next_stream(3), self.k - 1, self.ids_all, n,
@@ -614,8 +700,9 @@ class BatchedEngine:
             masked = torch.empty((senders, N), dtype=torch.int64, device=self.dev)
             self._ew(0, X, A, masked, senders * N)
         FR = torch.empty((n, N), dtype=torch.int64, device=self.dev)
+        tco = self._hb(idx, "tcoef") if (self.host and k > 1) else None
         _lib.call("ssn_trunc_elite", _lib.ptr(masked), N, senders, k, _lib.u64_array(self.w_front),
-                  _lib.u64_array(self.ext), op.value_bound, op.r, op.divisor, None, party_rng.seed,
+                  _lib.u64_array(self.ext), op.value_bound, op.r, op.divisor, _lib.ptr(tco), party_rng.seed,
                   party_rng.next_stream(), k - 1, self.ids_all, n, _lib.ptr(FR), N,
                   _lib.ptr(self.fail) if self.verify else None, N, p, _lib.stream_ptr())
         Y = torch.empty((n, B) + tuple(op.out_shape), dtype=torch.int64, device=self.dev)
@@ -652,6 +739,11 @@ class BatchedEngine:
         d.ext = ctypes.addressof(self._ext_host) if self._ext_host is not None else None
         d.p = p
         d.fault_rank = -1
+        if self.host:
+            d.host_masks = 1
+            d.h_beta = self.hm[(idx, "beta")].data_ptr()
+            d.h_binv = self.hm[(idx, "beta_inv")].data_ptr()
+            d.h_period, d.h_period_out = _count(op.in_shape), _count(op.out_shape)
         _lib.call("ssn_layer_chain", ctypes.byref(d), _lib.stream_ptr())
         self.kernel_launches += 1
         return Y
@@ -668,10 +760,13 @@ class BatchedEngine:
         else:
             c, h, w, kh, kw, kind = _count(op.in_shape), 1, 1, 1, 1, 0
         bmax = multiplicative_mask_bound(self.scheme.field, op.value_bound)
-        BETA = torch.empty((n, n_in), dtype=torch.int64, device=self.dev)
-        BINV = torch.empty((n, n_out), dtype=torch.int64, device=self.dev)
-        _lib.call("ssn_mask_beta", B, c, h, w, kh, kw, bmax, src_rng.seed, src_rng.next_stream(3), k - 1,
-                  self.ids_all, n, _lib.ptr(BETA), n_in, _lib.ptr(BINV), n_out, p, _lib.stream_ptr())
+        if self.host:
+            BETA, BINV = self._hb(idx, "beta"), self._hb(idx, "beta_inv")
+        else:
+            BETA = torch.empty((n, n_in), dtype=torch.int64, device=self.dev)
+            BINV = torch.empty((n, n_out), dtype=torch.int64, device=self.dev)
+            _lib.call("ssn_mask_beta", B, c, h, w, kh, kw, bmax, src_rng.seed, src_rng.next_stream(3), k - 1,
+                      self.ids_all, n, _lib.ptr(BETA), n_in, _lib.ptr(BINV), n_out, p, _lib.stream_ptr())
         MASKED = torch.empty((m, n_in), dtype=torch.int64, device=self.dev)
         self._ew(2, X, BETA, MASKED, m * n_in)
         plain = torch.empty(n_out, dtype=torch.int64, device=self.dev)
@@ -727,6 +822,8 @@ class StreamPipelinedEngine:
         if batch % streams:
             raise ValueError(f"batch {batch} not divisible by {streams} streams")
         self.batch, self.nstreams = batch, streams
+        if kw.get("rng_mode", "device") != "device":
+            raise ValueError("the stream-pipelined engine runs in speed mode (device randomness)")
         first = BatchedEngine(model, scheme, batch // streams, seed=seed, verify=verify, **kw)
         self.engines = [first] + [BatchedEngine(model, scheme, batch // streams, seed=seed + 1000 * i, verify=verify,
                                                 share_weights_with=first, **kw) for i in range(1, streams)]
