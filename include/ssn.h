@@ -124,6 +124,14 @@ int ssn_mask_beta(int nb, int c, int h, int wd, int kh, int kw, uint64_t bmax, u
                   int km1, const uint64_t *ids, int nids, uint64_t *beta, uint64_t beta_tstride, uint64_t *binv,
                   uint64_t binv_tstride, uint64_t p, void *strm);
 
+/* Overlapping-window gather of share tensors (builder op "gather"; e.g. ResNet's 3x3/s2/p1 stem
+ * max-pool as the reference's non-overlapping pool over gathered windows, S/model.py:374-377):
+ * x [nb][c][h][w] -> out [nb][c][OH*kh][OW*kw], OH = (h + 2 pad - kh) / stride + 1, with
+ * out[.., oy*kh + dy, ox*kw + dx] = x[.., oy*stride - pad + dy, ox*stride - pad + dx] or 0 (a
+ * valid share of 0) outside.  Local: every party gathers its own share. */
+int ssn_window_gather(const uint64_t *x, uint64_t *out, int nb, int c, int h, int w, int kh, int kw, int stride,
+                      int pad, void *strm);
+
 /* Repeat a (nb, c, h/kh, wd/kw) block over windows (np.repeat twice, S/masks.py:84). */
 int ssn_pool_expand(const uint64_t *blk, uint64_t *out, int nb, int c, int h, int wd, int kh, int kw, void *strm);
 
@@ -245,6 +253,12 @@ typedef struct ssn_chain_desc {
     int host_masks;
     const uint64_t *h_zero, *h_alpha, *h_comp, *h_tcoef, *h_beta, *h_binv;
     uint64_t h_period, h_period_out;
+    uint64_t h_period_in;   /* beta shares per image (0: h_period); the gathered size with gather */
+    /* 1: an overlapping-window gather (ssn_window_gather, builder op "gather") sits between the
+     * chain output (nb, c, gather_h, gather_w) and the nonlinearity, whose (c, h, w) input is
+     * the gathered (c, OH*kh, OW*kw) tensor: window (y0, x0) tap (wy, wx) reads source
+     * (y0*stride - pad + wy, x0*stride - pad + wx), zero outside.  Needs the split form. */
+    int gather, gather_h, gather_w, gather_stride, gather_pad;
 } ssn_chain_desc;
 
 int ssn_layer_chain(const ssn_chain_desc *desc, void *stream);

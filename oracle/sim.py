@@ -16,6 +16,9 @@ Schedule ops are the reference's ScheduledOp.meta() dicts (S/layers.py:63-73).
 Two builder extensions, used by the ResNet models and marked as such:
   * "src"/"src2": producer op index (-1 = model input); default = previous op.
   * kind "add": local share_add of two degree-(k-1) shares (S/sss.py:238).
+  * kind "gather": local overlapping-window gather of every party's share (zero fill), so the
+    following reference nonlinear op's non-overlapping pool is an overlapping pool (ResNet's
+    3x3/s2/p1 stem max-pool).  Fields: pool = (kh, kw), stride, padding.
   * verify=True: masked-value Reed-Solomon check at the truncation elite and
     at output collection; never changes outputs.
 """
@@ -28,7 +31,7 @@ import numpy as np
 
 from . import (DEFAULT_PRIME, decode_signed, encode_signed, ewise, gemm, gen, im2col,
                lagrange_weights, nonlin_elite, reducing_matrix, rec, reduce_apply,
-               trunc_elite)
+               trunc_elite, window_gather)
 
 # Phase tags (S/wire.py:32-41)
 MASK_DIST, SHARE_DIST, RESHARE_OUT, RESHARE_BACK = 2, 3, 4, 5
@@ -176,7 +179,7 @@ def source_masks(ops, sch, rng, record_plain=False):
             spread(idx, "beta", sch.share(beta.astype(np.uint64), rng))
             spread(idx, "beta_inv", sch.share(beta_inv, rng))
             plain[idx] = {"beta": beta}
-        elif kind in ("output", "add"):
+        elif kind in ("output", "add", "gather"):
             pass
         else:
             raise ValueError(f"unknown op kind {kind!r}")
@@ -338,6 +341,11 @@ def simulate(ops, sch, seed, input_int, weight_values, input_index=0, record=Fal
             for r in range(1, n + 1):
                 if r in x and r in y:
                     res[r] = (x[r][0], ewise("add", x[r][1], y[r][1], p))
+        elif kind == "gather":
+            kh, kw = op["pool"]
+            for r, (deg, xv) in x.items():
+                res[r] = (deg, window_gather(np.asarray(xv).reshape(tuple(op["in_shape"])), kh, kw,
+                                             op["stride"], op["padding"]))
         elif kind == "output":
             senders = range(2, (n if verify else k) + 1)
             for r in senders:
@@ -412,6 +420,9 @@ def plaintext(ops, input_int, weight_values, threads=0):
                 y = blk.max(axis=(2, 4)) if op["pool_kind"] == "max" else blk.sum(axis=(2, 4))
         elif kind == "add":
             y = x + vals[_src(op, idx, "src2")]
+        elif kind == "gather":
+            kh, kw = op["pool"]
+            y = window_gather(x.reshape(tuple(op["in_shape"])), kh, kw, op["stride"], op["padding"])
         elif kind == "output":
             out = x
             y = x

@@ -66,6 +66,7 @@ _SIGS = {
     "ssn_mask_trunc": [_U64, _U64, _U64, _U64, _U64, _I32, _P, _I32, _P, _P, _U64, _U64, _P],
     "ssn_mask_beta": [_I32, _I32, _I32, _I32, _I32, _I32, _U64, _U64, _U64, _I32, _P, _I32, _P, _U64, _P,
                       _U64, _U64, _P],
+    "ssn_window_gather": [_P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P],
     "ssn_pool_expand": [_P, _P, _I32, _I32, _I32, _I32, _I32, _I32, _P],
     "ssn_conv_simt": [_P, _U64, _P, _U64, _P, _U64, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _I32,
                       _I32, _U64, _P],
@@ -112,6 +113,8 @@ class ChainDesc(ctypes.Structure):
         ("host_masks", _I32),
         ("h_zero", _P), ("h_alpha", _P), ("h_comp", _P), ("h_tcoef", _P), ("h_beta", _P), ("h_binv", _P),
         ("h_period", _U64), ("h_period_out", _U64),
+        ("h_period_in", _U64),
+        ("gather", _I32), ("gather_h", _I32), ("gather_w", _I32), ("gather_stride", _I32), ("gather_pad", _I32),
     ]
 
 _lib = None

@@ -16,6 +16,7 @@ Per op (reference in parentheses, paths relative to /root/reference/pkg/src/ssne
               elite rec / decode / ReLU / pool / encode (S/layers.py:345-364)      ssn_nonlin_elite
               plain * beta^-1 at the receivers (S/layers.py:379-380)                ssn_ewise (broadcast)
   add         local share add (residual, S/sss.py:238)                             ssn_ewise
+  gather      local overlapping-window gather (builder op; 3x3/s2 stem pool)       ssn_window_gather
   output      rec at the elite + decode (S/protocol.py:289-305)                    ssn_rec, ssn_decode_signed
 Masks come from a device-side trusted source, generated per op just before use
 (S/protocol.py:354-388, S/masks.py): ssn_gen (zero), ssn_mask_trunc, ssn_mask_beta.
@@ -38,7 +39,7 @@ import torch
 from . import _lib
 from . import gemm as gemm_mod
 from .gemm import field_conv, field_dense
-from .layers import comm_estimate, consumers, plan_schedule
+from .layers import comm_estimate, consumers, plan_schedule, window_gather
 from .masks import additive_mask_bound, multiplicative_mask_bound
 from .protocol import VerificationError, extrapolation_coeffs
 from .rng import DeviceRng
@@ -278,8 +279,8 @@ class BatchedEngine:
         return s
 
     def _plan_chains(self):
-        """Group linear -> truncation [-> add] [-> nonlinear] runs whose intermediates have a
-        single consumer into one fused protocol launch (csrc/ssn_chain.cu)."""
+        """Group linear -> truncation [-> add] [-> gather] [-> nonlinear] runs whose intermediates
+        have a single consumer into one fused protocol launch (csrc/ssn_chain.cu)."""
         if (self.k, self.n) not in self.CHAIN_SCHEMES:
             return {}
         if not _lib.load(require_cuda=False).ssn_chain_supported(self.k, self.n, self.ids_all, self.p):
@@ -300,6 +301,12 @@ class BatchedEngine:
                     chain.append(a)
                     cur = a
                     nxt = cons.get(cur, [])
+            if (len(nxt) == 1 and ops[nxt[0]].kind == "gather" and len(cons.get(nxt[0], [])) == 1
+                    and ops[cons[nxt[0]][0]].kind == "nonlinear" and ops[cons[nxt[0]][0]].pool is not None):
+                g = nxt[0]
+                chain.append(g)
+                cur = g
+                nxt = cons.get(cur, [])
             if len(nxt) == 1 and ops[nxt[0]].kind == "nonlinear" and self._srcs(nxt[0]) == [cur]:
                 chain.append(nxt[0])
             chains[idx] = chain
@@ -312,6 +319,7 @@ class BatchedEngine:
         lin, tr = self.ops[chain[0]], self.ops[chain[1]]
         add = next((self.ops[i] for i in chain[2:] if self.ops[i].kind == "add"), None)
         nl = next((self.ops[i] for i in chain[2:] if self.ops[i].kind == "nonlinear"), None)
+        gat = next((self.ops[i] for i in chain[2:] if self.ops[i].kind == "gather"), None)
         last = self.ops[chain[-1]]
         O = lin.out_shape[0]
         ohw = _count(lin.out_shape[1:]) if len(lin.out_shape) > 1 else 1
@@ -342,6 +350,9 @@ class BatchedEngine:
                 c, h, w, kh, kw, kind = _count(nl.in_shape), 1, 1, 1, 1, 0
             d.nonlin, d.relu, d.pool_kind = 1, int(bool(nl.relu)), kind
             d.nb, d.c, d.h, d.w, d.kh, d.kw = B, c, h, w, kh, kw
+            if gat is not None:
+                d.gather, d.gather_h, d.gather_w = 1, gat.in_shape[1], gat.in_shape[2]
+                d.gather_stride, d.gather_pad = gat.stride, gat.padding
             d.fan = n if nl.passive_out else k
             d.bmax = multiplicative_mask_bound(self.scheme.field, nl.value_bound)
             tab = self._inv_table(d.bmax)
@@ -364,6 +375,7 @@ class BatchedEngine:
                 d.h_beta = hm[(nidx, "beta")].data_ptr()
                 d.h_binv = hm[(nidx, "beta_inv")].data_ptr()
                 d.h_period_out = _count(last.out_shape)
+                d.h_period_in = _count(nl.in_shape)
         shift = None
         ps = self._plane_src.get(chain[-1])
         if ps is not None and nl is not None and self.chain_planes and tuple(last.out_shape) == tuple(ps[3:]):
@@ -382,7 +394,7 @@ class BatchedEngine:
         nbytes = 8 * m * nel + (8 * n * nel if add is not None else 0)
         nbytes += 8 * (d.fan * n_out if nl is not None else n * nel)
         return {"d": d, "lin": lin, "last": last, "other": other, "nl": nl is not None, "nel": nel,
-                "shift": shift, "planes": bool(d.planes), "nbytes": nbytes}
+                "shift": shift, "planes": bool(d.planes), "nbytes": nbytes, "gather": gat is not None}
 
     def _chain(self, chain, vals, src_rng, party_rng):
         """One fused launch: reshare + rerand + bias + truncation [+ add] [+ nonlinear]."""
@@ -401,7 +413,7 @@ class BatchedEngine:
         d.src_seed, d.src_stream = src_rng.seed, src_rng.next_stream(7)
         d.fault_rank = self.fault[1] if (self.fault is not None and self.fault[0] == chain[0]) else -1
         scratch = None
-        if st["nl"] and self.split_chain:
+        if st["nl"] and (self.split_chain or st["gather"]):      # gathered windows read a scratch
             scratch = torch.empty((n, st["nel"]), dtype=torch.int64, device=self.dev)
             d.scratch = scratch.data_ptr()
         else:
@@ -564,6 +576,11 @@ class BatchedEngine:
                 nn = _count(op.out_shape) * B
                 y = torch.empty((n, B) + tuple(op.out_shape), dtype=torch.int64, device=self.dev)
                 self._ew(0, xin, other, y, n * nn)
+            elif op.kind == "gather":
+                kh, kw = op.pool
+                y = window_gather(xin, op.in_shape, kh, kw, op.stride, op.padding, nbatch=n * B) \
+                    .reshape((n, B) + tuple(op.out_shape))
+                self.kernel_launches += 1
             elif op.kind == "output":
                 if capture_shares is not None:
                     capture_shares[idx] = xin.clone()

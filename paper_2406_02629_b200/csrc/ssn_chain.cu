@@ -102,8 +102,13 @@ struct ChainArgs {
     //   h_zero / h_alpha / h_comp / h_beta [t*per + ii],  h_tcoef [e*per + ii] (the elite's fresh
     //   truncation coefficients, PURPOSE_PARTY lane), h_binv [t*per_out + oo]
     const u64 *h_zero, *h_alpha, *h_comp, *h_tcoef, *h_beta, *h_binv;
-    u64 per, per_out;
-    FastDiv f_per, f_per_out;
+    u64 per, per_out, per_in;      // per_in: nonlinear input elements per image (beta shares)
+    FastDiv f_per, f_per_out, f_per_in;
+    // overlapping-window gather before the nonlinearity (builder op "gather", e.g. the 3x3/s2/p1
+    // stem max-pool): the nonlinearity's (c, h, w) input is the gathered tensor whose window
+    // (y0, x0) element (wy, wx) is source element (y0*gs - gp + wy, x0*gs - gp + wx) of the
+    // (c, gh, gw) chain output, or a zero share outside it
+    int gather, gh, gw, gs, gp;
 };
 
 constexpr int CHAIN_THREADS = 128;
@@ -375,31 +380,45 @@ __global__ void __launch_bounds__(CHAIN_THREADS, 6) k_chain_nonlin(ChainArgs a, 
             if (o < n_out) {
                 if constexpr (!HF) bt = 1 + ssn_rand_range(a.sseed, a.sstream + 4, o, 0, a.bmax);  // window-constant beta
                 uint32_t base_in = o;
+                uint32_t src_base = 0;
+                int sy0 = 0, sx0 = 0;
                 if (pooled) {
                     const uint32_t img = fdiv(o, a.f_chw), rem = o - img * chw;
                     const uint32_t ci = fdiv(rem, a.f_hw), rr = rem - ci * hw;
                     const uint32_t y0 = fdiv(rr, a.f_ow), x0 = rr - y0 * ow;
                     base_in = ((img * a.c + ci) * a.h + y0 * a.kh) * a.w + x0 * a.kw;
+                    if (SPLIT && a.gather) {
+                        src_base = (img * a.c + ci) * (uint32_t)(a.gh * a.gw);
+                        sy0 = (int)y0 * a.gs - a.gp;
+                        sx0 = (int)x0 * a.gs - a.gp;
+                    }
                 }
                 i64 acc = a.pool_kind == 1 ? INT64_MIN : 0;
 #pragma unroll 1
                 for (int wy = 0; wy < a.kh; wy++)
 #pragma unroll 1
                     for (int wx = 0; wx < a.kw; wx++) {
-                        const uint32_t i = base_in + wy * a.w + wx;
+                        const uint32_t i = base_in + wy * a.w + wx;      // (gathered) nonlinear input element
                         u64 x[N];
                         if (SPLIT) {
+                            uint32_t si = i;
+                            bool inside = true;
+                            if (a.gather) {
+                                const int sy = sy0 + wy, sx = sx0 + wx;
+                                inside = sy >= 0 && sy < a.gh && sx >= 0 && sx < a.gw;
+                                si = src_base + (uint32_t)(sy * a.gw + sx);
+                            }
 #pragma unroll
-                            for (int t = 0; t < M; t++) x[t] = a.acc[(u64)t * a.acc_ps + i];
+                            for (int t = 0; t < M; t++) x[t] = inside ? a.acc[(u64)t * a.acc_ps + si] : 0;
                         } else {
                             chain_elem<K, N, HF>(a, tb, i, x, bad);
                         }
                         // participants mask with their beta shares (NONLIN_MASKED); elite rec over m
                         u64 mk[M];
                         if constexpr (HF) {
-                            const uint32_t ii = i - fdiv(i, a.f_per) * (uint32_t)a.per;
+                            const uint32_t ii = i - fdiv(i, a.f_per_in) * (uint32_t)a.per_in;
 #pragma unroll
-                            for (int j = 0; j < M; j++) mk[j] = mulm(x[j], a.h_beta[(u64)j * a.per + ii]);
+                            for (int j = 0; j < M; j++) mk[j] = mulm(x[j], a.h_beta[(u64)j * a.per_in + ii]);
                         } else {
                             u64 cb[K - 1];
                             coeffs<K>(cb, a.sseed, a.sstream + 5, i);
@@ -700,12 +719,20 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
     a.h_binv = d->h_binv;
     a.per = d->h_period;
     a.per_out = d->h_period_out;
+    a.per_in = d->h_period_in ? d->h_period_in : d->h_period;
+    a.gather = d->gather;
+    a.gh = d->gather_h;
+    a.gw = d->gather_w;
+    a.gs = d->gather_stride;
+    a.gp = d->gather_pad;
     if (hf) {
         if (a.per < 1 || a.per >= (1ull << 32) || a.nel % a.per) return SSN_ERR_ARG;
         if (!d->nonlin_only && (!a.h_zero || !a.h_alpha || !a.h_comp || (K > 1 && !a.h_tcoef))) return SSN_ERR_ARG;
         if (d->nonlin && (!a.h_beta || !a.h_binv || a.per_out < 1 || a.per_out >= (1ull << 32))) return SSN_ERR_ARG;
         a.f_per = make_fastdiv((uint32_t)a.per);
         a.f_per_out = make_fastdiv((uint32_t)(a.per_out ? a.per_out : 1));
+        if (a.per_in < 1 || a.per_in >= (1ull << 32)) return SSN_ERR_ARG;
+        a.f_per_in = make_fastdiv((uint32_t)a.per_in);
         a.inv_table = nullptr;
     }
     if (a.planes && (!d->nonlin || a.pl_copies < 1 || a.pl_nparty < 1 || a.pl_nparty > N)) return SSN_ERR_ARG;
@@ -780,7 +807,15 @@ extern "C" int ssn_layer_chain(const ssn_chain_desc *d, void *stream) {
         if (d->kh < 1 || d->kw < 1 || d->h % d->kh || d->w % d->kw || d->bmax < 1 || d->fan < 1 || d->fan > d->n ||
             d->pool_kind < 0 || d->pool_kind > 2 || (d->pool_kind == 0 && (d->kh != 1 || d->kw != 1)))
             return SSN_ERR_ARG;
-        if ((u64)d->nb * d->c * d->h * d->w != d->nel) return SSN_ERR_ARG;
+        if (d->gather) {
+            // gathered windows need the split (scratch) form: the chain output is read per tap
+            if ((!d->scratch && !d->nonlin_only) || d->gather_h < 1 || d->gather_w < 1 || d->gather_stride < 1 ||
+                d->gather_pad < 0 || (u64)d->nb * d->c * d->gather_h * d->gather_w != d->nel || d->kh < 1 ||
+                d->kw < 1 || d->h % d->kh || d->w % d->kw)
+                return SSN_ERR_ARG;
+        } else if ((u64)d->nb * d->c * d->h * d->w != d->nel) {
+            return SSN_ERR_ARG;
+        }
     }
     if (d->nel == 0) return 0;
     cudaStream_t st = (cudaStream_t)stream;

@@ -783,5 +783,31 @@ extern "C" int ssn_pool_expand(const u64 *blk, u64 *out, int nb, int c, int h, i
     return ssn_check_launch();
 }
 
+// overlapping-window gather (builder op "gather"): one thread per gathered element
+__global__ void k_window_gather(const u64 *__restrict__ x, u64 *__restrict__ out, int h, int w, int kh, int kw,
+                                int stride, int pad, int oh, int ow, u64 n) {
+    const int gw = ow * kw, gh = oh * kh;
+    for (u64 o = blockIdx.x * (u64)blockDim.x + threadIdx.x; o < n; o += (u64)gridDim.x * blockDim.x) {
+        const u64 plane = o / ((u64)gh * gw);
+        const int rem = (int)(o - plane * (u64)gh * gw);
+        const int Y = rem / gw, X = rem - Y * gw;
+        const int oy = Y / kh, dy = Y - oy * kh, ox = X / kw, dx = X - ox * kw;
+        const int sy = oy * stride - pad + dy, sx = ox * stride - pad + dx;
+        out[o] = (sy >= 0 && sy < h && sx >= 0 && sx < w) ? x[plane * (u64)h * w + (u64)sy * w + sx] : 0;
+    }
+}
+extern "C" int ssn_window_gather(const u64 *x, u64 *out, int nb, int c, int h, int w, int kh, int kw, int stride,
+                                 int pad, void *strm) {
+    if (!x || !out || nb < 0 || c < 0 || kh < 1 || kw < 1 || stride < 1 || pad < 0 || h + 2 * pad < kh ||
+        w + 2 * pad < kw)
+        return SSN_ERR_ARG;
+    const int oh = (h + 2 * pad - kh) / stride + 1, ow = (w + 2 * pad - kw) / stride + 1;
+    const u64 n = (u64)nb * c * oh * kh * ow * kw;
+    if (n == 0) return 0;
+    SSN_COUNT_LAUNCH();
+    k_window_gather<<<ssn_blocks(n), 256, 0, (cudaStream_t)strm>>>(x, out, h, w, kh, kw, stride, pad, oh, ow, n);
+    return ssn_check_launch();
+}
+
 extern "C" int ssn_version(void) { return SSN_ABI_VERSION; }
 extern "C" unsigned long long ssn_kernel_launches(void) { return ssn_launch_counter(); }

@@ -7,8 +7,14 @@ own secure ops with share_add for the shortcut.  This module builds such DAGs:
   conv  -> Truncation(12)                                  (BN folded into the conv)
   relu  -> NonLinear(relu)                                 (masked, S/layers.py:326-380)
   add   -> local share_add of two degree-(k-1) shares      (S/sss.py:238)
-  stem max-pool 3x3/s2 -> NonLinear(relu, max 2x2)         (non-overlapping stand-in, same shape)
-  global avg-pool      -> NonLinear(relu, sum 7x7|4x4) -> Truncation(7)   (sum, then /128)
+  stem max-pool 3x3/s2/p1 -> gather -> NonLinear(relu, max 3x3)
+        "gather" is a local op on every party's share: window (oy, ox) of the overlapping pool
+        becomes a non-overlapping 3x3 block (zero shares outside the image), so the reference's
+        own masked max-pool (window-constant beta, S/layers.py:326-380, S/masks.py:67-90) runs
+        unchanged on it.  After ReLU every value is >= 0, so zero fill == -inf padding.
+  global avg-pool 7x7 (4x4) -> NonLinear(relu, sum 7x7) -> Truncation(r=1, divisor=49)
+        a true average, round_half_away(sum / 49) -- the reference's merged-divisor rounding
+        (S/layers.py:300-308, S/model.py:44-50) with r = 1 (the sum is >= 0 after ReLU).
 
 Value bounds follow the reference's planner rules (S/layers.py:94-135, S/model.py:239-252)
 generalised to the DAG: an add doubles the bound, a sum pool multiplies it by the window.
@@ -35,7 +41,7 @@ B_MAX = (1 << (BIAS_BITS - 1)) - 1
 
 @dataclass
 class Node:
-    kind: str                  # conv | dense | trunc | relu | pool | add | output
+    kind: str                  # conv | dense | trunc | relu | gather | add | output
     name: str
     src: int                   # producer node index (-1 = input)
     src2: int = None
@@ -47,6 +53,7 @@ class Node:
     pool: tuple = None
     pool_kind: str = None
     relu: bool = True
+    divisor: int = 1           # trunc: extra round_half_away divisor (average pooling)
 
 
 @dataclass
@@ -84,6 +91,11 @@ class ResNetGraph:
             elif nd.kind == "relu" and nd.pool is not None:
                 c, h, w = s
                 shp[i] = (c, h // nd.pool[0], w // nd.pool[1])
+            elif nd.kind == "gather":
+                c, h, w = s
+                oh = (h + 2 * nd.padding - nd.kernel) // nd.stride + 1
+                ow = (w + 2 * nd.padding - nd.kernel) // nd.stride + 1
+                shp[i] = (c, oh * nd.kernel, ow * nd.kernel)
             else:
                 shp[i] = s
         return shp
@@ -108,7 +120,7 @@ class ResNetGraph:
                 prev = self.nodes[nd.src] if nd.src >= 0 else None
                 vb = bound[nd.src] if prev is not None and prev.kind in ("conv", "dense") else bound[nd.src]
                 bound[i] = ACT_BOUND
-                ops.append(ScheduledOp("truncation", i, nd.name, s_in, s_out, r=1 << nd.shift, divisor=1,
+                ops.append(ScheduledOp("truncation", i, nd.name, s_in, s_out, r=1 << nd.shift, divisor=nd.divisor,
                                        value_bound=vb, src=src))
             elif nd.kind == "relu":
                 vb = bound[nd.src]
@@ -117,6 +129,10 @@ class ResNetGraph:
                 bound[i] = vb
                 ops.append(ScheduledOp("nonlinear", i, nd.name, s_in, s_out, relu=nd.relu, pool=nd.pool,
                                        pool_kind=nd.pool_kind, value_bound=vb, src=src))
+            elif nd.kind == "gather":
+                bound[i] = bound[nd.src]
+                ops.append(ScheduledOp("gather", i, nd.name, s_in, s_out, pool=(nd.kernel, nd.kernel), stride=nd.stride,
+                                       padding=nd.padding, src=src))
             elif nd.kind == "add":
                 # residual stream re-bounded to 16 bits (checked by check_bounds on plaintext,
                 # like the reference's 16-bit activation check, S/model.py:409-410)
@@ -198,9 +214,16 @@ def _basic(g, x, name, width, stride, downsample):
     return g.relu(s, f"{name}.relu2")
 
 
+def _stem_pool(g, x):
+    """3x3 / stride 2 / pad 1 max-pool over ReLU: gathered windows + the reference's pool."""
+    x = g._add(Node("gather", "stem.gather", x, kernel=3, stride=2, padding=1))
+    return g.relu(x, "stem.pool", pool=(3, 3), pool_kind="max")
+
+
 def _head(g, x, pool_hw, classes):
+    """Global average pool: ReLU + window sum, then round_half_away(sum / pool_hw^2)."""
     x = g.relu(x, "gpool", pool=(pool_hw, pool_hw), pool_kind="sum")
-    x = g._add(Node("trunc", "div.gpool", x, shift=7))
+    x = g._add(Node("trunc", "div.gpool", x, shift=0, divisor=pool_hw * pool_hw))
     return _dense(g, x, "fc", classes)
 
 
@@ -214,7 +237,7 @@ def imagenet_resnet(depth, seed=7, classes=1000, image=224):
     blocks = {50: [3, 4, 6, 3], 101: [3, 4, 23, 3], 152: [3, 8, 36, 3]}[depth]
     g = ResNetGraph(f"resnet{depth}-ss", (3, image, image))
     x = g.conv_trunc(-1, "stem", 64, 7, stride=2, pad=3)
-    x = g.relu(x, "stem.pool", pool=(2, 2), pool_kind="max")
+    x = _stem_pool(g, x)
     for si, (nb, width) in enumerate(zip(blocks, (64, 128, 256, 512))):
         for bi in range(nb):
             stride = 2 if (bi == 0 and si > 0) else 1
@@ -239,7 +262,7 @@ def tiny_resnet(seed=3, classes=10):
     """Small residual net for smoke / parity tests (both block kinds, a downsample, both pools)."""
     g = ResNetGraph("tiny-resnet-ss", (3, 16, 16))
     x = g.conv_trunc(-1, "stem", 8, 3, pad=1)
-    x = g.relu(x, "stem.pool", pool=(2, 2), pool_kind="max")
+    x = _stem_pool(g, x)
     x = _basic(g, x, "s1.b0", 8, 1, downsample=False)
     x = _bottleneck(g, x, "s2.b0", 4, 2, downsample=True)
     _head(g, x, 4, classes)
@@ -268,6 +291,14 @@ def plaintext_forward(graph, x, device="cpu", check=True):
             y = t.reshape(t.shape[0], -1) @ w.T + b
         elif nd.kind == "trunc":
             y = torch.floor(t / float(1 << nd.shift))
+            if nd.divisor > 1:                      # round_half_away (S/model.py:44-50)
+                y = torch.sign(y) * torch.floor((2 * y.abs() + nd.divisor) / (2 * nd.divisor))
+        elif nd.kind == "gather":
+            B, c, h, w_ = t.shape
+            k, s_, pd = nd.kernel, nd.stride, nd.padding
+            cols = F.unfold(t.reshape(B * c, 1, h, w_), k, padding=pd, stride=s_)   # (B*c, k*k, OH*OW)
+            oh, ow = (h + 2 * pd - k) // s_ + 1, (w_ + 2 * pd - k) // s_ + 1
+            y = cols.reshape(B, c, k, k, oh, ow).permute(0, 1, 4, 2, 5, 3).reshape(B, c, oh * k, ow * k)
         elif nd.kind == "relu":
             y = torch.clamp(t, min=0) if nd.relu else t
             if nd.pool is not None:

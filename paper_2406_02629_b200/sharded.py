@@ -31,7 +31,7 @@ from . import _lib
 from . import gemm as gemm_mod
 from .batched import _count
 from .gemm import field_conv, field_dense
-from .layers import consumers, plan_schedule
+from .layers import consumers, plan_schedule, window_gather
 from .masks import additive_mask_bound, multiplicative_mask_bound
 from .protocol import VerificationError, extrapolation_coeffs
 from .rng import DeviceRng
@@ -229,6 +229,12 @@ class PartyShardedEngine:
                 if xin is not None and other is not None:
                     y = torch.empty_like(xin)
                     self._ew(0, xin, other, y, y.numel())
+            elif op.kind == "gather":               # local: this party's share only
+                y = None
+                if xin is not None:
+                    kh, kw = op.pool
+                    y = window_gather(xin, op.in_shape, kh, kw, op.stride, op.padding, nbatch=B) \
+                        .reshape((B,) + tuple(op.out_shape))
             elif op.kind == "output":
                 result = self._output(op, xin)
                 y = None

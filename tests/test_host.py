@@ -87,3 +87,31 @@ def test_metrics_epochs():
     m.on_send(1, 10, 1)
     assert m.rounds("op", 0) == 2
     assert m.elements_sent("op") == 3
+
+
+def test_gathered_stem_pool_equals_overlapping_maxpool():
+    """The builder op "gather" + the reference's non-overlapping max pool (S/model.py:374-377)
+    is ResNet's 3x3 / stride 2 / pad 1 max-pool after ReLU (zero fill == -inf padding there)."""
+    import torch
+    import torch.nn.functional as F
+    from oracle import window_gather
+    rng = np.random.default_rng(3)
+    for (c, h, w) in ((2, 16, 16), (3, 112, 112), (1, 7, 9)):
+        x = rng.integers(-2 ** 15, 2 ** 15, size=(c, h, w))
+        g = window_gather(np.maximum(x, 0), 3, 3, 2, 1)
+        oh, ow = g.shape[1] // 3, g.shape[2] // 3
+        pooled = g.reshape(c, oh, 3, ow, 3).max(axis=(2, 4))
+        want = F.max_pool2d(torch.as_tensor(np.maximum(x, 0), dtype=torch.float64)[None], 3, 2, 1)[0]
+        assert np.array_equal(pooled, want.numpy().astype(np.int64))
+
+
+def test_resnet_head_is_true_average():
+    """Global pool = round_half_away(sum / 49) (merged-divisor rounding, S/model.py:44-50)."""
+    from paper_2406_02629_b200 import resnet
+    g = resnet.imagenet_resnet(50, seed=7, classes=10)
+    ops = g.plan_ops()
+    tr = [op for op in ops if op.name == "div.gpool"][0]
+    assert (tr.r, tr.divisor) == (1, 49)
+    st = [op for op in ops if op.kind == "gather"]
+    assert len(st) == 1 and st[0].pool == (3, 3) and (st[0].stride, st[0].padding) == (2, 1)
+    assert tuple(st[0].out_shape) == (64, 168, 168)
