@@ -208,9 +208,171 @@ def engine_goldens():
         json.dump(cases, fh, indent=1, sort_keys=True)
 
 
+def _gather_obj(x, kh, kw, stride, pad):
+    """Builder op "gather" on one party's reference share values (object ndarray, c x h x w):
+    window (oy, ox) tap (dy, dx) -> block position (oy*kh+dy, ox*kw+dx), share 0 outside.
+    Written out with explicit loops here, independently of oracle.window_gather."""
+    c, h, w = x.shape
+    oh, ow = (h + 2 * pad - kh) // stride + 1, (w + 2 * pad - kw) // stride + 1
+    out = np.zeros((c, oh * kh, ow * kw), dtype=object)
+    for oy in range(oh):
+        for ox in range(ow):
+            for dy in range(kh):
+                for dx in range(kw):
+                    sy, sx = oy * stride - pad + dy, ox * stride - pad + dx
+                    if 0 <= sy < h and 0 <= sx < w:
+                        out[:, oy * kh + dy, ox * kw + dx] = x[:, sy, sx]
+    return out
+
+
+def residual_goldens():
+    """A residual network run through the REFERENCE's own secure ops (SURVEY.md section 7
+    step 1): per rank one thread over ssnet's SimHub, each op dispatched to ssnet's
+    sss_linear / sss_truncation / sss_nonlinear / share_add / output_collect, with the
+    reference's dealing (lanes 1, 3), trusted source (lane 4) and party streams (lane 5).
+    The DAG (residual adds, the gathered 3x3/s2 stem pool, the /16 average) comes from the
+    builder's tiny ResNet; the only builder-side step is the local window gather.  Masks:
+    the reference's trusted_source_prepare over the schedule with every local op ("add",
+    "gather") replaced by an "output" placeholder, so op indices and draw order line up.
+    Stores the decoded outputs and every rank's share of every op output."""
+    import threading
+    sys.path.insert(0, os.path.dirname(os.path.dirname(OUT)))
+    from paper_2406_02629_b200 import resnet as R
+    from ssnet.engine import deal_input_shares, deal_weight_shares, receive_bundle, seeded_rng, send_bundles
+    from ssnet.layers import sss_linear, sss_nonlinear, sss_truncation
+    from ssnet.protocol import PartyContext, output_collect
+    from ssnet.sss import share_add
+    from ssnet.transport import SimHub
+    net = R.tiny_resnet(seed=3)
+    dag = net.op_dicts()
+    ref_fields = [fl.name for fl in ScheduledOp.__dataclass_fields__.values()]
+
+    def ref_op(m, placeholder=False):
+        kw = {k: m[k] for k in ref_fields if k in m}
+        kw["in_shape"], kw["out_shape"] = tuple(m["in_shape"]), tuple(m["out_shape"])
+        kw["pool"] = tuple(m["pool"]) if m["pool"] else None
+        if placeholder:
+            kw.update(kind="output", pool=None, pool_kind=None)
+        return ScheduledOp(**kw)
+
+    ops = [ref_op(m) if m["kind"] not in ("add", "gather") else None for m in dag]
+    src_ops = [ref_op(m, placeholder=m["kind"] in ("add", "gather")) for m in dag]
+    weights = net.weight_values()
+    arrays, cases = {}, []
+    xs = net.random_inputs(5, 2)
+    for k, n in ((2, 3), (3, 5)):
+        scheme = SssScheme(F, k, n)
+        for index in range(2):
+            seed = 7
+            x = xs[index]
+            hub = SimHub(range(0, n + 1))
+            wsh = deal_weight_shares(weights, scheme, seed)
+            xsh = deal_input_shares(x, scheme, seed, index)
+            vals_by_rank, outputs, errors = {}, {}, {}
+
+            def party(rank):
+                def run():
+                    try:
+                        ctx = PartyContext(scheme, rank, hub.transport(rank), rng=seeded_rng(seed, 5, rank))
+                        receive_bundle(ctx)
+                        vals = {-1: xsh[rank - 1]}
+                        for idx, m in enumerate(dag):
+                            x_ = vals.get(m.get("src", idx - 1))
+                            kind = m["kind"]
+                            if kind == "linear":
+                                y = sss_linear(ctx, ops[idx], x_, wsh[rank][m["weight"] + ".w"],
+                                               wsh[rank][m["weight"] + ".b"], ctx.bundle.take(idx, "zero"))
+                            elif kind == "truncation":
+                                y = sss_truncation(ctx, ops[idx], x_, ctx.bundle.take(idx, "alpha"),
+                                                   ctx.bundle.take(idx, "comp"))
+                            elif kind == "nonlinear":
+                                y = sss_nonlinear(ctx, ops[idx], x_, ctx.bundle.take(idx, "beta"),
+                                                  ctx.bundle.take(idx, "beta_inv"))
+                            elif kind == "add":
+                                o = vals.get(m["src2"])
+                                y = share_add(x_, o) if (x_ is not None and o is not None) else None
+                            elif kind == "gather":
+                                y = None
+                                if x_ is not None:
+                                    g = _gather_obj(np.asarray(x_.values).reshape(tuple(m["in_shape"])),
+                                                    m["pool"][0], m["pool"][1], m["stride"], m["padding"])
+                                    y = ShareTensor(x_.party_id, x_.degree, g, scheme)
+                            elif kind == "output":
+                                vals[idx] = x_
+                                out = output_collect(ctx, x_)
+                                if out is not None:
+                                    outputs[rank] = out
+                                break
+                            vals[idx] = y
+                        vals_by_rank[rank] = vals
+                    except BaseException as exc:       # surface thread errors
+                        errors[rank] = exc
+                return run
+
+            threads = [threading.Thread(target=lambda: send_bundles(hub.transport(0), src_ops, scheme, seed))]
+            threads += [threading.Thread(target=party(r)) for r in range(1, n + 1)]
+            for t in threads:
+                t.start()
+            for t in threads:
+                t.join(600)
+            if errors:
+                raise errors[sorted(errors)[0]]
+            tag = f"tiny-resnet/{k}{n}/{index}"
+            arrays[tag + "/x"] = x.astype(np.int64)
+            arrays[tag + "/out"] = np.asarray(np.asarray(outputs[1]).tolist(), dtype=np.int64)
+            held = {}
+            for idx, m in enumerate(dag):
+                if m["kind"] == "gather":
+                    continue
+                ranks = [r for r in range(1, n + 1) if vals_by_rank[r].get(idx) is not None]
+                held[idx] = ranks
+                arrays[f"{tag}/shares/{idx}"] = np.stack([u64(vals_by_rank[r][idx].values).reshape(-1)
+                                                          for r in ranks])
+            cases.append({"tag": tag, "k": k, "n": n, "input_index": index, "seed": seed, "held": held,
+                          "transcript_digest": hub.transcript_digest()})
+    with open(os.path.join(OUT, "residual.json"), "w") as fh:
+        json.dump({"model": "tiny-resnet(seed=3)", "input_seed": 5, "ops": dag, "cases": cases}, fh, indent=1,
+                  sort_keys=True)
+    np.savez_compressed(os.path.join(OUT, "residual.npz"), **arrays)
+
+
+def acceptance_goldens():
+    """T/test_acceptance.py:155-176 (criterion 03): 100 inputs x {(2,3), (3,5)} through the
+    reference's simulate_schedule on the reference model -- decoded outputs, the rank-1..n
+    output shares and the SimHub transcript digest of every run."""
+    model, _ = build_reference_model(seed=7, pool="max")
+    weights = {name: qt.values for name, qt in model.weights.items()}
+    arrays, meta = {}, {}
+    xs = np.stack([random_input(7, model, index=i)[0] for i in range(100)])
+    arrays["x"] = xs.astype(np.int64)
+    for k, n in ((2, 3), (3, 5)):
+        scheme = SssScheme(F, k, n)
+        ops, sdig = plan_schedule(model, scheme)
+        outs, digests = [], []
+        for idx in range(100):
+            res = simulate_schedule(ops, sdig, scheme, 7, input_int=xs[idx], weight_values=weights,
+                                    input_index=idx, timeout=600)
+            assert np.all(res.output == plaintext_infer(model, xs[idx]))
+            outs.append(res.output.astype(np.int64))
+            digests.append(res.transcript_digest())
+        arrays[f"out_{k}{n}"] = np.stack(outs)
+        meta[f"{k}{n}"] = digests
+    np.savez_compressed(os.path.join(OUT, "acceptance.npz"), **arrays)
+    with open(os.path.join(OUT, "acceptance.json"), "w") as fh:
+        json.dump({"model": "reference-max(seed=7)", "seed": 7, "transcripts": meta}, fh, indent=1, sort_keys=True)
+
+
 if __name__ == "__main__":
-    with open(os.path.join(OUT, "unit.json"), "w") as fh:
-        json.dump(unit_goldens(), fh, indent=1, sort_keys=True)
-    vector_goldens()
-    engine_goldens()
+    which = sys.argv[1:] or ["unit", "vectors", "engine", "residual", "acceptance"]
+    if "unit" in which:
+        with open(os.path.join(OUT, "unit.json"), "w") as fh:
+            json.dump(unit_goldens(), fh, indent=1, sort_keys=True)
+    if "vectors" in which:
+        vector_goldens()
+    if "engine" in which:
+        engine_goldens()
+    if "residual" in which:
+        residual_goldens()
+    if "acceptance" in which:
+        acceptance_goldens()
     print("golden fixtures written to", OUT)

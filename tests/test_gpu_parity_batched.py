@@ -86,3 +86,97 @@ def test_unfused_shares_equal_reference(P, k, n):
 @pytest.mark.parametrize("fuse", [True, False])
 def test_verified_run_shares_equal_reference(P, fuse):
     _check(P, _models(P)["tiny-resnet"], 3, 5, fuse=fuse, verify=True)
+
+
+# ---------------------------------------------------------------- reference-composed fixtures
+import json  # noqa: E402
+import os  # noqa: E402
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _residual():
+    with open(os.path.join(GOLD, "residual.json")) as fh:
+        meta = json.load(fh)
+    return meta, np.load(os.path.join(GOLD, "residual.npz"))
+
+
+@pytest.mark.parametrize("fuse", [True, False])
+def test_batched_residual_net_equals_reference_composed_fixture(P, fuse):
+    """Residual DAG run through the reference's OWN sss_* ops (make_golden.residual_goldens)
+    vs the batched engine (fused chains with the gathered stem pool, residual add and the /16
+    average) in reference-stream mode: every rank's share of every materialised op output."""
+    from paper_2406_02629_b200 import resnet
+    from paper_2406_02629_b200.batched import BatchedEngine
+    meta, arr = _residual()
+    net = resnet.tiny_resnet(seed=3)
+    for k, n in ((2, 3), (3, 5)):
+        cases = [c for c in meta["cases"] if (c["k"], c["n"]) == (k, n)]
+        x = np.stack([arr[c["tag"] + "/x"] for c in cases])
+        eng = BatchedEngine(net, P.SssScheme(P.PrimeField(), k, n), batch=len(cases), seed=cases[0]["seed"],
+                            rng_mode="host", fuse=fuse)
+        assert [op.meta() for op in eng.ops] == meta["ops"]
+        cap = {}
+        out = eng.run_device(torch.as_tensor(x), capture_shares=cap,
+                             input_indices=[c["input_index"] for c in cases]).cpu().numpy()
+        compared = 0
+        for b, c in enumerate(cases):
+            assert np.array_equal(out[b], arr[c["tag"] + "/out"])
+            for idx, got in cap.items():
+                if str(idx) not in c["held"]:          # the fixture skips the local gather op
+                    continue
+                ranks = c["held"][str(idx)]
+                want = arr[f"{c['tag']}/shares/{idx}"]
+                for row, r in enumerate(ranks):
+                    assert np.array_equal(got[r - 1][b].cpu().numpy().astype(np.uint64).reshape(-1), want[row]), \
+                        (k, n, b, idx, r)
+                    compared += 1
+        assert compared > 10
+
+
+def test_per_party_api_residual_transcript_equals_reference(P):
+    """The per-party API path (simulate_schedule: one thread per rank over the DeviceHub, the
+    reference's seam) on the residual DAG reproduces the reference-composed run's SimHub
+    transcript sha256 and outputs."""
+    from paper_2406_02629_b200 import resnet
+    from paper_2406_02629_b200.engine import simulate_schedule
+    from paper_2406_02629_b200.layers import plan_schedule
+    meta, arr = _residual()
+    net = resnet.tiny_resnet(seed=3)
+    for c in meta["cases"]:
+        scheme = P.SssScheme(P.PrimeField(), c["k"], c["n"])
+        ops, digest = plan_schedule(net, scheme)
+        res = simulate_schedule(ops, digest, scheme, c["seed"], input_int=arr[c["tag"] + "/x"],
+                                weight_values=net.weight_values(), input_index=c["input_index"], rng_mode="host",
+                                record=True, timeout=600)
+        assert np.array_equal(res.output, arr[c["tag"] + "/out"])
+        assert res.transcript_digest() == c["transcript_digest"], c["tag"]
+
+
+@pytest.mark.parametrize("k,n", [(2, 3), (3, 5)])
+def test_acceptance_100_inputs_batched(P, k, n):
+    """T/test_acceptance.py:155-176 (criterion 03): 100 inputs through the timed batched
+    engine in one launch sequence, both randomness modes, == the reference's 100 runs."""
+    from paper_2406_02629_b200.batched import BatchedEngine
+    arr = np.load(os.path.join(GOLD, "acceptance.npz"))
+    model, _ = P.build_reference_model(7, pool="max")
+    scheme = P.SssScheme(P.PrimeField(), k, n)
+    want = arr[f"out_{k}{n}"]
+    for mode in ("host", "device"):
+        eng = BatchedEngine(model, scheme, batch=100, seed=7, rng_mode=mode)
+        got = eng.run_device(torch.as_tensor(arr["x"])).cpu().numpy()
+        assert np.array_equal(got, want), mode
+
+
+def test_acceptance_transcripts_per_party_api(P):
+    """Transcript sha256 of every tenth acceptance run through the per-party API."""
+    with open(os.path.join(GOLD, "acceptance.json")) as fh:
+        meta = json.load(fh)
+    arr = np.load(os.path.join(GOLD, "acceptance.npz"))
+    model, _ = P.build_reference_model(7, pool="max")
+    for k, n in ((2, 3), (3, 5)):
+        scheme = P.SssScheme(P.PrimeField(), k, n)
+        for idx in range(0, 100, 10):
+            res = P.simulate_inference(model, scheme, 7, arr["x"][idx], input_index=idx, record=True)
+            assert np.array_equal(res.output, arr[f"out_{k}{n}"][idx])
+            assert res.transcript_digest() == meta["transcripts"][f"{k}{n}"][idx]

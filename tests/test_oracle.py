@@ -143,3 +143,59 @@ def test_verify_mode_detects_corruption(engine):
     bad = sim.simulate(ops, sch, case["seed"], x, weights, input_index=case["input_index"],
                        verify=True, corrupt=(1, 5))
     assert bad["checks_failed"] == 1
+
+
+@pytest.fixture(scope="module")
+def residual():
+    with open(os.path.join(GOLD, "residual.json")) as fh:
+        meta = json.load(fh)
+    return meta, np.load(os.path.join(GOLD, "residual.npz"))
+
+
+def _tiny_resnet_weights():
+    from paper_2406_02629_b200 import resnet     # host-side graph builder (no GPU needed)
+    return resnet.tiny_resnet(seed=3).weight_values()
+
+
+def test_oracle_sim_matches_reference_composed_residual_net(residual):
+    """The reference's own sss_linear / sss_truncation / sss_nonlinear / share_add /
+    output_collect composed over a residual DAG (tests/golden/make_golden.py
+    residual_goldens) == the lockstep oracle: decoded outputs, every rank's share of every
+    op output, and the SimHub transcript sha256."""
+    meta, arr = residual
+    weights = _tiny_resnet_weights()
+    ops = meta["ops"]
+    for case in meta["cases"]:
+        tag = case["tag"]
+        x = arr[tag + "/x"]
+        res = sim.simulate(ops, sim.Scheme(case["k"], case["n"]), case["seed"], x, weights,
+                           input_index=case["input_index"], record=True, return_shares=True)
+        assert np.array_equal(res["output"], arr[tag + "/out"]), tag
+        assert res["transcript_digest"] == case["transcript_digest"], tag
+        for idx, ranks in case["held"].items():
+            want = arr[f"{tag}/shares/{idx}"]
+            vals = res["values"][int(idx)]
+            assert sorted(vals) == ranks, (tag, idx)
+            for row, r in enumerate(ranks):
+                got = np.asarray(vals[r][1], dtype=np.uint64).reshape(-1)
+                assert np.array_equal(got, want[row]), (tag, idx, r)
+
+
+def test_oracle_sim_acceptance_100_inputs_two_schemes():
+    """T/test_acceptance.py:155-176 (criterion 03) fixture: 100 inputs x {(2,3), (3,5)} --
+    decoded outputs and transcript digests of the reference's runs."""
+    with open(os.path.join(GOLD, "acceptance.json")) as fh:
+        meta = json.load(fh)
+    arr = np.load(os.path.join(GOLD, "acceptance.npz"))
+    from paper_2406_02629_b200 import build_reference_model, layers, PrimeField, SssScheme
+    model, _ = build_reference_model(7, pool="max")
+    weights = {name: qt.values for name, qt in model.weights.items()}
+    for k, n in ((2, 3), (3, 5)):
+        ops, _ = layers.plan_schedule(model, SssScheme(PrimeField(), k, n))
+        ops = [op.meta() for op in ops]
+        for idx in range(100):
+            rec = idx % 10 == 0                  # transcript digests on a tenth (CPU time)
+            res = sim.simulate(ops, sim.Scheme(k, n), 7, arr["x"][idx], weights, input_index=idx, record=rec)
+            assert np.array_equal(res["output"], arr[f"out_{k}{n}"][idx]), (k, n, idx)
+            if rec:
+                assert res["transcript_digest"] == meta["transcripts"][f"{k}{n}"][idx]
