@@ -118,6 +118,20 @@ def field_dense(w, x, p, nimg=1, nparty=1, planes=None, force=None, timing=None)
     out = torch.empty((nparty, nimg, O) if (nparty > 1 or nimg > 1) else (O,), dtype=torch.int64,
                       device=x.device)
     tc = use_tc(p, nimg, K, O) if force is None else force == "tc"
+    if tc and kpad(K) > max_k_chunk(p):
+        # split-K: exact partial products over K chunks (each within the int32 limb budget),
+        # added mod p
+        chunk = max_k_chunk(p)
+        for k0 in range(0, K, chunk):
+            k1 = min(K, k0 + chunk)
+            part = field_dense(w[..., k0:k1].contiguous(), x[..., k0:k1].contiguous(), p, nimg=nimg, nparty=nparty,
+                               force="tc")
+            if k0 == 0:
+                out.copy_(part)
+            else:
+                _lib.call("ssn_ewise", 0, _lib.ptr(out), _lib.ptr(part), _lib.ptr(out), out.numel(), 1, out.numel(),
+                          1 << 62, 0, p, _lib.stream_ptr())
+        return out
     if tc:
         L, Kp = limbs(p), kpad(K)
         if planes is None:

@@ -198,6 +198,15 @@ def test_resnet152_5pc_full_size_matches_plaintext(ssn):
     want, _ = resnet.plaintext_forward(net, xb, device="cuda")
     assert np.array_equal(eng.run(xb), want)
     assert int(eng.fail.item()) == 0
+    # and the oracle's integer plaintext over the schedule (oracle/sim.py, pinned to the
+    # reference's plaintext_infer and the reference-composed residual fixture)
+    import oracle
+    from oracle import sim
+    oracle.set_threads(0)
+    ops = net.op_dicts()
+    for b in range(2):
+        got, _ = sim.plaintext(ops, xb[b], net.weight_values())
+        assert np.array_equal(got, want[b]), b
 
 
 @pytest.mark.parametrize("streams", [2, 3])

@@ -131,3 +131,17 @@ def test_small_row_dense_on_tensor_cores(rows, K, O):
     tc = G.field_dense(w, x, p, nimg=rows, nparty=2, force="tc")
     simt = G.field_dense(w, x, p, nimg=rows, nparty=2, force="simt")
     assert torch.equal(tc, simt)
+
+
+@pytest.mark.parametrize("rows,O,K", [(256, 128, 11009), (256, 64, 16384), (384, 256, 16384)])
+def test_split_k_dense_exact(g, rows, O, K):
+    """K > 11,008 overflows the u32 limb-diagonal budget (L*K*255^2 < 2^32) and is split into
+    exact partial GEMMs added mod p (gemm.field_matmul) -- the config-5 sweep's 16384^3 path.
+    Against the CUDA-core 64x64->128 GEMM everywhere, and the CPU oracle on a row block."""
+    rng = np.random.default_rng(K + O)
+    w = rng.integers(0, P, size=(O, K), dtype=np.uint64)
+    x = rng.integers(0, P, size=(rows, K), dtype=np.uint64)
+    tc, simt = _dense_both(g, w, x, rows)
+    assert np.array_equal(tc, simt)
+    blk = slice(0, 16)
+    assert np.array_equal(tc.reshape(rows, O)[blk], oracle.gemm(x[blk], w.T))
