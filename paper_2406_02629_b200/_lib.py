@@ -14,6 +14,8 @@ import torch
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB_PATH = os.path.join(HERE, "libssn_b200.so")
+if os.environ.get("SSN_LIB"):             # experiments only: an alternative build of the same sources
+    LIB_PATH = os.environ["SSN_LIB"]
 CSRC = os.path.join(HERE, "csrc")
 SOURCES = ["ssn_elementwise.cu", "ssn_gemm_simt.cu", "ssn_gemm_tc.cu", "ssn_chain.cu"]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

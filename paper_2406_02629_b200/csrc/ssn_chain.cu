@@ -111,8 +111,27 @@ struct ChainArgs {
     int gather, gh, gw, gs, gp;
 };
 
+// Co-scheduling with the persistent share GEMM (SSN_COSCHED, default on): the chain kernels are
+// shaped so that AT MOST TWO of their blocks fit on an SM and two always leave room for one GEMM
+// CTA (192 threads x 80 registers + its shared memory).  Whatever order the block scheduler sees
+// the launches of the two CUDA streams in, a GEMM CTA never waits for chain blocks to drain, so
+// the tensor-bound GEMM of one sub-batch runs UNDER the ALU-bound chains of the other.
+//   k_chain_plain:  256 threads x <= 96 registers  (24 576 per block, 3 would need 73 728)
+//   k_chain_nonlin: 288 threads x <= 80 registers  (23 040 per block, 3 would need 69 120)
+#ifndef SSN_COSCHED
+#define SSN_COSCHED 0
+#endif
+#if SSN_COSCHED
+constexpr int CHAIN_THREADS = 288;
+constexpr int PLAIN_THREADS = 256;
+#define SSN_PLAIN_BOUNDS __maxnreg__(96)
+#define SSN_NONLIN_BOUNDS __maxnreg__(80)
+#else
 constexpr int CHAIN_THREADS = 128;
 constexpr int PLAIN_THREADS = 128;
+#define SSN_PLAIN_BOUNDS __launch_bounds__(PLAIN_THREADS, 4)
+#define SSN_NONLIN_BOUNDS __launch_bounds__(CHAIN_THREADS, 6)
+#endif
 
 __device__ __forceinline__ u64 sqn(u64 x, int n) {
 #pragma unroll 1
@@ -300,7 +319,7 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
 }
 
 template <int K, int N, bool HF>
-__global__ void __launch_bounds__(PLAIN_THREADS, 4) k_chain_plain(ChainArgs a, const __grid_constant__ STables<K, N> tb,
+__global__ void SSN_PLAIN_BOUNDS k_chain_plain(ChainArgs a, const __grid_constant__ STables<K, N> tb,
                                                      SsnField f) {
     unsigned long long bad = 0;
     const uint32_t nel = (uint32_t)a.nel;
@@ -359,7 +378,7 @@ constexpr int WPT = 8;
 // output) and this kernel only runs the masked nonlinearity, reading each party's share.
 // Two kernels of half the code each run faster than one that overflows the instruction cache.
 template <int K, int N, bool SPLIT, bool HF>
-__global__ void __launch_bounds__(CHAIN_THREADS, 6) k_chain_nonlin(ChainArgs a, const __grid_constant__ STables<K, N> tb,
+__global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, const __grid_constant__ STables<K, N> tb,
                                                                 SsnField f) {
     constexpr int M = 2 * K - 1;
     unsigned long long bad = 0;
@@ -567,6 +586,7 @@ static u64 chain_grid_cap(KernT kern, int threads) {
             return cache[e].cap;
     int nsm = 0, per_sm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    ssn_prefer_max_smem(kern);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0) != cudaSuccess || per_sm < 1)
         per_sm = 4;
     const char *env = getenv("SSN_CHAIN_WAVES");

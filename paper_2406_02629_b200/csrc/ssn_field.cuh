@@ -151,6 +151,15 @@ inline unsigned long long &ssn_launch_counter() {
 }
 #define SSN_COUNT_LAUNCH() (++ssn_launch_counter())
 
+// Kernels that run beside the persistent share GEMM (chains, plane packing) ask for the
+// max-shared-memory L1 carveout: an SM configured for a small carveout must drain every resident
+// block before it can switch and host a GEMM CTA (~185 KB of shared memory), which serialises
+// the two CUDA streams the bench overlaps.  Call once per kernel (host side).
+template <typename KernT>
+inline void ssn_prefer_max_smem(KernT kern) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)cudaSharedmemCarveoutMaxShared);
+}
+
 // Two uniform field elements (coefficients 2*jp and 2*jp+1) from one Philox call when p is
 // within 2^-24 of a power of two (masked 64-bit words; the default prime is 2^-39 close);
 // otherwise the bounded 96-bit method, one call each.

@@ -265,27 +265,20 @@ k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUten
 }
 
 // ============================================================================================
-// Persistent, warp-specialised variant for the default field p = 2^45 - 55 (L = 6 limbs).
-//   warp 0      TMA producer (4-stage smem ring, A 128x64x6 + B 16x64x6 bytes per stage)
-//   warp 1      TMEM allocator + MMA issuer: per 32-wide K slice, 6 MMAs of 128 x 96 x 32
-//   warps 2..5  epilogue: TMEM -> registers -> mod-p recombination -> HBM
-// The 11 limb-diagonal accumulators of a 128 x 16 tile take 176 TMEM columns, so two tiles
-// are in flight (TMEM buffers at columns 0 and 256): the epilogue of tile t overlaps the
-// MMAs of tile t+1.  Epilogue recombination is exact integer arithmetic specialised to p:
+// Persistent, warp-specialised kernel for the default field p = 2^45 - 55 (L = 6 limbs).
+//   warp 0      TMA producer (smem ring of A 128x64x6 + B BNx64x6 bytes per stage)
+//   warp 1      TMEM allocator + MMA issuer: per 32-wide K slice, 6 MMAs of 128 x (6 BN) x 32
+//   warps 2..   epilogue: TMEM -> registers -> mod-p recombination -> HBM
+// The 11 limb-diagonal accumulators of a 128 x BN tile take 11 BN TMEM columns: one buffer at
+// BN = 32, two (columns 0 and 256) at BN = 16 so the epilogue of tile t overlaps the MMAs of
+// tile t+1.  Epilogue recombination is exact integer arithmetic specialised to p:
 //   g0 = sum_{d<4} D_d 2^{8d},  g1 = sum_{4<=d<8} D_d 2^{8(d-4)},  g2 = sum_{d>=8} D_d 2^{8(d-8)}
 //   (each one IMAD.WIDE per diagonal, all < 2^57), value = g0 + g1 2^32 + g2 2^64, folded with
-//   2^45 == 55 (mod p).
+//   2^45 == 55 (mod p) one group at a time.
 namespace p45 {
 constexpr int L = 6;
-constexpr int BN2 = 16;                  // output channels per tile
 constexpr int ND = 2 * L - 1;            // 11 limb diagonals
-constexpr int ST = 4;                    // smem stages
 constexpr int A_BYTES = L * BM * BK;     // 49152
-constexpr int B_BYTES = L * BN2 * BK;    // 6144
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int SMEM = ST * STAGE_BYTES + 1024 + 256;
-constexpr int THREADS = 192;
-constexpr uint32_t TBUF = 256;           // TMEM column offset of the second accumulator buffer
 constexpr u64 P = (1ull << 45) - 55;
 constexpr u64 MASK45 = (1ull << 45) - 1;
 
@@ -298,172 +291,42 @@ __device__ __forceinline__ u64 mad_wide(uint32_t a, uint32_t b, u64 acc) {
     return r;
 }
 
-// (g0 + g1*2^32 + g2*2^64) mod p for g0, g1 < 2^57, g2 < 2^49
-__device__ __forceinline__ u64 combine(u64 g0, u64 g1, u64 g2) {
-    const u64 x = lz(g1);                                   // < 2^46
-    const u64 t1 = (x >> 13) * 55 + ((x & 0x1FFF) << 32);   // x*2^32: (x>>13)*2^45 + (x&8191)*2^32
-    const u64 y = lz(g2);                                   // < 2^46
-    const u64 z = (y >> 26) * 55 + ((y & 0x3FFFFFF) << 19); // y*2^19
-    const u64 t = lz(g0) + t1 + z * 55;                     // y*2^64 == y*2^19*55;  < 2^52
-    const u64 r = lz(t);
-    return r >= P ? r - P : r;
-}
-
-__global__ void __launch_bounds__(THREADS, 1)
-k_gemm_p45(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, u64 *__restrict__ out,
-           u64 out_pstride, uint32_t ohw, int O, int M, int nkb, int ntm, int ntn, int ntiles) {
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint64_t *full = reinterpret_cast<uint64_t *>(base + ST * STAGE_BYTES);
-    uint64_t *empty = full + ST;
-    uint64_t *tfull = empty + ST;        // [2]
-    uint64_t *tempty = tfull + 2;        // [2]
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < ST; s++) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
-        }
-        for (int b = 0; b < 2; b++) {
-            mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], 4);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot)));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tmem = *tmem_slot;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            // ---- TMA producer ----
-            int it = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                const int nt = t % ntn, mt = (t / ntn) % ntm, party = t / (ntn * ntm);
-                for (int kb = 0; kb < nkb; kb++, it++) {
-                    const int s = it % ST;
-                    mbar_wait(&empty[s], ((it / ST) & 1) ^ 1);
-                    mbar_arrive_expect_tx(&full[s], STAGE_BYTES);
-                    uint8_t *sa = base + s * STAGE_BYTES;
-                    tma_load_4d(sa, &tmA, &full[s], kb * BK, mt * BM, 0, party);
-                    tma_load_4d(sa + A_BYTES, &tmB, &full[s], kb * BK, nt * BN2, 0, party);
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (lane == 0) {
-            // ---- MMA issuer ----
-            constexpr uint32_t ID_ALL = idesc_i8(L * BN2), ID_HEAD = idesc_i8((L - 1) * BN2), ID_ONE = idesc_i8(BN2);
-            int it = 0, lt = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
-                const int buf = lt & 1;
-                mbar_wait(&tempty[buf], ((lt >> 1) & 1) ^ 1);
-                asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                const uint32_t dbase = tmem + (uint32_t)buf * TBUF;
-                for (int kb = 0; kb < nkb; kb++, it++) {
-                    const int s = it % ST;
-                    mbar_wait(&full[s], (it / ST) & 1);
-                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-                    const uint32_t sa = smem_u32(base + s * STAGE_BYTES);
-                    const uint32_t sb = sa + A_BYTES;
-#pragma unroll
-                    for (int kk = 0; kk < BK / UK; kk++) {
-                        const uint64_t bdesc = umma_desc_sw64(sb + kk * UK);
-                        const bool first = kb == 0 && kk == 0;
-#pragma unroll
-                        for (int i = 0; i < L; i++) {
-                            const uint64_t adesc = umma_desc_sw64(sa + i * BM * BK + kk * UK);
-                            const uint32_t d = dbase + (uint32_t)(i * BN2);
-                            if (!first) {
-                                mma_i8(d, adesc, bdesc, ID_ALL, 1u);
-                            } else if (i == 0) {
-                                mma_i8(d, adesc, bdesc, ID_ALL, 0u);
-                            } else {
-                                mma_i8(d, adesc, bdesc, ID_HEAD, 1u);
-                                mma_i8(d + (uint32_t)((L - 1) * BN2), adesc,
-                                       umma_desc_sw64(sb + (L - 1) * BN2 * BK + kk * UK), ID_ONE, 0u);
-                            }
-                        }
-                    }
-                    mma_commit(&empty[s]);
-                }
-                mma_commit(&tfull[buf]);
-            }
-        }
-    } else {
-        // ---- epilogue warps 2..5: TMEM lane quarter = warp % 4 ----
-        const int q = warp & 3;
-        const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-        int lt = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
-            const int buf = lt & 1;
-            const int nt = t % ntn, mt = (t / ntn) % ntm, party = t / (ntn * ntm);
-            mbar_wait(&tfull[buf], (lt >> 1) & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t taddr = tmem + lane_off + (uint32_t)buf * TBUF;
-            u64 g[3][BN2];
-#pragma unroll
-            for (int grp = 0; grp < 3; grp++) {
-                uint32_t r[4][16];
-#pragma unroll
-                for (int dd = 0; dd < 4; dd++)
-                    if (grp * 4 + dd < ND) {
-                        asm volatile(
-                            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                            : "=r"(r[dd][0]), "=r"(r[dd][1]), "=r"(r[dd][2]), "=r"(r[dd][3]), "=r"(r[dd][4]),
-                              "=r"(r[dd][5]), "=r"(r[dd][6]), "=r"(r[dd][7]), "=r"(r[dd][8]), "=r"(r[dd][9]),
-                              "=r"(r[dd][10]), "=r"(r[dd][11]), "=r"(r[dd][12]), "=r"(r[dd][13]), "=r"(r[dd][14]),
-                              "=r"(r[dd][15])
-                            : "r"(taddr + (uint32_t)((grp * 4 + dd) * BN2)));
-                    }
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-                for (int c = 0; c < BN2; c++) {
-                    u64 acc = 0;
-#pragma unroll
-                    for (int dd = 0; dd < 4; dd++)
-                        if (grp * 4 + dd < ND) acc = mad_wide(r[dd][c], 1u << (8 * dd), acc);
-                    g[grp][c] = acc;
-                }
-            }
-            // TMEM buffer drained: hand it back to the MMA warp before the stores
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
-            const int row = mt * BM + q * 32 + lane;
-            if (row < M) {
-                const uint32_t img = (uint32_t)row / ohw, pix = (uint32_t)row - img * ohw;
-                u64 *ob = out + (u64)party * out_pstride + ((u64)img * O + (u64)nt * BN2) * ohw + pix;
-#pragma unroll
-                for (int c = 0; c < BN2; c++)
-                    if (nt * BN2 + c < O) ob[(u64)c * ohw] = combine(g[0][c], g[1][c], g[2][c]);
-            }
-        }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
-}
-
 // ---- wide variant: 128 x 32 tiles, N = 6 x 32 = 192 per MMA (A re-read from smem 6x less
 // than with 16-wide tiles: ~107 B/clk of operand traffic per SM), one TMEM accumulator of
 // 11 x 32 = 352 columns.  Eight epilogue warps (two per TMEM lane quarter, 16 columns each)
 // drain TMEM into registers and release it BEFORE the mod-p recombination and the stores,
 // so the next tile's MMAs overlap the arithmetic and the HBM writes.
 namespace wide {
-constexpr int BNW = 32;
-constexpr int STW = 3;
-constexpr int B_BYTES_W = L * BNW * BK;                 // 12288
-constexpr int STAGE_W = A_BYTES + B_BYTES_W;
-constexpr int SMEM_W = STW * STAGE_W + 1024 + 256;
-constexpr int THREADS_W = 320;                          // TMA, MMA, 8 epilogue warps
+// Tile widths: BN = 32 (one 352-column TMEM accumulator, 3 smem stages: the MMA waits for the
+// epilogue's drain) or BN = 16 (N = 96 per MMA, two 176-column accumulators 256 columns apart,
+// 4 stages: the MMA of tile t+1 runs while the epilogue drains tile t -- what keeps the tensor
+// pipe busy when co-scheduled chain warps take most of the issue slots).
+template <int BN>
+struct Cfg {
+    static constexpr int NBUF = BN == 16 ? 2 : 1;
+    static constexpr int ST = BN == 16 ? 4 : 3;
+    static constexpr int B_BYTES = L * BN * BK;
+    static constexpr int STAGE = A_BYTES + B_BYTES;
+    static constexpr int SMEM = ST * STAGE + 1024 + 256;
+    static constexpr uint32_t TB = 256;                  // TMEM column offset of buffer 1
+};
+// Epilogue: 8 warps (two per TMEM lane quarter, 112 registers) or -- co-scheduled with the chain
+// kernels (SSN_COSCHED, see ssn_chain.cu) -- 4 warps draining 8 columns per pass at <= 80
+// registers, so one GEMM CTA (192 x 80 registers) always fits beside two chain blocks.
+#ifndef SSN_COSCHED
+#define SSN_COSCHED 0
+#endif
+#if SSN_COSCHED
+constexpr int EPI_W = 4, EPI_COLS = 8;
+#define SSN_GEMM_W_BOUNDS __maxnreg__(80)
+#else
+constexpr int EPI_W = 8, EPI_COLS = 16;
+#define SSN_GEMM_W_BOUNDS __maxnreg__(112)
+#endif
+constexpr int THREADS_W = 64 + 32 * EPI_W;              // TMA, MMA, epilogue warps
+#ifndef SSN_GEMM_BN_DEFAULT
+#define SSN_GEMM_BN_DEFAULT 32
+#endif
 
 // A operand modes: 0 = K-major limb planes [party][L][rows][Kpad] (explicit im2col / dense);
 // 1 = channel-major planes [party*L][C][B*H*W] of a 1x1 stride-1 conv input (M-major, TMA 3-D);
@@ -475,17 +338,35 @@ struct ConvGeom {
     int C, H, W, Wp, cblocks, ntf, nparty;   // ntf: 128-row tiles per image (mode 2)
 };
 
-template <int AMODE>
-__global__ void __launch_bounds__(THREADS_W, 1)
+// tcgen05.ld of NC consecutive 32-bit TMEM columns of this warp's lane quarter (NC = 8 or 16)
+template <int NC>
+__device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[NC]) {
+    if constexpr (NC == 16) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+    } else {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+                     : "r"(taddr));
+    }
+}
+
+template <int AMODE, int BN>
+__global__ void SSN_GEMM_W_BOUNDS
 k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, u64 *__restrict__ out,
             u64 out_pstride, uint32_t ohw, int O, int M, int nkb, int ntm, int ntn, int ntiles, ConvGeom geo) {
+    using C = Cfg<BN>;
+    constexpr int STW = C::ST, STAGE_W = C::STAGE, NBUF = C::NBUF;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t *full = reinterpret_cast<uint64_t *>(base + STW * STAGE_W);
     uint64_t *empty = full + STW;
-    uint64_t *tfull = empty + STW;
-    uint64_t *tempty = tfull + 1;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 1);
+    uint64_t *tfull = empty + STW;             // [NBUF]
+    uint64_t *tempty = tfull + NBUF;           // [NBUF]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + NBUF);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     if (threadIdx.x == 0) {
@@ -493,8 +374,10 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tfull, 1);
-        mbar_init(tempty, 8);
+        for (int b = 0; b < NBUF; b++) {
+            mbar_init(&tfull[b], 1);
+            mbar_init(&tempty[b], EPI_W);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -529,19 +412,21 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         tma_load_4d(sa, &tmA, &full[s], ft * BM + (dy - 1) * geo.Wp, img, cb * BK,
                                     (dx * geo.nparty + party) * L);
                     }
-                    tma_load_4d(sa + A_BYTES, &tmB, &full[s], kb * BK, nt * BNW, 0, party);
+                    tma_load_4d(sa + A_BYTES, &tmB, &full[s], kb * BK, nt * BN, 0, party);
                 }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
             constexpr uint32_t AM = AMODE ? (1u << 15) : 0u;          // A major-ness: MN for conv planes
-            constexpr uint32_t ID_ALL = idesc_i8(L * BNW) | AM, ID_HEAD = idesc_i8((L - 1) * BNW) | AM,
-                               ID_ONE = idesc_i8(BNW) | AM;
+            constexpr uint32_t ID_ALL = idesc_i8(L * BN) | AM, ID_HEAD = idesc_i8((L - 1) * BN) | AM,
+                               ID_ONE = idesc_i8(BN) | AM;
             int it = 0, lt = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
-                mbar_wait(tempty, (lt & 1) ^ 1);
+                const int buf = lt % NBUF;
+                mbar_wait(&tempty[buf], ((lt / NBUF) & 1) ^ 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                const uint32_t dbase = tmem + (uint32_t)buf * C::TB;
                 for (int kb = 0; kb < nkb; kb++, it++) {
                     const int s = it % STW;
                     mbar_wait(&full[s], (it / STW) & 1);
@@ -556,63 +441,36 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         for (int i = 0; i < L; i++) {
                             const uint64_t adesc = AMODE ? umma_desc_sw128_mn(sa + i * BM * BK + kk * UK * BM)
                                                          : umma_desc_sw64(sa + i * BM * BK + kk * UK);
-                            const uint32_t d = tmem + (uint32_t)(i * BNW);
+                            const uint32_t d = dbase + (uint32_t)(i * BN);
                             if (!first) {
                                 mma_i8(d, adesc, bdesc, ID_ALL, 1u);
                             } else if (i == 0) {
                                 mma_i8(d, adesc, bdesc, ID_ALL, 0u);
                             } else {
                                 mma_i8(d, adesc, bdesc, ID_HEAD, 1u);
-                                mma_i8(d + (uint32_t)((L - 1) * BNW), adesc,
-                                       umma_desc_sw64(sb + (L - 1) * BNW * BK + kk * UK), ID_ONE, 0u);
+                                mma_i8(d + (uint32_t)((L - 1) * BN), adesc,
+                                       umma_desc_sw64(sb + (L - 1) * BN * BK + kk * UK), ID_ONE, 0u);
                             }
                         }
                     }
                     mma_commit(&empty[s]);
                 }
-                mma_commit(tfull);
+                mma_commit(&tfull[buf]);
             }
         }
     } else {
-        // epilogue warps 2..9: TMEM lane quarter = warp % 4, column half = (warp - 2) / 4
-        const int q = warp & 3, half = (warp - 2) >> 2;
+        // epilogue warps: TMEM lane quarter = warp % 4; with 8 warps the two of a quarter take one
+        // 16-column half each, with 4 warps one warp drains all 32 columns, EPI_COLS per pass
+        const int q = warp & 3;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
+        constexpr int CPW = BN / (EPI_W / 4);               // columns per epilogue warp
+        constexpr int ECOLS = EPI_COLS < CPW ? EPI_COLS : CPW;
+        constexpr int NPASS = CPW / ECOLS;
+        const int colbase = EPI_W == 8 ? ((warp - 2) >> 2) * CPW : 0;
         int lt = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
             const int nt = t % ntn, mt = (t / ntn) % ntm, party = t / (ntn * ntm);
-            mbar_wait(tfull, lt & 1);
-            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-            const uint32_t taddr = tmem + lane_off + (uint32_t)(half * 16);
-            u64 g[3][16];
-#pragma unroll
-            for (int grp = 0; grp < 3; grp++) {
-                uint32_t r[4][16];
-#pragma unroll
-                for (int dd = 0; dd < 4; dd++)
-                    if (grp * 4 + dd < ND) {
-                        asm volatile(
-                            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-                            : "=r"(r[dd][0]), "=r"(r[dd][1]), "=r"(r[dd][2]), "=r"(r[dd][3]), "=r"(r[dd][4]),
-                              "=r"(r[dd][5]), "=r"(r[dd][6]), "=r"(r[dd][7]), "=r"(r[dd][8]), "=r"(r[dd][9]),
-                              "=r"(r[dd][10]), "=r"(r[dd][11]), "=r"(r[dd][12]), "=r"(r[dd][13]), "=r"(r[dd][14]),
-                              "=r"(r[dd][15])
-                            : "r"(taddr + (uint32_t)((grp * 4 + dd) * BNW)));
-                    }
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-                for (int c = 0; c < 16; c++) {
-                    u64 acc = 0;
-#pragma unroll
-                    for (int dd = 0; dd < 4; dd++)
-                        if (grp * 4 + dd < ND) acc = mad_wide(r[dd][c], 1u << (8 * dd), acc);
-                    g[grp][c] = acc;
-                }
-            }
-            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-            __syncwarp();
-            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(tempty)) : "memory");
             const int v = q * 32 + lane;
-            const int c0 = nt * BNW + half * 16;
             bool ok;
             uint32_t img, pix;
             if (AMODE == 2) {
@@ -627,11 +485,57 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 img = (uint32_t)row / ohw;
                 pix = (uint32_t)row - img * ohw;
             }
-            if (ok) {
-                u64 *ob = out + (u64)party * out_pstride + ((u64)img * O + (u64)c0) * ohw + pix;
+            const int buf = lt % NBUF;
+            mbar_wait(&tfull[buf], (lt / NBUF) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll 1
+            for (int pp = 0; pp < NPASS; pp++) {
+                const int cb = colbase + pp * ECOLS;
+                const uint32_t taddr = tmem + lane_off + (uint32_t)buf * C::TB + (uint32_t)cb;
+                // running lazy residue per column, folded group by group (EPI_COLS live u64
+                // instead of 3 x EPI_COLS partial sums)
+                u64 s[ECOLS];
 #pragma unroll
-                for (int c = 0; c < 16; c++)
-                    if (c0 + c < O) ob[(u64)c * ohw] = combine(g[0][c], g[1][c], g[2][c]);
+                for (int grp = 0; grp < 3; grp++) {
+                    uint32_t r[4][ECOLS];
+#pragma unroll
+                    for (int dd = 0; dd < 4; dd++)
+                        if (grp * 4 + dd < ND) tmem_ld_cols<ECOLS>(taddr + (uint32_t)((grp * 4 + dd) * BN), r[dd]);
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                    if (grp == 2 && pp == NPASS - 1) {
+                        // TMEM drained: hand it back to the MMA warp before the last fold and stores
+                        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+                        __syncwarp();
+                        if (lane == 0)
+                            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&tempty[buf])) : "memory");
+                    }
+#pragma unroll
+                    for (int c = 0; c < ECOLS; c++) {
+                        u64 acc = 0;
+#pragma unroll
+                        for (int dd = 0; dd < 4; dd++)
+                            if (grp * 4 + dd < ND) acc = mad_wide(r[dd][c], 1u << (8 * dd), acc);
+                        // acc carries weight 2^(32 grp): combine()'s fold, one group at a time
+                        if (grp == 0) {
+                            s[c] = lz(acc);                                            // < 2^46
+                        } else if (grp == 1) {
+                            const u64 x = lz(acc);
+                            s[c] += (x >> 13) * 55 + ((x & 0x1FFF) << 32);             // x * 2^32, < 2^47
+                        } else {
+                            const u64 y = lz(acc);
+                            const u64 z = (y >> 26) * 55 + ((y & 0x3FFFFFF) << 19);   // y * 2^64 = y * 2^19 * 55
+                            const u64 tt = lz(s[c] + z * 55);                         // < 2^52 before the fold
+                            s[c] = tt >= P ? tt - P : tt;
+                        }
+                    }
+                }
+                const int c0 = nt * BN + cb;
+                if (ok) {
+                    u64 *ob = out + (u64)party * out_pstride + ((u64)img * O + (u64)c0) * ohw + pix;
+#pragma unroll
+                    for (int c = 0; c < ECOLS; c++)
+                        if (c0 + c < O) ob[(u64)c * ohw] = s[c];
+                }
             }
         }
     }
@@ -641,6 +545,42 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 }
 }  // namespace wide
 }  // namespace p45
+
+// tile width of the p45 share GEMM: SSN_GEMM_BN=16 (double-buffered TMEM) or 32
+static int p45_bn() {
+    static int bn = 0;
+    if (!bn) {
+        const char *e = getenv("SSN_GEMM_BN");
+        bn = (e && atoi(e) == 32) ? 32 : (e && atoi(e) == 16) ? 16 : SSN_GEMM_BN_DEFAULT;
+    }
+    return bn;
+}
+
+template <int AMODE, int BN>
+static int launch_wide_bn(int grid, cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb, u64 *out,
+                          u64 out_pstride, uint32_t ohw, int O, int M, int nkb, int ntm, int ntn, int ntiles,
+                          p45::wide::ConvGeom geo) {
+    using namespace p45::wide;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(k_gemm_p45w<AMODE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM) !=
+            cudaSuccess)
+            return SSN_ERR_CUDA;
+        attr = true;
+    }
+    SSN_COUNT_LAUNCH();
+    k_gemm_p45w<AMODE, BN><<<grid, THREADS_W, Cfg<BN>::SMEM, st>>>(ma, mb, out, out_pstride, ohw, O, M, nkb, ntm, ntn,
+                                                                 ntiles, geo);
+    return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
+}
+
+template <int AMODE>
+static int launch_wide(int bn, int grid, cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb, u64 *out,
+                       u64 out_pstride, uint32_t ohw, int O, int M, int nkb, int ntm, int ntn, int ntiles,
+                       p45::wide::ConvGeom geo) {
+    return bn == 16 ? launch_wide_bn<AMODE, 16>(grid, st, ma, mb, out, out_pstride, ohw, O, M, nkb, ntm, ntn, ntiles, geo)
+                    : launch_wide_bn<AMODE, 32>(grid, st, ma, mb, out, out_pstride, ohw, O, M, nkb, ntm, ntn, ntiles, geo);
+}
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -697,22 +637,9 @@ int launch_tc(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int 
 int launch_p45(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int Kpad, u64 *out, u64 out_pstride,
                u64 ohw, cudaStream_t st) {
     using namespace p45;
-    static int variant = -1;            // 1: wide 128x32 tiles (default), 0: 128x16 double-buffered
-    if (variant < 0) {
-        const char *e = getenv("SSN_GEMM_VARIANT");
-        variant = (e && e[0] == '0') ? 0 : 1;
-    }
-    const int bn = variant ? wide::BNW : BN2;
+    const int bn = p45_bn();
     CUtensorMap ma, mb;
     if (make_map(&ma, a, Kpad, M, L, nparty, BM) || make_map(&mb, b, Kpad, O, L, nparty, bn)) return SSN_ERR_CUDA;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(k_gemm_p45, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM) != cudaSuccess ||
-            cudaFuncSetAttribute(wide::k_gemm_p45w<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, wide::SMEM_W) !=
-                cudaSuccess)
-            return SSN_ERR_CUDA;
-        attr = true;
-    }
     if (ohw >= (1ull << 32) || (u64)M * 1 >= (1ull << 31)) return SSN_ERR_UNSUPPORTED;
     const int ntm = (M + BM - 1) / BM, ntn = (O + bn - 1) / bn;
     const long long ntiles = (long long)ntm * ntn * nparty;
@@ -724,14 +651,8 @@ int launch_p45(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
     const int grid = (int)(ntiles < nsm ? ntiles : nsm);
-    SSN_COUNT_LAUNCH();
-    if (variant)
-        wide::k_gemm_p45w<0><<<grid, wide::THREADS_W, wide::SMEM_W, st>>>(
-            ma, mb, out, out_pstride, (uint32_t)ohw, O, M, (Kpad + BK - 1) / BK, ntm, ntn, (int)ntiles, wide::ConvGeom{});
-    else
-        k_gemm_p45<<<grid, THREADS, SMEM, st>>>(ma, mb, out, out_pstride, (uint32_t)ohw, O, M, (Kpad + BK - 1) / BK,
-                                                ntm, ntn, (int)ntiles);
-    return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
+    return launch_wide<0>(bn, grid, st, ma, mb, out, out_pstride, (uint32_t)ohw, O, M, (Kpad + BK - 1) / BK, ntm, ntn,
+                          (int)ntiles, wide::ConvGeom{});
 }
 
 static int num_sms() {
@@ -778,16 +699,8 @@ int launch_cn(const uint8_t *a, int mode, int nimg, int C, int H, int W, int Wp,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
     if (r != CUDA_SUCCESS) return SSN_ERR_CUDA;
-    if (make_map(&mb, b, Kpad, O, L, nparty, wide::BNW)) return SSN_ERR_CUDA;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(wide::k_gemm_p45w<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, wide::SMEM_W) !=
-                cudaSuccess ||
-            cudaFuncSetAttribute(wide::k_gemm_p45w<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, wide::SMEM_W) !=
-                cudaSuccess)
-            return SSN_ERR_CUDA;
-        attr = true;
-    }
+    const int bn = p45_bn();
+    if (make_map(&mb, b, Kpad, O, L, nparty, bn)) return SSN_ERR_CUDA;
     wide::ConvGeom geo{C, H, W, Wp, C / BK, 0, nparty};
     const int M = nimg * H * W;
     int ntm;
@@ -797,19 +710,16 @@ int launch_cn(const uint8_t *a, int mode, int nimg, int C, int H, int W, int Wp,
         geo.ntf = (H * Wp + BM - 1) / BM;
         ntm = nimg * geo.ntf;
     }
-    const int ntn = (O + wide::BNW - 1) / wide::BNW;
+    const int ntn = (O + bn - 1) / bn;
     const long long ntiles = (long long)ntm * ntn * nparty;
     if (ntiles >= (1ll << 31)) return SSN_ERR_UNSUPPORTED;
     const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
     const uint32_t ohw = (uint32_t)(H * W);
-    SSN_COUNT_LAUNCH();
     if (mode == 1)
-        wide::k_gemm_p45w<1><<<grid, wide::THREADS_W, wide::SMEM_W, st>>>(ma, mb, out, out_pstride, ohw, O, M, taps * geo.cblocks,
-                                                                       ntm, ntn, (int)ntiles, geo);
-    else
-        wide::k_gemm_p45w<2><<<grid, wide::THREADS_W, wide::SMEM_W, st>>>(ma, mb, out, out_pstride, ohw, O, M, taps * geo.cblocks,
-                                                                       ntm, ntn, (int)ntiles, geo);
-    return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
+        return launch_wide<1>(bn, grid, st, ma, mb, out, out_pstride, ohw, O, M, taps * geo.cblocks, ntm, ntn,
+                              (int)ntiles, geo);
+    return launch_wide<2>(bn, grid, st, ma, mb, out, out_pstride, ohw, O, M, taps * geo.cblocks, ntm, ntn, (int)ntiles,
+                          geo);
 }
 
 // ---------------------------------------------------------------- operand preparation
@@ -983,6 +893,8 @@ extern "C" int ssn_planes_shift(uint8_t *planes, uint64_t rows, int Wp, void *st
     u64 blocks = (total + 255) / 256;
     if (blocks > 148 * 64) blocks = 148 * 64;
     SSN_COUNT_LAUNCH();
+    static const bool carve_k_planes_shift = (ssn_prefer_max_smem(k_planes_shift), true);
+    (void)carve_k_planes_shift;
     k_planes_shift<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(planes, rows, Wp);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
@@ -995,6 +907,8 @@ extern "C" int ssn_planes_cn(const u64 *x, int nparty, int nimg, int C, int H, i
     u64 blocks = (total + 255) / 256;
     if (blocks > 148 * 64) blocks = 148 * 64;
     SSN_COUNT_LAUNCH();
+    static const bool carve_k_planes_cn = (ssn_prefer_max_smem(k_planes_cn), true);
+    (void)carve_k_planes_cn;
     k_planes_cn<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, nimg, C, H, W, Wp, L, planes, x_pstride, total,
                                                                      copies, nparty);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
@@ -1008,6 +922,8 @@ extern "C" int ssn_limb_split(const u64 *x, u64 rows, u64 K, u64 Kpad, int L, ui
     u64 blocks = (total + 255) / 256;
     if (blocks > 148 * 64) blocks = 148 * 64;
     SSN_COUNT_LAUNCH();
+    static const bool carve_k_limb_split = (ssn_prefer_max_smem(k_limb_split), true);
+    (void)carve_k_limb_split;
     k_limb_split<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(x, rows, K, Kpad, L, planes, x_pstride, total);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
@@ -1023,6 +939,8 @@ extern "C" int ssn_im2col_limbs(const u64 *x, int nparty, int nimg, int C, int H
     if ((Kpad + IC_K - 1) / IC_K > 65535 || nparty > 65535) return SSN_ERR_UNSUPPORTED;
     dim3 grid((unsigned)((rows + IC_ROWS - 1) / IC_ROWS), (unsigned)((Kpad + IC_K - 1) / IC_K), (unsigned)nparty);
     SSN_COUNT_LAUNCH();
+    static const bool carve_k_im2col_limbs = (ssn_prefer_max_smem(k_im2col_limbs), true);
+    (void)carve_k_im2col_limbs;
     k_im2col_limbs<<<grid, IC_THREADS, 0, (cudaStream_t)stream>>>(x, C, H, W, kh, kw, stride, pad, OH, OW, L,
                                                                   (uint32_t)rows, K, (int)Kpad, planes, x_pstride);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
