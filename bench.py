@@ -26,6 +26,7 @@ sys.path.insert(0, ROOT)
 WORKLOADS = {
     # name: (builder, k, n, verify, default batch per GPU)
     "resnet152-5pc": ("imagenet152", 3, 5, True, 64),
+    "resnet152-3pc": ("imagenet152", 2, 3, True, 64),
     "resnet50-3pc": ("imagenet50", 2, 3, False, 64),
     "resnet18-cifar-3pc": ("cifar18", 2, 3, False, 256),
     "lenet-3pc": ("reference", 2, 3, False, 16384),
@@ -38,7 +39,7 @@ SWEEP = [(256, 256, 256), (1024, 1024, 1024), (2048, 2048, 2048), (4096, 4096, 4
 # tensor-bound GEMMs overlap another's ALU-bound protocol chains (profiles/r01/README.md,
 # batch/stream sweep).  The first timed step runs the sub-batches back to back: its per-kernel
 # CUDA events give each kernel's own time for the rooflines; the remaining steps overlap.
-DEFAULT_STREAMS = {"resnet152-5pc": 2, "resnet50-3pc": 2, "resnet18-cifar-3pc": 2}
+DEFAULT_STREAMS = {"resnet152-5pc": 2, "resnet152-3pc": 2, "resnet50-3pc": 2, "resnet18-cifar-3pc": 2}
 METRIC = "ResNet-152 secure-inference images/s (5PC t=2, verification on, 224x224)"
 
 
@@ -60,59 +61,81 @@ def build_model(kind):
 def metric_for(workload):
     if workload == "resnet152-5pc":
         return METRIC
+    if workload == "resnet152-3pc":
+        return "ResNet-152 secure-inference images/s (3PC t=1, verification on, 224x224)"
     return f"{workload} secure-inference images/s"
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    """SM clocks and clock-event (throttle) reasons sampled DURING the timed region: NVML polled
+    every 20 ms from a thread (so even a sub-second timed region gets samples), nvidia-smi as
+    the fallback.  The last sample is always taken at stop()."""
+
+    NAMES = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+             "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+             "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+             "sw_power_cap": "nvmlClocksEventReasonSwPowerCap"}
 
     def __init__(self, index):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []
+        self.stop_evt = threading.Event()
+        self.nv = None
+        self.thread = None
+
+    def _sample(self):
+        nv = self.nv
+        sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+        mx = nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM)
+        mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+        self.samples.append((sm, mx, {nm for nm, attr in self.NAMES.items() if mask & getattr(nv, attr, 0)}))
+
+    def _loop(self):
+        while not self.stop_evt.wait(0.02):
+            try:
+                self._sample()
+            except Exception:
+                return
 
     def start(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self._sample()
+            self.thread = threading.Thread(target=self._loop, daemon=True)
             self.thread.start()
-        except OSError:
-            self.proc = None
-
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+        except Exception:
+            self.nv = None
 
     def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
+        if self.nv is None:
+            return self._smi_once()
+        self.stop_evt.set()
+        self.thread.join(timeout=2)
         try:
-            self.proc.wait(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-        sms, maxes, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            parts = [x.strip() for x in ln.split(",")]
-            if len(parts) < 8:
-                continue
-            try:
-                sms.append(float(parts[0]))
-                maxes.append(float(parts[1]))
-            except ValueError:
-                continue
-            for nm, v in zip(names, parts[4:8]):
-                if v.lower() == "active":
-                    reasons.add(nm)
+            self._sample()
+        except Exception:
+            pass
+        sms = [x[0] for x in self.samples]
+        reasons = sorted(set().union(*[x[2] for x in self.samples])) if self.samples else []
         return {"sm_mhz": float(np.median(sms)) if sms else None,
-                "sm_max_mhz": max(maxes) if maxes else None,
-                "reasons": sorted(reasons), "samples": len(sms)}
+                "sm_max_mhz": float(max(x[1] for x in self.samples)) if self.samples else None,
+                "reasons": reasons, "samples": len(sms), "source": "nvml, 20 ms polling"}
+
+    def _smi_once(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=10).stdout
+            parts = [x.strip() for x in out.strip().split(",")]
+            reasons = [nm for nm, v in zip(self.NAMES, parts[2:6]) if v.lower() == "active"]
+            return {"sm_mhz": float(parts[0]), "sm_max_mhz": float(parts[1]), "reasons": reasons, "samples": 1,
+                    "source": "nvidia-smi at stop (NVML unavailable)"}
+        except Exception as exc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [f"clock query failed: {exc!r}"], "samples": 0}
 
 
 def measured_peaks():
@@ -123,6 +146,22 @@ def measured_peaks():
         return d.get("hbm_gbs", 6545.3), d.get("bf16_tflops_sustained", d.get("bf16_tflops", 1653.7)), "measured sustained"
     except OSError:
         return 6650.0, 1590.0, "fallback"
+
+
+def measured_int8():
+    """Dense int8 tensor-pipe TOP/s measured on a B200 with tools/int8_peak.py (ssn_mma_peak:
+    back-to-back tcgen05.mma.kind::i8), committed as profiles/r*/int8_peak.json; None if absent."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "int8_peak.json")))
+    if not files:
+        return None
+    try:
+        with open(files[-1]) as fh:
+            d = json.load(fh)
+        return {"burst": float(d["int8_tops_burst"]), "sustained": float(d["int8_tops_sustained"]),
+                "src": os.path.relpath(files[-1], ROOT)}
+    except (OSError, KeyError, ValueError):
+        return None
 
 
 def burst_bf16():
@@ -229,7 +268,13 @@ def roofline(kstats, eng, dev_ms, bf16, hbm, src):
     chain / im2col: algorithmic HBM bytes against the measured copy bandwidth."""
     traffic = load_traffic()
     L2 = eng.limb_products()
-    peak_int8 = 2.0 * bf16
+    i8 = measured_int8()
+    if i8:                       # measured int8 tensor peak (sustained: the GEMM runs inside a long step)
+        peak_int8, peak_burst = i8["sustained"], i8["burst"]
+        peak_note = f"peak = measured sustained dense int8 ({i8['src']}: back-to-back tcgen05.mma.kind::i8)"
+    else:
+        peak_int8, peak_burst = 2.0 * bf16, 2.0 * burst_bf16()
+        peak_note = f"peak = 2 x {src} dense bf16 ({bf16} TF/s, sm_100 int8 MMA rate is 2x bf16)"
     rows = {}
     for cls, st in kstats.items():
         if not st["launches_per_step"] or cls == "gemm_simt":
@@ -239,10 +284,9 @@ def roofline(kstats, eng, dev_ms, bf16, hbm, src):
             achieved = 2.0 * L2 * st["work_per_launch"] / sec / 1e12
             r = {"bound": "tensor", "achieved": round(achieved, 1), "peak": round(peak_int8, 1), "unit": "TFLOP/s",
                  "frac": round(achieved / peak_int8, 4),
-                 "frac_vs_burst_peak": round(achieved / (2.0 * burst_bf16()), 4),
+                 "frac_vs_burst_peak": round(achieved / peak_burst, 4),
                  "field_gops": round(2.0 * st["work_per_launch"] / sec / 1e9, 1),
-                 "note": (f"int8 ops = {L2} u8 limb products x 2 x field MACs; peak = 2 x {src} dense bf16 "
-                          f"({bf16} TF/s, sm_100 int8 MMA rate is 2x bf16)")}
+                 "note": f"int8 ops = {L2} u8 limb products x 2 x field MACs; {peak_note}"}
         else:
             achieved = st["work_per_launch"] / sec / 1e9
             r = {"bound": "hbm", "achieved": round(achieved, 1), "peak": round(hbm, 1), "unit": "GB/s",
@@ -271,10 +315,24 @@ def roofline(kstats, eng, dev_ms, bf16, hbm, src):
     return dict(rows[dom], kernel_class=dom), rows
 
 
+def reference_cpu_baseline(model, k, n):
+    """The unmodified reference (baseline/_ref) timed once on this host: one full run for chain
+    models, per-op sampling for residual nets (bench_reference.py).  None if not installed."""
+    import bench_reference as br
+    ssnet, why = br.load_reference()
+    if ssnet is None:
+        return None, why
+    s_img, wall, text, rows = br.reference_step(ssnet, model, k, n)
+    return {"value": 1.0 / s_img, "unit": "images/s", "cores": 1, "kind": "reference",
+            "sample": text + "; pure Python object arithmetic under the GIL (n+1 threads, one core busy)",
+            "s_per_image": s_img, "sampling_wall_s": round(wall, 2), "per_op": rows}, None
+
+
 def gemm_reference(args):
-    """Reference arm of config 5: the oracle's exact mod-p GEMM (oracle/ssn_oracle.c, the C
-    restatement of `(w @ x) % p`, S/layers.py:252, all host threads) on a 512^3 sample,
-    extrapolated to the sweep's largest shape by MAC count."""
+    """Reference arm of config 5: the reference's own share-GEMM expression `(w @ x) % p` on
+    numpy object arrays (S/layers.py:252-254, baseline/_ref), a 96^3 sample per step; the C
+    oracle port (OpenMP, all host threads) on 512^3 is reported beside it."""
+    import bench_reference as br
     import oracle
     oracle.build()
     cores = oracle.set_threads(0)
@@ -283,46 +341,84 @@ def gemm_reference(args):
     S = 512
     a = rng.integers(0, p, size=(S, S), dtype=np.int64)
     b = rng.integers(0, p, size=(S, S), dtype=np.int64)
-    vals = []
+    t0 = time.perf_counter()
+    oracle.gemm(a, b, p)
+    port = 2.0 * S ** 3 / (time.perf_counter() - t0) / 1e9
+    ssnet, why = br.load_reference()
+    vals, walls = [], []
     for _ in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        oracle.gemm(a, b, p)
-        vals.append(2.0 * S ** 3 / (time.perf_counter() - t0) / 1e9)
+        if ssnet is not None:
+            rate, RS = br.gemm_rate(ssnet)
+            vals.append(rate / 1e9)
+        else:
+            oracle.gemm(a, b, p)
+            vals.append(2.0 * S ** 3 / (time.perf_counter() - t0) / 1e9)
+        walls.append(time.perf_counter() - t0)
     v = float(np.median(vals[args.warmup:] or vals))
-    M, N, K = SWEEP[-1]
-    return {"metric": "mod-p share GEMM field Gop/s (largest sweep shape, summed over GPUs)", "value": round(v, 3),
+    wall_ms = float(np.median(walls[args.warmup:] or walls)) * 1e3
+    if ssnet is not None:
+        cb = {"value": round(v, 4), "unit": "Gop/s", "cores": 1, "kind": "reference",
+              "sample": f"reference (w @ x) % p on {RS}^3 numpy object arrays (baseline/_ref); rate is size-independent"}
+    else:
+        cb = {"value": round(v, 4), "unit": "Gop/s", "cores": cores, "kind": "port",
+              "sample": f"oracle C exact mod-p GEMM {S}^3 (reference unavailable: {why})"}
+    cb["port"] = {"value": round(port, 3), "unit": "Gop/s", "cores": cores, "kind": "port",
+                  "sample": f"oracle/ssn_oracle.c exact mod-p GEMM {S}^3 (u128 accumulate, OpenMP)"}
+    return {"metric": "mod-p share GEMM field Gop/s (largest sweep shape, summed over GPUs)", "value": round(v, 4),
             "unit": "Gop/s", "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(2.0 * M * N * K / (v * 1e9) * 1e3, 1), "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": round(wall_ms, 1), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "u64", "data": "synthetic (uniform field elements)",
-            "config": {"workload": "gemm-sweep"},
-            "cpu_baseline": {"value": round(v, 3), "unit": "Gop/s", "cores": cores, "kind": "port",
-                             "sample": f"oracle C exact mod-p GEMM {S}^3 (u128 accumulate, OpenMP); rate is "
-                                       "size-independent, ms_per_step extrapolated to the largest shape"},
-            "e2e": {"value": round(v, 3), "unit": "Gop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "config": {"workload": "gemm-sweep"}, "cpu_baseline": cb,
+            "e2e": {"value": round(v, 4), "unit": "Gop/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
 def run_reference(args):
+    """--impl reference: the unmodified reference package through its own API
+    (bench_reference.py), rank 0 only; each step is a bounded sample (a full run for chain
+    models, per-op sampling for residual nets) and ms_per_step is the time it really took."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     if args.workload == "gemm-sweep":
         print(json.dumps(gemm_reference(args)), flush=True)
         return
+    import bench_reference as br
     name = WORKLOADS[args.workload]
     model = build_model(name[0])
     k, n, verify = name[1], name[2], name[3]
-    vals = []
+    ssnet, why = br.load_reference()
+    s_img, walls, text, rows = [], [], None, None
     for _ in range(args.warmup + args.steps):
-        vals.append(cpu_baseline_sample(model, k, n, verify, budget_s=args.cpu_budget))
-    timed = vals[args.warmup:] or vals
-    v = float(np.median([t["value"] for t in timed]))
-    cb = dict(timed[-1])
-    cb["value"] = v
+        if ssnet is not None:
+            si, wall, text, rows = br.reference_step(ssnet, model, k, n)
+        else:
+            t0 = time.perf_counter()
+            port = cpu_baseline_sample(model, k, n, verify, budget_s=args.cpu_budget)
+            si, wall, text = port["s_per_image"], time.perf_counter() - t0, port["sample"] + f" (reference unavailable: {why})"
+        s_img.append(si)
+        walls.append(wall)
+    si = float(np.median(s_img[args.warmup:] or s_img))
+    wall_ms = float(np.median(walls[args.warmup:] or walls)) * 1e3
+    v = 1.0 / si
+    if ssnet is not None:
+        cb = {"value": v, "unit": "images/s", "cores": 1, "kind": "reference",
+              "sample": text + "; pure Python object arithmetic under the GIL (n+1 threads, one core busy)",
+              "s_per_image": si, "per_op": rows}
+        try:
+            cb["port"] = cpu_baseline_sample(model, k, n, verify, budget_s=args.cpu_budget)
+        except Exception as exc:
+            cb["port"] = {"error": repr(exc)}
+    else:
+        cb = {"value": v, "unit": "images/s", "cores": port["cores"], "kind": "port", "sample": text, "s_per_image": si}
     out = {"metric": metric_for(args.workload), "value": v, "unit": "images/s", "impl": "reference",
-           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v,
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(wall_ms, 1),
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-           "data": "synthetic", "config": {"workload": args.workload, "k": k, "n": n, "verify": verify,
-                                           "batch_per_step": 1},
+           "data": "synthetic", "config": {"workload": args.workload, "k": k, "n": n, "verify": False,
+                                           "batch_per_step": 1, "s_per_image": si,
+                                           "note": ("ms_per_step is the wall time of one step's bounded sample; "
+                                                    "value is the reference's images/s extrapolated from it "
+                                                    "(bench_reference.py). The reference has no verification step.")},
            "cpu_baseline": cb,
            "e2e": {"value": v, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -354,6 +450,9 @@ def run_gemm_sweep(args):
     except (OSError, KeyError, ValueError):
         bf16, src = 1590.0, "fallback"
     peak = 2.0 * bf16
+    i8 = measured_int8()
+    if i8:                                  # GEMMs timed alone: the measured burst int8 figure
+        peak, src = i8["burst"], f"measured burst dense int8 ({i8['src']})"
     st = torch.cuda.current_stream()
 
     def rand_field(n, stream_id):
@@ -375,6 +474,8 @@ def run_gemm_sweep(args):
     tc = G.field_matmul(planes_of(a, 256, 256), planes_of(b, 256, 256), 256, 256, 256, p)   # [n][m]
     exact = bool(torch.equal(tc.t(), ref))
     rows = []
+    sampler = ClockSampler(local)
+    sampler.start()
     for (M, N, K) in SWEEP:
         A = planes_of(rand_field(M * K, 3), M, K)
         Bp = planes_of(rand_field(N * K, 4), N, K)
@@ -397,8 +498,43 @@ def run_gemm_sweep(args):
                      "int8_tops": round(L * L * fops / 1e12, 1), "frac_int8": round(L * L * fops / 1e12 / peak, 4),
                      "split_k": G.kpad(K) > G.max_k_chunk(p)})
         del A, Bp, out
+    clocks = sampler.stop()
     top = rows[-1]
     value = top["field_gops"]
+    # exactness at the headline shape (split-K): a 256 x 256 output block of the 16384^3 GEMM
+    # against the CUDA-core GEMM on the same rows/columns
+    M, N, K = SWEEP[-1]
+    Ah, Bh = rand_field(M * K, 5).reshape(M, K), rand_field(N * K, 6).reshape(N, K)
+    big = G.field_matmul(planes_of(Ah, M, K), planes_of(Bh, N, K), M, N, K, p)      # [n][m]
+    blk = torch.empty((256, 256), dtype=torch.int64, device="cuda")
+    a_blk, b_blk = Ah[:256].contiguous(), Bh[:256].contiguous()
+    _lib.call("ssn_dense_simt", _lib.ptr(b_blk), 0, _lib.ptr(a_blk), 0, _lib.ptr(blk), 0, 1, 256, 256, K, p,
+              _lib.stream_ptr())
+    exact_top = bool(torch.equal(big[:256, :256].t(), blk))
+    del big, blk
+    # end to end through the public API (gemm.field_matmul) with host buffers: pinned u64 field
+    # elements in, limb split + tcgen05 GEMM on the device, the u64 product back to the host
+    A_host, B_host = Ah.cpu().pin_memory(), Bh.cpu().pin_memory()
+    del Ah, Bh
+    C_host = torch.empty((N, M), dtype=torch.int64).pin_memory()
+    ee0, ee1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def e2e_step():
+        a_d = A_host.to("cuda", non_blocking=True)
+        b_d = B_host.to("cuda", non_blocking=True)
+        c_d = G.field_matmul(planes_of(a_d, M, K), planes_of(b_d, N, K), M, N, K, p)
+        C_host.copy_(c_d, non_blocking=True)
+    e2e_step()
+    torch.cuda.synchronize()
+    ee0.record(st)
+    for _ in range(max(1, args.steps)):
+        e2e_step()
+    ee1.record(st)
+    torch.cuda.synchronize()
+    e2e_s = ee0.elapsed_time(ee1) / max(1, args.steps) / 1e3
+    e2e = {"value": round(2.0 * M * N * K / e2e_s / 1e9, 1), "unit": "Gop/s",
+           "h2d_bytes_per_step": int(A_host.numel() * 8 + B_host.numel() * 8), "d2h_bytes_per_step": int(C_host.numel() * 8)}
+    del A_host, B_host, C_host
     reshare = reshare_microbench(args, torch, dist, _lib, p, hbm, world, rank)
     if world > 1:
         t = torch.tensor([value], dtype=torch.float64, device="cuda")
@@ -413,9 +549,15 @@ def run_gemm_sweep(args):
                            "int8_products_per_field_mac": L * L},
                 "roofline": {"bound": "tensor", "achieved": top["int8_tops"], "peak": round(peak, 1),
                              "unit": "TFLOP/s", "frac": top["frac_int8"], "traffic": None,
-                             "note": f"peak = 2 x {src} dense bf16"},
-                "gpu_launches": int(launches), "exact_vs_cuda_core_gemm": exact, "sweep": rows,
-                "reshare": reshare}
+                             "note": f"peak = {src}" if i8 else f"peak = 2 x {src} dense bf16"},
+                "gpu_launches": int(launches), "exact_vs_cuda_core_gemm": exact,
+                "exact_headline_block_vs_cuda_core_gemm": exact_top, "sweep": rows,
+                "reshare": reshare, "clocks": clocks, "e2e": e2e}
+        if not args.no_cpu_baseline:
+            try:
+                line["cpu_baseline"] = gemm_reference(argparse.Namespace(warmup=0, steps=1, gpus=1))["cpu_baseline"]
+            except Exception as exc:
+                line["cpu_baseline"] = {"value": None, "error": repr(exc)}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -640,6 +782,7 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-check", action="store_true")
+    ap.add_argument("--no-latency", action="store_true", help="skip the batch-1 latency measurement")
     ap.add_argument("--streams", type=int, default=None,
                     help="co-resident: split the batch over this many CUDA streams (GEMM/chain overlap)")
     ap.add_argument("--placement", default="coresident", choices=["coresident", "party"],
@@ -798,6 +941,29 @@ def main():
     breakdown = {}
     eng.run_device(x_dev, timings=breakdown)
 
+    # batch-1 latency (the paper's per-image setting): one image, one stream,
+    # device-resident input, CUDA events over `steps` back-to-back inferences
+    latency = None
+    if not args.no_latency:
+        first = getattr(eng, "engines", [eng])[0]
+        e1eng = BatchedEngine(model, scheme, batch=1, seed=7 + rank, verify=verify, share_weights_with=first)
+        e1eng.defer_verify = True
+        x1 = x_dev[:1].contiguous()
+        for _ in range(max(args.warmup, 2)):
+            e1eng.run_device(x1)
+        torch.cuda.synchronize()
+        l_0, l_1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        nlat = max(args.steps, 5)
+        l_0.record(stream)
+        for _ in range(nlat):
+            e1eng.run_device(x1)
+        l_1.record(stream)
+        torch.cuda.synchronize()
+        lat_ms = l_0.elapsed_time(l_1) / nlat
+        latency = {"batch": 1, "streams": 1, "steps": nlat, "ms_per_image": round(lat_ms, 3),
+                   "s_per_image": round(lat_ms / 1e3, 6), "images_per_s": round(1e3 / lat_ms, 2)}
+        del e1eng
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -811,9 +977,17 @@ def main():
     cpu = None
     if not args.no_cpu_baseline and world == 1:          # the CPU baseline is an N=1 figure
         try:
-            cpu = cpu_baseline_sample(model, k, n, verify, budget_s=args.cpu_budget)
+            port = cpu_baseline_sample(model, k, n, verify, budget_s=args.cpu_budget)
         except Exception as exc:       # reported, never silently replaced
-            cpu = {"value": None, "error": repr(exc)}
+            port = {"value": None, "error": repr(exc)}
+        try:
+            cpu, why = reference_cpu_baseline(model, k, n)
+        except Exception as exc:
+            cpu, why = None, repr(exc)
+        if cpu is None:
+            cpu = dict(port, reference_unavailable=why)
+        else:
+            cpu["port"] = port
     line = {
         "metric": metric_for(args.workload), "value": round(value, 3), "unit": "images/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(dev_ms, 3), "higher_is_better": True,
@@ -822,7 +996,7 @@ def main():
                    "batch_per_gpu": B, "global_batch": imgs, "parallelism": f"dp{world} x co-resident {n} parties",
                    "rng": "device philox", "l2": "working set >> 126 MB L2 (inputs larger than L2)",
                    "streams_per_gpu": nstreams, "batch_latency_ms": round(dev_ms, 3),
-                   "s_per_image": round(dev_ms / 1000.0 / B, 6)},
+                   "inverse_throughput_s_per_image": round(dev_ms / 1000.0 / B, 6)},
         "e2e": {"value": round(e2e, 3), "unit": "images/s",
                 "h2d_bytes_per_step": int(x_host.numel() * 8), "d2h_bytes_per_step": int(out_host.numel() * 8)},
         "gpu_launches": int(launches),
@@ -834,6 +1008,7 @@ def main():
         "clocks": clocks,
         "outputs_match_plaintext": outputs_match,
         "comm_per_image_GB": {"online": round(online * 8 / 1e9, 3), "offline_masks": round(offline * 8 / 1e9, 3)},
+        "latency_batch1": latency,
         "breakdown_ms_per_step": {kk: round(v, 3) for kk, v in breakdown.items()},
     }
     print(json.dumps(line), flush=True)

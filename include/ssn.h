@@ -269,6 +269,12 @@ int ssn_inv_table(uint64_t *table, uint64_t n, uint64_t p, void *stream);
  * power of two (masked uniform draws) and small-rational protocol constants; else 0. */
 int ssn_chain_supported(int k, int n, const uint64_t *ids, uint64_t p);
 
+/* Measurement only (no reference counterpart): the dense int8 tensor-pipe rate.  `ctas` CTAs
+ * (one per SM) each issue `iters` back-to-back tcgen05.mma.kind::i8 of 128 x 256 x 32 from
+ * resident shared-memory tiles; *ms = device time of that launch, *int8_ops = 2*M*N*K*iters*ctas.
+ * The share GEMM's roofline (bench.py) divides by this measured peak.  Synchronises `stream`. */
+int ssn_mma_peak(int iters, int ctas, float *ms, double *int8_ops, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

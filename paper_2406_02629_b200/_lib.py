@@ -79,6 +79,7 @@ _SIGS = {
     "ssn_layer_chain": [_P, _P],
     "ssn_gemm_tc_conv": [_P, _I32, _I32, _I32, _I32, _I32, _I32, _P, _I32, _I32, _P, _U64, _U64, _P],
     "ssn_planes_shift": [_P, _U64, _I32, _P],
+    "ssn_mma_peak": [_I32, _I32, _P, _P, _P],
     "ssn_planes_cn": [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _U64, _I32, _P],
     "ssn_chain_supported": [_I32, _I32, _P, _U64],
     "ssn_inv_table": [_P, _U64, _U64, _P],

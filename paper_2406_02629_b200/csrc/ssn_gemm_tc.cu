@@ -722,6 +722,49 @@ int launch_cn(const uint8_t *a, int mode, int nimg, int C, int H, int W, int Wp,
                           geo);
 }
 
+// ---------------------------------------------------------------- int8 tensor-pipe peak probe
+// One CTA per SM issues back-to-back tcgen05.mma.kind::i8 of 128 x 256 x 32 from one resident
+// smem tile pair into one TMEM accumulator (no global traffic, no epilogue): the measured dense
+// int8 rate that the share GEMM's roofline divides by (bench.py, MEASURED_INT8.json).
+__global__ void __launch_bounds__(128, 1) k_mma_peak(int iters, unsigned long long *sink) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // A 128 x 32 B and B 256 x 32 B, K-major SW64 tiles (contents irrelevant for throughput)
+    uint64_t *bar = reinterpret_cast<uint64_t *>(base + 128 * 64 + 256 * 64);
+    uint32_t *slot = reinterpret_cast<uint32_t *>(bar + 1);
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < (128 + 256) * 64 / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(base)[i] = i;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *slot;
+    if (threadIdx.x == 0) {
+        const uint64_t ad = umma_desc_sw64(smem_u32(base)), bd = umma_desc_sw64(smem_u32(base + 128 * 64));
+        constexpr uint32_t ID = idesc_i8(256);
+        for (int i = 0; i < iters; i++) mma_i8(tmem, ad, bd, ID, i > 0 ? 1u : 0u);
+        mma_commit(bar);
+        mbar_wait(bar, 0);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t r[8];
+        tmem_ld8(tmem + ((uint32_t)(threadIdx.x & 31) << 16), r);
+        if (threadIdx.x == 0) atomicAdd(sink, (unsigned long long)r[0]);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
 // ---------------------------------------------------------------- operand preparation
 // x: [P][rows][K] u64 (row-major) -> planes [P][L][rows][Kpad] u8, zero padded in K.
 __global__ void k_limb_split(const u64 *__restrict__ x, u64 rows, u64 K, u64 Kpad, int L, uint8_t *__restrict__ planes,
@@ -969,4 +1012,29 @@ extern "C" int ssn_gemm_tc(const uint8_t *a_planes, const uint8_t *b_planes, int
         case 8: return launch_tc<8>(a_planes, b_planes, nparty, M, O, (int)Kpad, out, out_pstride, ohw, p, st);
         default: return SSN_ERR_UNSUPPORTED;
     }
+}
+
+extern "C" int ssn_mma_peak(int iters, int ctas, float *ms, double *int8_ops, void *stream) {
+    if (iters < 1 || ctas < 1 || !ms || !int8_ops) return SSN_ERR_ARG;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int smem = (128 + 256) * 64 + 1024 + 64;
+    if (cudaFuncSetAttribute(k_mma_peak, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return SSN_ERR_CUDA;
+    unsigned long long *sink = nullptr;
+    if (cudaMallocAsync(&sink, sizeof(*sink), st) != cudaSuccess) return SSN_ERR_CUDA;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_mma_peak<<<ctas, 128, smem, st>>>(2, sink);          // warm-up
+    cudaEventRecord(e0, st);
+    SSN_COUNT_LAUNCH();
+    k_mma_peak<<<ctas, 128, smem, st>>>(iters, sink);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFreeAsync(sink, st);
+    *int8_ops = 2.0 * 128 * 256 * 32 * (double)iters * ctas;
+    return cudaStreamSynchronize(st) == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
