@@ -158,23 +158,9 @@ class DistTransport:
 
 
 def mask_bundle_decoder(scheme, device):
-    """Inverse of MaskBundle.encode (S/protocol.py:324-351) onto `device`."""
+    """MASK_DIST payload -> MaskBundle on `device` (MaskBundle.decode, S/protocol.py:337-351)."""
     from .protocol import MaskBundle
-    from .sss import ShareTensor
-
-    def decode(blob):
-        (hlen,) = struct.unpack_from("<I", blob, 0)
-        meta = json.loads(blob[4:4 + hlen].decode())
-        off = 4 + hlen
-        b = MaskBundle()
-        for m in meta:
-            n = int(np.prod(m["shape"])) if m["shape"] else 1
-            arr = np.frombuffer(blob, dtype="<u8", count=n, offset=off).astype(np.int64).reshape(m["shape"])
-            off += 8 * n
-            vals = torch.as_tensor(arr, device=device)
-            b.put(m["op"], m["name"], ShareTensor(m["party_id"], m["degree"], vals, scheme))
-        return b
-    return decode
+    return lambda blob: MaskBundle.decode(blob, scheme, device)
 
 
 def transcript_digest(frames_by_rank):

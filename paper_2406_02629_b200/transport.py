@@ -7,7 +7,9 @@ Payloads are device tensors instead of bytes:
 * DeviceHub / DeviceTransport: all parties co-resident on one GPU; a send hands the
   receiver the producer's HBM buffer (the send buffer IS the receive buffer).  Ordering is
   stream order: every party enqueues on the same CUDA stream.
-* NcclTransport (transport_nccl.py): one party per GPU, torch.distributed send/recv.
+* DistTransport (dist.py): one party per process over torch.distributed (the API path), and
+  the grouped NCCL hops of PartyShardedEngine (sharded.py, the NVLink throughput path).
+* TcpTransport (tcp.py): cross-host parties over the reference's own TCP wire protocol.
 
 A DeviceHub created with record=True serializes every message into the reference frame
 format so the canonical transcript (S/transport.py:68-80) can be compared byte for byte.
