@@ -684,10 +684,13 @@ def reshare_microbench(args, torch, dist, _lib, p, hbm, world, rank):
 
 def run_party_placement(args):
     """Party-per-GPU placement (sharded.PartyShardedEngine): ranks [g*(n+1), (g+1)*(n+1)) form
-    group g (source + n parties); leftover ranks idle.  value = G*B images / max-over-ranks step."""
+    group g (trusted source + n parties, elite rotating over the front ranks); the GPUs no group
+    uses each run a co-resident replica (all n parties on one GPU, its own batch) so no GPU
+    idles.  value = (G*B + L*B_co) images / max-over-ranks step time."""
     import torch
     import torch.distributed as dist
     from paper_2406_02629_b200 import _lib, resnet
+    from paper_2406_02629_b200.batched import BatchedEngine, StreamPipelinedEngine
     from paper_2406_02629_b200.field import PrimeField
     from paper_2406_02629_b200.sharded import PartyShardedEngine
     from paper_2406_02629_b200.sss import SssScheme
@@ -701,6 +704,7 @@ def run_party_placement(args):
     torch.cuda.set_device(local)
     kind, k, n, verify, dflt_batch = WORKLOADS[args.workload]
     groups = world // (n + 1)
+    leftover = world - groups * (n + 1)
     if groups < 1:
         if rank == 0:
             print(json.dumps({"metric": metric_for(args.workload), "unavailable":
@@ -714,23 +718,32 @@ def run_party_placement(args):
     model = build_model(kind)
     scheme = SssScheme(PrimeField(), k, n)
     g = rank // (n + 1)
-    eng = PartyShardedEngine(model, scheme, batch=B, seed=7 + g, verify=verify, group=g) if g < groups else None
+    in_group = g < groups
+    if in_group:
+        eng = PartyShardedEngine(model, scheme, batch=B, seed=7 + g, verify=verify, group=g)
+    else:                                   # a leftover GPU: co-resident replica
+        ns = DEFAULT_STREAMS.get(args.workload, 1)
+        eng = (StreamPipelinedEngine(model, scheme, batch=B, streams=ns, seed=7 + rank, verify=verify) if ns > 1
+               else BatchedEngine(model, scheme, batch=B, seed=7 + rank, verify=verify))
+        for e in getattr(eng, "engines", [eng]):
+            e.defer_verify = True
     # a collective before the first point-to-point call creates the NCCL communicator on every
     # rank (batch_isend_irecv as the first call of a group must otherwise involve all ranks)
     dist.barrier()
-    xb = (model.random_inputs(seed=100 + g, batch=B) if hasattr(model, "random_inputs")
+    xb = (model.random_inputs(seed=100 + rank, batch=B) if hasattr(model, "random_inputs")
           else np.stack([__import__("paper_2406_02629_b200.model", fromlist=["random_input"])
-                         .random_input(100 + g, model, index=i)[0] for i in range(B)]))
+                         .random_input(100 + rank, model, index=i)[0] for i in range(B)]))
+    if in_group:
+        xb = (model.random_inputs(seed=100 + g, batch=B) if hasattr(model, "random_inputs") else xb)
     x_dev = torch.as_tensor(xb, device="cuda")
     outputs_match = None
-    if eng is not None and not args.no_check:
+    if not args.no_check:
         got = eng.run(xb)
-        if eng.role == 1:
-            want = resnet.plaintext_forward(model, xb, device="cuda")[0] if hasattr(model, "nodes") else None
-            outputs_match = bool(np.array_equal(got, want)) if want is not None else None
+        if (not in_group or eng.role == 1) and hasattr(model, "nodes"):
+            want = resnet.plaintext_forward(model, xb, device="cuda")[0]
+            outputs_match = bool(np.array_equal(got, want))
     for _ in range(args.warmup):
-        if eng is not None:
-            eng.run_device(x_dev)
+        eng.run_device(x_dev)
     torch.cuda.synchronize()
     dist.barrier()
     sampler = ClockSampler(local)
@@ -739,8 +752,7 @@ def run_party_placement(args):
     l0 = _lib.launch_count()
     e0.record()
     for _ in range(args.steps):
-        if eng is not None:
-            eng.run_device(x_dev)
+        eng.run_device(x_dev)
     e1.record()
     torch.cuda.synchronize()
     dist.barrier()
@@ -756,15 +768,16 @@ def run_party_placement(args):
     checked = int(m[1].item())
     match = None if checked == 0 else int(m[0].item()) == checked
     if rank == 0:
-        imgs = groups * B
+        imgs = groups * B + leftover * B
         line = {"metric": metric_for(args.workload), "value": round(imgs / (ms / 1e3), 3), "unit": "images/s",
                 "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
                 "data": "synthetic",
                 "config": {"workload": args.workload, "model": model.name, "k": k, "n": n, "verify": verify,
-                           "placement": f"party-per-GPU: {groups} group(s) x (source + {n} parties), "
-                                        f"{world - groups * (n + 1)} idle",
-                           "batch_per_group": B, "global_batch": imgs, "parallelism": f"party{n + 1} x dp{groups}"},
+                           "placement": (f"party-per-GPU: {groups} group(s) x (source + {n} parties, elite rotating "
+                                         f"over the {k} front ranks) + {leftover} co-resident replica GPU(s)"),
+                           "batch_per_group": B, "global_batch": imgs,
+                           "parallelism": f"party{n + 1} x dp{groups} + coresident x {leftover}"},
                 "gpu_launches": int(nl.item()), "gpu_launches_scope": "summed over ranks, per step",
                 "clocks": clocks, "outputs_match_plaintext": match}
         print(json.dumps(line), flush=True)

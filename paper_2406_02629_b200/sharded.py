@@ -18,7 +18,11 @@ ONLY its own party's shares, and every message crosses a process boundary:
                             (S/layers.py:326-380); output: OUTPUT_SHARE (S/protocol.py:289-305).
 
 Each protocol hop is one grouped batch_isend_irecv (ncclGroupStart / ncclSend / ncclRecv /
-ncclGroupEnd) over all of the rank's peers for that hop.  A world of G*(n+1) ranks runs G
+ncclGroupEnd) over all of the rank's peers for that hop.  The elite role of the masked
+truncations and nonlinearities rotates over the front ranks op by op (rotate_elite, default on;
+any front rank can reconstruct over the same front ids, S/sss.py:172-194), so the elite's
+extra receives, reconstructions and fan-out sends -- and its NVLink ingress -- are spread
+over k GPUs instead of landing on rank 1; the final output is still collected at rank 1.  A world of G*(n+1) ranks runs G
 independent groups, each on its own image batch (data parallel over images, SURVEY.md
 section 8e placement 2).  Decoded outputs equal the reference / integer plaintext exactly.
 """
@@ -38,8 +42,9 @@ from .rng import DeviceRng
 
 
 class PartyShardedEngine:
-    def __init__(self, model, scheme, batch, seed=7, verify=False, ordering="ltn", group=0):
+    def __init__(self, model, scheme, batch, seed=7, verify=False, ordering="ltn", group=0, rotate_elite=True):
         self.model, self.scheme, self.batch, self.seed, self.verify = model, scheme, int(batch), seed, verify
+        self.rotate_elite = rotate_elite
         self.k, self.n = scheme.k, scheme.n
         self.m = 2 * self.k - 1
         self.p = scheme.field.p
@@ -214,15 +219,19 @@ class PartyShardedEngine:
         del X
         remaining = {i: len(c) for i, c in self.cons.items()}
         result = None
+        masked_ops = 0
         for idx, op in enumerate(self.ops):
             src = idx - 1 if op.src is None else op.src
             xin = vals.get(src)
+            if op.kind in ("truncation", "nonlinear"):
+                e = masked_ops % k if self.rotate_elite else 0          # this op's elite (front index)
+                masked_ops += 1
             if op.kind == "linear":
                 y = self._linear(op, xin, prng)
             elif op.kind == "truncation":
-                y = self._truncation(op, xin, prng)
+                y = self._truncation(op, xin, prng, e)
             elif op.kind == "nonlinear":
-                y = self._nonlinear(op, xin)
+                y = self._nonlinear(op, xin, e)
             elif op.kind == "add":
                 other = vals.get(op.src2)
                 y = None
@@ -301,7 +310,8 @@ class PartyShardedEngine:
                   _lib.ptr(bias), 0, ohw, O, None, 0, _lib.ptr(Y), 0, N, 1, p, _lib.stream_ptr())
         return Y
 
-    def _truncation(self, op, X, prng):
+    def _truncation(self, op, X, prng, e=0):
+        """S/layers.py:277-323 with front rank e+1 as the elite."""
         B, n, k, t, p = self.batch, self.n, self.k, self.t, self.p
         N = B * _count(op.in_shape)
         A = self._recv_new(0, (N,))
@@ -311,24 +321,27 @@ class PartyShardedEngine:
         if t < senders:
             masked = torch.empty(N, dtype=torch.int64, device=self.dev)
             self._ew(0, X, A, masked, N)
-        FR = torch.empty((n if t == 0 else 1, N), dtype=torch.int64, device=self.dev)
-        if t == 0:                                                       # elite
-            PTS = torch.empty((senders, N), dtype=torch.int64, device=self.dev)
-            self._exchange([], [(j + 1, PTS[j]) for j in range(1, senders)])
-            PTS[0].copy_(masked)
+        FR = torch.empty((n if t == e else 1, N), dtype=torch.int64, device=self.dev)
+        if t == e:                                                       # elite
+            PTS = torch.empty((senders, N), dtype=torch.int64, device=self.dev)   # points in id order
+            self._exchange([], [(j + 1, PTS[j]) for j in range(senders) if j != e])
+            PTS[e].copy_(masked)
             _lib.call("ssn_trunc_elite", _lib.ptr(PTS), N, senders, k, _lib.u64_array(self.w_front),
                       _lib.u64_array(self.ext), op.value_bound, op.r, op.divisor, None, prng.seed,
                       prng.next_stream(), k - 1, self.ids_all, n, _lib.ptr(FR), N,
                       _lib.ptr(self.fail) if self.verify else None, N, p, _lib.stream_ptr())
-            self._exchange([(o + 1, FR[o]) for o in range(1, n)], [])     # SHARE_DIST
+            self._exchange([(o + 1, FR[o]) for o in range(n) if o != e], [])     # SHARE_DIST
+            own = FR[e]
         else:
-            self._exchange([(1, masked)] if masked is not None else [], [])    # TRUNC_MASKED
-            self._exchange([], [(1, FR[0])])
+            self._exchange([(e + 1, masked)] if masked is not None else [], [])   # TRUNC_MASKED
+            self._exchange([], [(e + 1, FR[0])])
+            own = FR[0]
         Y = torch.empty((B,) + tuple(op.out_shape), dtype=torch.int64, device=self.dev)
-        self._ew(0, FR[0], Cm, Y, N)
+        self._ew(0, own, Cm, Y, N)
         return Y
 
-    def _nonlinear(self, op, X):
+    def _nonlinear(self, op, X, e=0):
+        """S/layers.py:326-380 with participant e+1 (a front rank) as the elite."""
         B, n, k, m, t, p = self.batch, self.n, self.k, self.m, self.t, self.p
         n_in, n_out = B * _count(op.in_shape), B * _count(op.out_shape)
         BETA = self._recv_new(0, (n_in,))
@@ -340,17 +353,17 @@ class PartyShardedEngine:
             MK = torch.empty(n_in, dtype=torch.int64, device=self.dev)
             self._ew(2, X, BETA, MK, n_in)
         plain = torch.empty(n_out, dtype=torch.int64, device=self.dev)
-        if t == 0:
+        if t == e:
             PTS = torch.empty((m, n_in), dtype=torch.int64, device=self.dev)
-            self._exchange([], [(j + 1, PTS[j]) for j in range(1, m)])       # NONLIN_MASKED
-            PTS[0].copy_(MK)
+            self._exchange([], [(j + 1, PTS[j]) for j in range(m) if j != e])   # NONLIN_MASKED
+            PTS[e].copy_(MK)
             _lib.call("ssn_nonlin_elite", _lib.ptr(PTS), n_in, m, _lib.u64_array(self.w_part), int(bool(op.relu)),
                       kind, B, c, h, w, kh, kw, _lib.ptr(plain), p, _lib.stream_ptr())
-            self._exchange([(o + 1, plain) for o in range(1, fan)], [])     # NONLIN_PLAIN
+            self._exchange([(o + 1, plain) for o in range(fan) if o != e], [])  # NONLIN_PLAIN
         else:
-            self._exchange([(1, MK)] if MK is not None else [], [])
+            self._exchange([(e + 1, MK)] if MK is not None else [], [])
             if t < fan:
-                self._exchange([], [(1, plain)])
+                self._exchange([], [(e + 1, plain)])
         if t >= fan:
             return None
         Y = torch.empty((B,) + tuple(op.out_shape), dtype=torch.int64, device=self.dev)

@@ -92,3 +92,55 @@ def test_dist_transport_gloo(world):
     # elements: 12 + 3 + 3 per peer, + 2 for the divergent share
     assert out[0]["sent"][0] == (world - 1) * 18 + 2
     assert out[0]["frames"][(0, 1)] == 4
+
+
+class _HopStub:
+    """The plumbing PartyShardedEngine._exchange needs (host-staged gloo, group base 0)."""
+    nccl = False
+    base = 0
+
+    def _g(self, role):
+        return self.base + role
+
+
+def _hop_worker(rank, port, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=2, timeout=datetime.timedelta(seconds=90))
+    from paper_2406_02629_b200.sharded import PartyShardedEngine
+    try:
+        other = 1 - rank
+        # reshare step 1's pattern: BOTH ranks send a large buffer to the other before either
+        # receives -- one grouped hop must complete without deadlock and keep per-peer order
+        big = [torch.arange(1 << 20, dtype=torch.int64) * (rank + 1) + i for i in range(3)]
+        outs = [torch.empty(1 << 20, dtype=torch.int64) for _ in range(3)]
+        PartyShardedEngine._exchange(_HopStub(), [(other, t) for t in big], [(other, o) for o in outs])
+        ok = all(torch.equal(outs[i], torch.arange(1 << 20, dtype=torch.int64) * (other + 1) + i) for i in range(3))
+        # a hop with only sends on one side and only receives on the other (SHARE_DIST shape)
+        buf = torch.empty(7, dtype=torch.int64)
+        if rank == 0:
+            PartyShardedEngine._exchange(_HopStub(), [(1, torch.full((7,), 42, dtype=torch.int64))], [])
+        else:
+            PartyShardedEngine._exchange(_HopStub(), [], [(0, buf)])
+            ok = ok and buf.tolist() == [42] * 7
+        q.put((rank, ok))
+    except BaseException as exc:
+        q.put((rank, repr(exc)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_grouped_hop_exchange_gloo_world2():
+    """PartyShardedEngine._exchange (one batch_isend_irecv per protocol hop) on CPU gloo."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_hop_worker, args=(r, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(60)
+    assert res == {0: True, 1: True}, res
