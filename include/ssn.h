@@ -269,6 +269,24 @@ int ssn_inv_table(uint64_t *table, uint64_t n, uint64_t p, void *stream);
  * power of two (masked uniform draws) and small-rational protocol constants; else 0. */
 int ssn_chain_supported(int k, int n, const uint64_t *ids, uint64_t p);
 
+/* sss_linear's local product fused with reshare step 1 (S/layers.py:245-255 then
+ * S/protocol.py:154-164, RESHARE_OUT): the tcgen05 share GEMM of ssn_gemm_tc (p = 2^45 - 55,
+ * K-major limb planes, Kpad within one exact pass) whose epilogue, instead of the product y of
+ * party `pt`, writes its nf sub-shares  y + sum_{e<km1} c_e * front_ids[f]^(e+1)  to
+ *   sub[pt * party_stride + f * front_stride + (img*O + o)*ohw + pix]
+ * -- the per-destination send buffers of the first reshare hop.  c_e are drawn exactly as
+ * ssn_gen draws them for (seed, stream + pt) (bit-identical to GEMM + ssn_gen). */
+typedef struct {
+    uint64_t *sub;
+    uint64_t party_stride, front_stride;
+    uint64_t seed, stream;
+    int km1, nf;
+    const uint64_t *front_ids;
+} ssn_subshare_desc;
+
+int ssn_gemm_tc_subshares(const uint8_t *a_planes, const uint8_t *b_planes, int nparty, int M, int O, uint64_t Kpad,
+                          uint64_t ohw, const ssn_subshare_desc *desc, uint64_t p, void *stream);
+
 /* Measurement only (no reference counterpart): the dense int8 tensor-pipe rate.  `ctas` CTAs
  * (one per SM) each issue `iters` back-to-back tcgen05.mma.kind::i8 of 128 x 256 x 32 from
  * resident shared-memory tiles; *ms = device time of that launch, *int8_ops = 2*M*N*K*iters*ctas.

@@ -80,6 +80,7 @@ _SIGS = {
     "ssn_gemm_tc_conv": [_P, _I32, _I32, _I32, _I32, _I32, _I32, _P, _I32, _I32, _P, _U64, _U64, _P],
     "ssn_planes_shift": [_P, _U64, _I32, _P],
     "ssn_mma_peak": [_I32, _I32, _P, _P, _P],
+    "ssn_gemm_tc_subshares": [_P, _P, _I32, _I32, _I32, _U64, _U64, _P, _U64, _P],
     "ssn_planes_cn": [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _U64, _I32, _P],
     "ssn_chain_supported": [_I32, _I32, _P, _U64],
     "ssn_inv_table": [_P, _U64, _U64, _P],
@@ -157,6 +158,13 @@ def call(name, *args):
         if rc == SSN_ERR_ARG:
             raise ValueError(f"{name}: invalid arguments")
         raise SsnKernelError(f"{name} failed with code {rc}")
+
+
+class SubshareDesc(ctypes.Structure):
+    """ssn_subshare_desc (include/ssn.h)."""
+    _fields_ = [("sub", ctypes.c_uint64), ("party_stride", ctypes.c_uint64), ("front_stride", ctypes.c_uint64),
+                ("seed", ctypes.c_uint64), ("stream", ctypes.c_uint64), ("km1", ctypes.c_int), ("nf", ctypes.c_int),
+                ("front_ids", ctypes.c_uint64)]
 
 
 def stream_ptr():

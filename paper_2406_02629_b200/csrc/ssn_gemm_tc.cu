@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include "ssn_field.cuh"
+#include "ssn_lincomb.cuh"
 #include "ssn.h"
 
 namespace {
@@ -338,6 +339,19 @@ struct ConvGeom {
     int C, H, W, Wp, cblocks, ntf, nparty;   // ntf: 128-row tiles per image (mode 2)
 };
 
+// Reshare step 1 fused into the epilogue (SUB instantiation): instead of the product y of
+// party `party`, write its nf RESHARE_OUT sub-shares  y + sum_e c_e * id_f^(e+1)  (front ranks
+// f < nf, S/protocol.py:154-164) straight into the per-destination send buffers
+//   sub[party * sub_pstride + f * sub_fstride + element],
+// drawing c_e exactly as ssn_gen does (Philox4x32-10 of (seed, stream + party, element,
+// 0x800 | pair), masked 45-bit words), so the fused and unfused paths are bit-identical.
+struct EpiSub {
+    u64 *sub;
+    u64 sub_pstride, sub_fstride, seed, stream;
+    int km1, nf;
+    uint32_t pw[SSN_MAXK][SSN_MAXK];        // front id powers id_f^(e+1) (small, p45)
+};
+
 // tcgen05.ld of NC consecutive 32-bit TMEM columns of this warp's lane quarter (NC = 8 or 16)
 template <int NC>
 __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[NC]) {
@@ -354,10 +368,11 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[NC]) 
     }
 }
 
-template <int AMODE, int BN>
+template <int AMODE, int BN, bool SUB = false>
 __global__ void SSN_GEMM_W_BOUNDS
 k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, u64 *__restrict__ out,
-            u64 out_pstride, uint32_t ohw, int O, int M, int nkb, int ntm, int ntn, int ntiles, ConvGeom geo) {
+            u64 out_pstride, uint32_t ohw, int O, int M, int nkb, int ntm, int ntn, int ntiles, ConvGeom geo,
+            const __grid_constant__ EpiSub es) {
     using C = Cfg<BN>;
     constexpr int STW = C::ST, STAGE_W = C::STAGE, NBUF = C::NBUF;
     extern __shared__ uint8_t smem_raw[];
@@ -531,10 +546,39 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                 }
                 const int c0 = nt * BN + cb;
                 if (ok) {
-                    u64 *ob = out + (u64)party * out_pstride + ((u64)img * O + (u64)c0) * ohw + pix;
+                    const u64 e0 = ((u64)img * O + (u64)c0) * ohw + pix;     // element index in [img][O][ohw]
+                    if constexpr (SUB) {
+                        u64 *sb = es.sub + (u64)party * es.sub_pstride + e0;
+#pragma unroll 1
+                        for (int c = 0; c < ECOLS; c++) {
+                            if (c0 + c >= O) break;
+                            const u64 i = e0 + (u64)c * ohw;
+                            u64 cf[SSN_MAXK];
 #pragma unroll
-                    for (int c = 0; c < ECOLS; c++)
-                        if (c0 + c < O) ob[(u64)c * ohw] = s[c];
+                            for (int jp = 0; jp < SSN_MAXK / 2; jp++)
+                                if (2 * jp < es.km1) {
+                                    const ssn_u4 r = ssn_philox_at(es.seed, es.stream + party, i, 0x800u | jp);
+                                    const u64 x0 = (((u64)r.x << 32) | r.y) & MASK45, x1 = (((u64)r.z << 32) | r.w) & MASK45;
+                                    cf[2 * jp] = x0 >= P ? x0 - P : x0;
+                                    cf[2 * jp + 1] = x1 >= P ? x1 - P : x1;
+                                }
+#pragma unroll 1
+                            for (int f = 0; f < es.nf; f++) {
+                                u64 acc = s[c];
+#pragma unroll
+                                for (int e = 0; e < SSN_MAXK; e++)
+                                    if (e < es.km1) acc += ((u64)(uint32_t)(cf[e] >> 32) * es.pw[f][e] << 32) +
+                                                           (u64)(uint32_t)cf[e] * es.pw[f][e];
+                                const u64 t = lz(acc);
+                                sb[(u64)f * es.sub_fstride + (u64)c * ohw] = t >= P ? t - P : t;
+                            }
+                        }
+                    } else {
+                        u64 *ob = out + (u64)party * out_pstride + e0;
+#pragma unroll
+                        for (int c = 0; c < ECOLS; c++)
+                            if (c0 + c < O) ob[(u64)c * ohw] = s[c];
+                    }
                 }
             }
         }
@@ -556,30 +600,39 @@ static int p45_bn() {
     return bn;
 }
 
-template <int AMODE, int BN>
+template <int AMODE, int BN, bool SUB = false>
 static int launch_wide_bn(int grid, cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb, u64 *out,
                           u64 out_pstride, uint32_t ohw, int O, int M, int nkb, int ntm, int ntn, int ntiles,
-                          p45::wide::ConvGeom geo) {
+                          p45::wide::ConvGeom geo, const p45::wide::EpiSub &es) {
     using namespace p45::wide;
     static bool attr = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(k_gemm_p45w<AMODE, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM) !=
-            cudaSuccess)
+        if (cudaFuncSetAttribute(k_gemm_p45w<AMODE, BN, SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 Cfg<BN>::SMEM) != cudaSuccess)
             return SSN_ERR_CUDA;
         attr = true;
     }
     SSN_COUNT_LAUNCH();
-    k_gemm_p45w<AMODE, BN><<<grid, THREADS_W, Cfg<BN>::SMEM, st>>>(ma, mb, out, out_pstride, ohw, O, M, nkb, ntm, ntn,
-                                                                 ntiles, geo);
+    k_gemm_p45w<AMODE, BN, SUB><<<grid, THREADS_W, Cfg<BN>::SMEM, st>>>(ma, mb, out, out_pstride, ohw, O, M, nkb,
+                                                                       ntm, ntn, ntiles, geo, es);
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
 
 template <int AMODE>
 static int launch_wide(int bn, int grid, cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb, u64 *out,
                        u64 out_pstride, uint32_t ohw, int O, int M, int nkb, int ntm, int ntn, int ntiles,
-                       p45::wide::ConvGeom geo) {
-    return bn == 16 ? launch_wide_bn<AMODE, 16>(grid, st, ma, mb, out, out_pstride, ohw, O, M, nkb, ntm, ntn, ntiles, geo)
-                    : launch_wide_bn<AMODE, 32>(grid, st, ma, mb, out, out_pstride, ohw, O, M, nkb, ntm, ntn, ntiles, geo);
+                       p45::wide::ConvGeom geo, const p45::wide::EpiSub *es = nullptr) {
+    const p45::wide::EpiSub none{};
+    if (es) {                          // fused RESHARE_OUT epilogue: 128 x 32 tiles, K-major A only
+        if constexpr (AMODE == 0)
+            return launch_wide_bn<0, 32, true>(grid, st, ma, mb, out, out_pstride, ohw, O, M, nkb, ntm, ntn, ntiles,
+                                               geo, *es);
+        return SSN_ERR_UNSUPPORTED;
+    }
+    return bn == 16 ? launch_wide_bn<AMODE, 16>(grid, st, ma, mb, out, out_pstride, ohw, O, M, nkb, ntm, ntn, ntiles,
+                                                geo, none)
+                    : launch_wide_bn<AMODE, 32>(grid, st, ma, mb, out, out_pstride, ohw, O, M, nkb, ntm, ntn, ntiles,
+                                                geo, none);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
@@ -635,9 +688,9 @@ int launch_tc(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int 
 }
 
 int launch_p45(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int Kpad, u64 *out, u64 out_pstride,
-               u64 ohw, cudaStream_t st) {
+               u64 ohw, cudaStream_t st, const p45::wide::EpiSub *es = nullptr) {
     using namespace p45;
-    const int bn = p45_bn();
+    const int bn = es ? 32 : p45_bn();
     CUtensorMap ma, mb;
     if (make_map(&ma, a, Kpad, M, L, nparty, BM) || make_map(&mb, b, Kpad, O, L, nparty, bn)) return SSN_ERR_CUDA;
     if (ohw >= (1ull << 32) || (u64)M * 1 >= (1ull << 31)) return SSN_ERR_UNSUPPORTED;
@@ -652,7 +705,7 @@ int launch_p45(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int
     }
     const int grid = (int)(ntiles < nsm ? ntiles : nsm);
     return launch_wide<0>(bn, grid, st, ma, mb, out, out_pstride, (uint32_t)ohw, O, M, (Kpad + BK - 1) / BK, ntm, ntn,
-                          (int)ntiles, wide::ConvGeom{});
+                          (int)ntiles, wide::ConvGeom{}, es);
 }
 
 static int num_sms() {
@@ -1012,6 +1065,31 @@ extern "C" int ssn_gemm_tc(const uint8_t *a_planes, const uint8_t *b_planes, int
         case 8: return launch_tc<8>(a_planes, b_planes, nparty, M, O, (int)Kpad, out, out_pstride, ohw, p, st);
         default: return SSN_ERR_UNSUPPORTED;
     }
+}
+
+extern "C" int ssn_gemm_tc_subshares(const uint8_t *a_planes, const uint8_t *b_planes, int nparty, int M, int O,
+                                     u64 Kpad, u64 ohw, const ssn_subshare_desc *d, u64 p, void *stream) {
+    if (!d || !d->sub || !d->front_ids || Kpad % 16 || M < 1 || O < 1 || nparty < 1 || ohw < 1 || d->km1 < 0 ||
+        d->km1 > SSN_MAXK - 1 || d->nf < 1 || d->nf > SSN_MAXK)
+        return SSN_ERR_ARG;
+    if (p != p45::P || (unsigned __int128)6 * Kpad * 65025 >= ((unsigned __int128)1 << 32)) return SSN_ERR_UNSUPPORTED;
+    p45::wide::EpiSub es{};
+    es.sub = d->sub;
+    es.sub_pstride = d->party_stride;
+    es.sub_fstride = d->front_stride;
+    es.seed = d->seed;
+    es.stream = d->stream;
+    es.km1 = d->km1;
+    es.nf = d->nf;
+    for (int f = 0; f < d->nf; f++) {
+        unsigned __int128 acc = 1;
+        for (int e = 0; e < d->km1; e++) {
+            acc = acc * (d->front_ids[f] % p) % p;
+            if (acc >= (1u << 13)) return SSN_ERR_UNSUPPORTED;      // small id powers (ids 1..k)
+            es.pw[f][e] = (uint32_t)acc;
+        }
+    }
+    return launch_p45(a_planes, b_planes, nparty, M, O, (int)Kpad, nullptr, 0, ohw, (cudaStream_t)stream, &es);
 }
 
 extern "C" int ssn_mma_peak(int iters, int ctas, float *ms, double *int8_ops, void *stream) {

@@ -8,6 +8,8 @@ All paths are exact mod p.
   odd shapes and tiny test primes.
 """
 
+import ctypes
+
 import torch
 
 from . import _lib
@@ -73,10 +75,35 @@ def direct_conv(p, O, K):
     return p == (1 << 45) - 55 and O <= 16 and K * O <= 256
 
 
-def field_conv(w, x, stride, padding, p, nimg=1, nparty=1, planes=None, force=None, timing=None):
+class SubShares:
+    """Reshare step 1 fused into the share GEMM's epilogue (ssn_gemm_tc_subshares): instead of
+    the product, write each party's k RESHARE_OUT sub-shares (S/protocol.py:154-164) into
+    out[party][f][element] -- bit-identical to the GEMM followed by ssn_gen(seed, stream + party)
+    over the front ids."""
+
+    def __init__(self, out, seed, stream, km1, front_ids):
+        self.out, self.seed, self.stream, self.km1 = out, seed, stream, km1
+        self.front_ids = list(front_ids)
+
+    def call(self, a_planes, b_planes, nparty, rows, O, Kp, ohw, p):
+        nf = len(self.front_ids)
+        N = self.out.shape[-1]
+        ids = _lib.u64_array(self.front_ids)            # alive for the duration of the call
+        d = _lib.SubshareDesc(_lib.ptr(self.out).value, nf * N, N, self.seed, self.stream, self.km1, nf,
+                              ctypes.cast(ids, ctypes.c_void_p).value)
+        _lib.call("ssn_gemm_tc_subshares", _lib.ptr(a_planes), _lib.ptr(b_planes), nparty, rows, O, Kp, ohw,
+                  ctypes.byref(d), p, _lib.stream_ptr())
+
+
+def fused_subshares_supported(p, K):
+    return p == (1 << 45) - 55 and kpad(K) <= max_k_chunk(p)
+
+
+def field_conv(w, x, stride, padding, p, nimg=1, nparty=1, planes=None, force=None, timing=None, sub=None):
     """w: (nparty, O, C, kh, kw), x: (nparty, nimg, C, H, W) -> (nparty, nimg, O, OH, OW)
     (leading unit dims squeezed when nparty == nimg == 1).  timing: optional dict that
-    receives CUDA events around the operand-prep and GEMM launches."""
+    receives CUDA events around the operand-prep and GEMM launches.  sub: a SubShares -- the
+    tensor-core GEMM then emits the RESHARE_OUT sub-shares instead (returns None)."""
     O, C, kh, kw = w.shape[-4:]
     H, W = x.shape[-2:]
     OH = (H + 2 * padding - kh) // stride + 1
@@ -96,12 +123,17 @@ def field_conv(w, x, stride, padding, p, nimg=1, nparty=1, planes=None, force=No
         _lib.call("ssn_im2col_limbs", _lib.ptr(x), nparty, nimg, C, H, W, kh, kw, stride, padding, L, _lib.ptr(a),
                   Kp, nimg * C * H * W, _lib.stream_ptr())
         e1 = _ev() if timing is not None else None
-        _lib.call("ssn_gemm_tc", _lib.ptr(a), _lib.ptr(planes), nparty, L, rows, O, Kp, OH * OW, _lib.ptr(out),
-                  nimg * O * OH * OW, p, _lib.stream_ptr())
+        if sub is not None:
+            sub.call(a, planes, nparty, rows, O, Kp, OH * OW, p)
+        else:
+            _lib.call("ssn_gemm_tc", _lib.ptr(a), _lib.ptr(planes), nparty, L, rows, O, Kp, OH * OW, _lib.ptr(out),
+                      nimg * O * OH * OW, p, _lib.stream_ptr())
         if timing is not None:
             timing["prep"] = (e0, e1, "k_im2col_limbs")
             timing["gemm"] = (e1, _ev(), gemm_kernel_name(p, L, rows))
-        return out
+        return None if sub is not None else out
+    if sub is not None:
+        raise ValueError("fused sub-shares need the tensor-core path")
     w = w.contiguous()
     e0 = _ev() if timing is not None else None
     _lib.call("ssn_conv_simt", _lib.ptr(w), O * C * kh * kw, _lib.ptr(x), nimg * C * H * W, _lib.ptr(out),
@@ -111,13 +143,16 @@ def field_conv(w, x, stride, padding, p, nimg=1, nparty=1, planes=None, force=No
     return out
 
 
-def field_dense(w, x, p, nimg=1, nparty=1, planes=None, force=None, timing=None):
-    """w: (nparty, O, K), x: (nparty, nimg, K) -> (nparty, nimg, O) (squeezed for 1 x 1)."""
+def field_dense(w, x, p, nimg=1, nparty=1, planes=None, force=None, timing=None, sub=None):
+    """w: (nparty, O, K), x: (nparty, nimg, K) -> (nparty, nimg, O) (squeezed for 1 x 1).
+    sub: as field_conv."""
     O, K = w.shape[-2:]
     x = x.contiguous()
     out = torch.empty((nparty, nimg, O) if (nparty > 1 or nimg > 1) else (O,), dtype=torch.int64,
                       device=x.device)
     tc = use_tc(p, nimg, K, O) if force is None else force == "tc"
+    if sub is not None and not (tc and fused_subshares_supported(p, K)):
+        raise ValueError("fused sub-shares need the single-pass tensor-core path")
     if tc and kpad(K) > max_k_chunk(p):
         # split-K: exact partial products over K chunks (each within the int32 limb budget),
         # added mod p
@@ -140,12 +175,15 @@ def field_dense(w, x, p, nimg=1, nparty=1, planes=None, force=None, timing=None)
         e0 = _ev() if timing is not None else None
         _lib.call("ssn_limb_split", _lib.ptr(x), nimg, K, Kp, L, _lib.ptr(a), nimg * K, nparty, _lib.stream_ptr())
         e1 = _ev() if timing is not None else None
-        _lib.call("ssn_gemm_tc", _lib.ptr(a), _lib.ptr(planes), nparty, L, nimg, O, Kp, 1, _lib.ptr(out), nimg * O,
-                  p, _lib.stream_ptr())
+        if sub is not None:
+            sub.call(a, planes, nparty, nimg, O, Kp, 1, p)
+        else:
+            _lib.call("ssn_gemm_tc", _lib.ptr(a), _lib.ptr(planes), nparty, L, nimg, O, Kp, 1, _lib.ptr(out),
+                      nimg * O, p, _lib.stream_ptr())
         if timing is not None:
             timing["prep"] = (e0, e1, "k_limb_split")
             timing["gemm"] = (e1, _ev(), gemm_kernel_name(p, L, nimg))
-        return out
+        return None if sub is not None else out
     w = w.contiguous()
     e0 = _ev() if timing is not None else None
     _lib.call("ssn_dense_simt", _lib.ptr(w), O * K, _lib.ptr(x), nimg * K, _lib.ptr(out), nimg * O, nparty,

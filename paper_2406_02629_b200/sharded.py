@@ -27,6 +27,8 @@ independent groups, each on its own image batch (data parallel over images, SURV
 section 8e placement 2).  Decoded outputs equal the reference / integer plaintext exactly.
 """
 
+import os
+
 import numpy as np
 import torch
 import torch.distributed as dist
@@ -45,6 +47,11 @@ class PartyShardedEngine:
     def __init__(self, model, scheme, batch, seed=7, verify=False, ordering="ltn", group=0, rotate_elite=True):
         self.model, self.scheme, self.batch, self.seed, self.verify = model, scheme, int(batch), seed, verify
         self.rotate_elite = rotate_elite
+        # reshare step 1 in the share GEMM's epilogue (ssn_gemm_tc_subshares, bit-identical to the
+        # GEMM + ssn_gen pair).  Opt-in (SSN_FUSED_SUBSHARES=1): measured slower on every ResNet
+        # layer class (profiles/r02/fused_subshares_probe.json) -- the single-buffered 352-column
+        # TMEM accumulator makes the longer epilogue the critical path on small-K layers
+        self.fuse_subshares = os.environ.get("SSN_FUSED_SUBSHARES", "0") == "1"
         self.k, self.n = scheme.k, scheme.n
         self.m = 2 * self.k - 1
         self.p = scheme.field.p
@@ -274,16 +281,22 @@ class PartyShardedEngine:
                 planes = self._planes.get(op.weight)
                 if planes is None:
                     planes = self._planes[op.weight] = gemm_mod.weight_planes(w.reshape(1, O, K), p, 1)
+            SUB = torch.empty((k, N), dtype=torch.int64, device=self.dev)    # step 1 sub-shares
+            stream = prng.next_stream()
+            # reshare step 1 fused into the GEMM epilogue: the sub-shares are written straight into
+            # the RESHARE_OUT send buffers (bit-identical to GEMM + ssn_gen)
+            fused = self.fuse_subshares and tc and gemm_mod.fused_subshares_supported(p, K)
+            sub = gemm_mod.SubShares(SUB, prng.seed, stream, k - 1, self.scheme.front_ids) if fused else None
             if w.dim() == 5:
                 C, H, Wd = op.in_shape
                 acc = field_conv(w, X.reshape(1, B, C, H, Wd), op.stride, op.padding, p, nimg=B, nparty=1,
-                                 planes=planes, force="tc" if tc else "simt")
+                                 planes=planes, force="tc" if tc else "simt", sub=sub)
             else:
                 acc = field_dense(w, X.reshape(1, B, -1), p, nimg=B, nparty=1, planes=planes,
-                                  force="tc" if tc else "simt")
-            SUB = torch.empty((k, N), dtype=torch.int64, device=self.dev)    # step 1 sub-shares
-            _lib.call("ssn_gen", _lib.ptr(acc), N, None, 0, prng.seed, prng.next_stream(), k - 1, self.ids_front, k,
-                      _lib.ptr(SUB), N, N, N, 1, p, _lib.stream_ptr())
+                                  force="tc" if tc else "simt", sub=sub)
+            if not fused:
+                _lib.call("ssn_gen", _lib.ptr(acc), N, None, 0, prng.seed, stream, k - 1, self.ids_front, k,
+                          _lib.ptr(SUB), N, N, N, 1, p, _lib.stream_ptr())
         # hop 1 (RESHARE_OUT): participant -> every other front rank
         PTS = torch.empty((m, N), dtype=torch.int64, device=self.dev) if t < k else None
         sends = [(f + 1, SUB[f]) for f in range(k) if f != t] if SUB is not None else []

@@ -145,3 +145,36 @@ def test_split_k_dense_exact(g, rows, O, K):
     assert np.array_equal(tc, simt)
     blk = slice(0, 16)
     assert np.array_equal(tc.reshape(rows, O)[blk], oracle.gemm(x[blk], w.T))
+
+
+@pytest.mark.parametrize("k,n", [(2, 3), (3, 5)])
+@pytest.mark.parametrize("kind,nparty", [("dense", 1), ("conv", 1), ("conv", 3)])
+def test_fused_subshares_equal_gemm_then_gen(g, k, n, kind, nparty):
+    """ssn_gemm_tc_subshares (GEMM epilogue writes the RESHARE_OUT sub-shares) == the share GEMM
+    followed by ssn_gen over the front ids with (seed, stream + party) -- bit for bit."""
+    from paper_2406_02629_b200 import _lib
+    from paper_2406_02629_b200.field import PrimeField
+    from paper_2406_02629_b200.sss import SssScheme
+    rng = np.random.default_rng(k * 10 + nparty)
+    sch = SssScheme(PrimeField(), k, n)
+    if kind == "dense":
+        B, O, K = 70, 100, 300
+        w = dev(rng.integers(0, P, size=(nparty, O, K), dtype=np.uint64))
+        x = dev(rng.integers(0, P, size=(nparty, B, K), dtype=np.uint64))
+        N = B * O
+        run = lambda sub=None: g.field_dense(w, x, P, nimg=B, nparty=nparty, force="tc", sub=sub)  # noqa: E731
+    else:
+        B, C, H, O = 2, 16, 10, 40
+        w = dev(rng.integers(0, P, size=(nparty, O, C, 3, 3), dtype=np.uint64))
+        x = dev(rng.integers(0, P, size=(nparty, B, C, H, H), dtype=np.uint64))
+        N = B * O * 5 * 5
+        run = lambda sub=None: g.field_conv(w, x, 2, 1, P, nimg=B, nparty=nparty, force="tc", sub=sub)  # noqa: E731
+    acc = run().reshape(nparty, N)
+    ids = _lib.u64_array(sch.front_ids)
+    want = torch.empty((nparty, k, N), dtype=torch.int64, device="cuda")
+    for pt in range(nparty):
+        _lib.call("ssn_gen", _lib.ptr(acc[pt]), N, None, 0, 1234, 77 + pt, k - 1, ids, k, _lib.ptr(want[pt]),
+                  k * N, N, N, 1, P, _lib.stream_ptr())
+    got = torch.empty_like(want)
+    assert run(g.SubShares(got, 1234, 77, k - 1, sch.front_ids)) is None
+    assert torch.equal(got, want)
