@@ -38,20 +38,96 @@
 #include "ssn_field.cuh"
 #include "ssn_lincomb.cuh"
 #include "ssn_p45.cuh"
+#include "ssn_chain_consts.cuh"
+#include <type_traits>
 
 namespace {
 using namespace ssn45;
 
 
-template <int K, int N>
-struct STables {
-    static constexpr int M = 2 * K - 1;
-    SRow<K> wf;          // Lagrange weights of the front ids at 0
-    SRow<M> wp;          // Lagrange weights of the participant ids at 0
-    SRow<M> rt[N];       // R^T rows: out rank t <- participants j
-    SRow<K> ext[N];      // Reed-Solomon rows: id t (t >= k) <- front ids
-    uint32_t pw[N][K - 1];   // id_t^(e+1), e < k-1 (small, non-negative)
+// ---- compile-time protocol constants (default party ids 1..n, ssn_chain_consts.cuh)
+// Every constant linear combination of the chain -- reducing-matrix columns (scaled by their
+// common denominator D_t), Lagrange rows at 0, Reed-Solomon rows, party-id powers -- is an
+// integer immediate, so the multiplies fold into shift/LEA sequences or 32-bit IMADs and the
+// signs are known: no offset trick, no per-row D^-1 multiply (measured: the chain kernels are
+// bound by the FMA-heavy pipe that executes IMAD, profiles/r02/alu).
+template <int I, int E, class F>
+__device__ __forceinline__ void sfor(F &&f) {
+    if constexpr (I < E) {
+        f(std::integral_constant<int, I>{});
+        sfor<I + 1, E>(f);
+    }
+}
+
+template <int K, int N, int T>
+struct RtRow {        // column T of the reducing matrix times D_T: out rank T <- participants j
+    static constexpr int len = 2 * K - 1;
+    SSN_CC static int64_t c(int j) { return ChainConsts<K, N>::rt(T, j); }
 };
+template <int K, int N>
+struct WfRow {        // Lagrange weights at 0 of the front ids 1..k
+    static constexpr int len = K;
+    SSN_CC static int64_t c(int j) { return ChainConsts<K, N>::wf(j); }
+};
+template <int K, int N>
+struct WpRow {        // Lagrange weights at 0 of the participant ids 1..2k-1
+    static constexpr int len = 2 * K - 1;
+    SSN_CC static int64_t c(int j) { return ChainConsts<K, N>::wp(j); }
+};
+template <int K, int N, int T>
+struct ExtRow {       // Reed-Solomon row: share at id T+1 from the front shares
+    static constexpr int len = K;
+    SSN_CC static int64_t c(int j) { return ChainConsts<K, N>::ext(T, j); }
+};
+template <class Row>
+SSN_CC int64_t row_sum(int sign) {
+    int64_t s = 0;
+    for (int j = 0; j < Row::len; j++)
+        if (Row::c(j) * sign > 0) s += Row::c(j) * sign;
+    return s;
+}
+SSN_CC u64 cmod(int64_t c) { return c >= 0 ? (u64)c % PP : PP - (u64)(-c) % PP; }
+
+// sum_j c_j x_j mod p, lazy (< 2^46), for compile-time integer c_j and inputs x_j < 2^XB.
+// Fast form: positive and negative terms in two u64 sums, one fold:  pos < 2^63 and
+// BIAS (a multiple of p above any neg) < 2^63 + p, so pos + BIAS - neg is exact in u64.
+template <class Row, int XB>
+__device__ __forceinline__ u64 clin(const u64 (&x)[Row::len]) {
+    constexpr int64_t P = row_sum<Row>(1), Q = row_sum<Row>(-1);
+    constexpr bool fast = XB < 62 && (u64)P < (1ull << (63 - XB)) && (u64)Q < (1ull << (63 - XB));
+    if constexpr (fast) {
+        u64 pos = 0, neg = 0;
+#pragma unroll
+        for (int j = 0; j < Row::len; j++) {
+            const int64_t c = Row::c(j);
+            if (c > 0) pos += x[j] * (u64)c;
+            else if (c < 0) neg += x[j] * (u64)(-c);
+        }
+        constexpr u64 BIAS = (((u64)Q << XB) / PP + 1) * PP;
+        return lz(pos + BIAS - neg);
+    } else {
+        // wide coefficients (k = 4 reducing-matrix columns): full field products
+        u64 s = 0;
+#pragma unroll
+        for (int j = 0; j < Row::len; j++) {
+            const int64_t c = Row::c(j);
+            if (c != 0) s += mulm(XB > 58 ? lz(x[j]) : x[j], cmod(c));
+        }
+        return lz(s);
+    }
+}
+// bits of (s + sum_e c_e * id^(e+1)) for s < 2^46, c_e < 2^45, id <= MAXID
+SSN_CC int poly_bits(int k, int maxid) {
+    u64 b = 2;                   // s < 2 * 2^45
+    u64 pw = 1;
+    for (int e = 0; e < k - 1; e++) {
+        pw *= (u64)maxid;
+        b += pw;
+    }
+    int bits = 45;
+    while ((1ull << (bits - 45)) < b) bits++;
+    return bits;
+}
 
 // Division of a 32-bit numerator by a launch-constant 32-bit divisor: q = umulhi64(x, ceil(2^64/d))
 // is exact for all x < 2^32 (Granlund-Montgomery with a 64-bit magic), ~3 IMADs instead of the
@@ -149,19 +225,17 @@ __device__ __noinline__ u64 invm(u64 x) {
     return mulm(sqn(x39, 6), x7);
 }
 
-// share of s at rank t: s + sum_e c_e * id_t^(e+1), UNREDUCED: for s < 2^48 and id powers
-// < 2^9 (n <= 7) the value stays below 2^57, a valid mulm operand and summand before lz.
-template <int K, int N>
-__device__ __forceinline__ u64 share_raw(u64 s, const u64 (&c)[K - 1], const STables<K, N> &tb, int t) {
-    u64 acc = s;
+// share of s at party id `id` (a compile-time constant after unrolling): s + sum_e c_e id^(e+1),
+// UNREDUCED (< 2^poly_bits(K, id) for s < 2^46): multiplies by small immediates.
+template <int K>
+__device__ __forceinline__ u64 poly_at(u64 s, const u64 (&c)[K - 1], int id) {
+    u64 acc = s, pw = 1;
 #pragma unroll
-    for (int e = 0; e < K - 1; e++) acc += mul_small(c[e], tb.pw[t][e]);
+    for (int e = 0; e < K - 1; e++) {
+        pw *= (u64)id;
+        acc += c[e] * pw;
+    }
     return acc;
-}
-// the same, lazily reduced (< 2^46): operand of lin_s
-template <int K, int N>
-__device__ __forceinline__ u64 share_at(u64 s, const u64 (&c)[K - 1], const STables<K, N> &tb, int t) {
-    return lz(share_raw<K, N>(s, c, tb, t));
 }
 
 // K-1 uniform field elements: masked 45-bit Philox words.  Values in [p, 2^45) are lazy
@@ -223,10 +297,19 @@ __device__ __forceinline__ u64 trunc_val(u64 v, const ChainArgs &a) {
 // reshare + rerand + bias + truncation (+ residual add) of element i for all N parties.
 // HF: the trusted source's masks and the elite's truncation coefficients are host-fed shares
 // (reference-stream parity mode) instead of in-register Philox draws.
+//
+// Every message is computed (RESHARE_OUT sub-shares, RESHARE_BACK rows, TRUNC_MASKED, the elite's
+// fresh shares); two representation choices keep the FMA-heavy pipe light:
+//  * front fr's RESHARE_BACK row to out rank t is held as D_t * back (D_t the common denominator
+//    of R's column t); rank t multiplies its reconstruction by D_t^-1 once, instead of every front
+//    row paying one full modular multiply;
+//  * a rank adds the zero share and the alpha share it receives as one polynomial evaluation of
+//    the summed coefficients (the same integer), likewise the fresh truncation share and comp.
 template <int K, int N, bool HF>
-__device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, N> &tb, uint32_t i, u64 (&x)[N],
-                                           unsigned long long &bad) {
+__device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (&x)[N], unsigned long long &bad) {
     constexpr int M = 2 * K - 1;
+    using CC = ChainConsts<K, N>;
+    constexpr int XB_SUB = poly_bits(K, K);          // sub-share bound: front ids <= K
     u64 acc[M];
 #pragma unroll
     for (int j = 0; j < M; j++) acc[j] = a.acc[(u64)j * a.acc_ps + i];
@@ -242,14 +325,11 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
 #pragma unroll
         for (int e = 0; e < K - 1; e++) c[e] = take45<NCR>(rr, 45 * (j * (K - 1) + e));
 #pragma unroll
-        for (int fr = 0; fr < K; fr++) sub[fr][j] = share_at<K, N>(acc[j], c, tb, fr);
+        for (int fr = 0; fr < K; fr++) sub[fr][j] = poly_at<K>(acc[j], c, fr + 1);
     }
-    u64 subsum[K];
-#pragma unroll
-    for (int fr = 0; fr < K; fr++) subsum[fr] = xsum_of<M>(sub[fr]);
     // source: zero shares (gen_zero_shares) and the truncation masks (gen_additive_mask)
     // (zero, alpha and comp coefficients + the 64 bits of e from one source reservoir)
-    u64 z[K - 1], ca[K - 1], cc[K - 1];
+    u64 za[K - 1], cc[K - 1];        // zero + alpha coefficients, comp coefficients
     u64 alpha = 0, comp = 0;
     uint32_t ii = 0;
     if constexpr (HF) {
@@ -260,8 +340,7 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
         fill<NCS>(rs, a.sseed, a.sstream, i, 0x900u);
 #pragma unroll
         for (int e = 0; e < K - 1; e++) {
-            z[e] = take45<NCS>(rs, 45 * e);
-            ca[e] = take45<NCS>(rs, 45 * (K - 1 + e));
+            za[e] = take45<NCS>(rs, 45 * e) + take45<NCS>(rs, 45 * (K - 1 + e));
             cc[e] = take45<NCS>(rs, 45 * (2 * (K - 1) + e));
         }
         // e = 1 + U[0, emax) by multiply-shift of 64 random bits (bias <= emax / 2^64 <= 2^-32)
@@ -273,32 +352,32 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
     const uint32_t bq = fdiv(i, a.bias_div);
     const uint32_t ch = bq - fdiv(bq, a.bias_mod) * a.bias_mod.d;
     // ---- step 2 (RESHARE_BACK): front fr applies R^T; step 3: out rank t reconstructs,
-    //      + zero share (rerand) + bias share, then + alpha share (TRUNC_MASKED)
-    // Unrolled over the out ranks: with the nonlinearity split into its own kernel, k_chain_plain
-    // stays within the instruction cache and the unrolled form keeps masked[] in registers.
+    //      + zero share (rerand) + bias share + alpha share (TRUNC_MASKED)
     u64 masked[N];
-#pragma unroll
-    for (int t = 0; t < N; t++) {
+    sfor<0, N>([&](auto tc) {
+        constexpr int t = decltype(tc)::value;
         if (t < a.senders) {
-            u64 back[K];
+            u64 back[K];                                   // D_t * RESHARE_BACK[fr -> t]
 #pragma unroll
-            for (int fr = 0; fr < K; fr++) back[fr] = lin_s<M>(sub[fr], subsum[fr], tb.rt[t]);
-            u64 y = lin<K>(back, tb.wf) + a.bias[(u64)t * a.bias_ps + ch];
-            if constexpr (HF) y += a.h_zero[(u64)t * a.per + ii];
-            else y += share_raw<K, N>(0, z, tb, t);
+            for (int fr = 0; fr < K; fr++) back[fr] = clin<RtRow<K, N, t>, XB_SUB>(sub[fr]);
+            u64 y = clin<WfRow<K, N>, 46>(back);
+            if constexpr (CC::rt_den(t) != 1) y = mulm(y, CC::rt_dinv(t));
+            y += a.bias[(u64)t * a.bias_ps + ch];
+            if constexpr (HF) y += a.h_zero[(u64)t * a.per + ii] + a.h_alpha[(u64)t * a.per + ii];
+            else y += poly_at<K>(alpha, za, t + 1);
             if (t == a.fault_rank && i == 0) y += 1;                                        // test hook
-            if constexpr (HF) masked[t] = lz(y + a.h_alpha[(u64)t * a.per + ii]);
-            else masked[t] = lz(y + share_raw<K, N>(alpha, ca, tb, t));
+            masked[t] = lz(y);
         }
-    }
+    });
     // ---- truncation elite: rec over the front, RS check of the extra points, decode/floor/round
     u64 front[K];
 #pragma unroll
     for (int j = 0; j < K; j++) front[j] = masked[j];
-    const u64 v = canon(lin<K>(front, tb.wf));
-#pragma unroll
-    for (int t = K; t < N; t++)
-        if (t < a.senders) bad += (canon(lin<K>(front, tb.ext[t])) != canon(masked[t]));
+    const u64 v = canon(clin<WfRow<K, N>, 46>(front));
+    sfor<K, N>([&](auto tc) {
+        constexpr int t = decltype(tc)::value;
+        if (t < a.senders) bad += (canon(clin<ExtRow<K, N, t>, 46>(front)) != canon(masked[t]));
+    });
     const u64 tm = trunc_val(v, a);
     // fresh (k, n) shares of the truncated value (SHARE_DIST), + comp at every rank
     u64 g[K - 1];
@@ -307,26 +386,27 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, const STables<K, 
         for (int e = 0; e < K - 1; e++) g[e] = a.h_tcoef[(u64)e * a.per + ii];
     } else {
         coeffs<K>(g, a.pseed, a.pstream + M, i);
+#pragma unroll
+        for (int e = 0; e < K - 1; e++) g[e] += cc[e];
     }
 #pragma unroll
     for (int t = 0; t < N; t++) {
-        u64 s = share_raw<K, N>(tm, g, tb, t);
-        if constexpr (HF) s += a.h_comp[(u64)t * a.per + ii];
-        else s += share_raw<K, N>(comp, cc, tb, t);
+        u64 s;
+        if constexpr (HF) s = poly_at<K>(tm, g, t + 1) + a.h_comp[(u64)t * a.per + ii];
+        else s = poly_at<K>(tm + comp, g, t + 1);
         if (a.other) s += a.other[(u64)t * a.other_ps + i];                              // residual add
         x[t] = lz(s);                                                                   // lazy
     }
 }
 
 template <int K, int N, bool HF>
-__global__ void SSN_PLAIN_BOUNDS k_chain_plain(ChainArgs a, const __grid_constant__ STables<K, N> tb,
-                                                     SsnField f) {
+__global__ void SSN_PLAIN_BOUNDS k_chain_plain(ChainArgs a, SsnField f) {
     unsigned long long bad = 0;
     const uint32_t nel = (uint32_t)a.nel;
 #pragma unroll 1
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nel; i += gridDim.x * blockDim.x) {
         u64 x[N];
-        chain_elem<K, N, HF>(a, tb, i, x, bad);
+        chain_elem<K, N, HF>(a, i, x, bad);
 #pragma unroll
         for (int t = 0; t < N; t++) a.out[(u64)t * a.out_ps + i] = canon(x[t]);
     }
@@ -378,8 +458,7 @@ constexpr int WPT = 8;
 // output) and this kernel only runs the masked nonlinearity, reading each party's share.
 // Two kernels of half the code each run faster than one that overflows the instruction cache.
 template <int K, int N, bool SPLIT, bool HF>
-__global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, const __grid_constant__ STables<K, N> tb,
-                                                                SsnField f) {
+__global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
     constexpr int M = 2 * K - 1;
     unsigned long long bad = 0;
     const int lane = threadIdx.x & 31;
@@ -430,7 +509,7 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, const __grid_const
 #pragma unroll
                             for (int t = 0; t < M; t++) x[t] = inside ? a.acc[(u64)t * a.acc_ps + si] : 0;
                         } else {
-                            chain_elem<K, N, HF>(a, tb, i, x, bad);
+                            chain_elem<K, N, HF>(a, i, x, bad);
                         }
                         // participants mask with their beta shares (NONLIN_MASKED); elite rec over m
                         u64 mk[M];
@@ -442,9 +521,9 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, const __grid_const
                             u64 cb[K - 1];
                             coeffs<K>(cb, a.sseed, a.sstream + 5, i);
 #pragma unroll
-                            for (int j = 0; j < M; j++) mk[j] = mulm(x[j], share_raw<K, N>(bt, cb, tb, j));
+                            for (int j = 0; j < M; j++) mk[j] = mulm(x[j], poly_at<K>(bt, cb, j + 1));
                         }
-                        const u64 v = canon(lin<M>(mk, tb.wp));
+                        const u64 v = canon(clin<WpRow<K, N>, 46>(mk));
                         i64 sv = v > PHALF ? (i64)v - (i64)PP : (i64)v;
                         if (a.relu && sv <= 0) sv = 0;
                         if (a.pool_kind == 1) acc = sv > acc ? sv : acc;
@@ -502,7 +581,7 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, const __grid_const
                     if (t < a.fan) {
                         u64 bis;
                         if constexpr (HF) bis = a.h_binv[(u64)t * a.per_out + oo];
-                        else bis = share_raw<K, N>(binv, cbi, tb, t);
+                        else bis = poly_at<K>(binv, cbi, t + 1);
                         const u64 v = canon(mulm(plain[q], bis));
                         a.out[(u64)t * a.out_ps + o] = v;
                         if (pb != nullptr && t < a.pl_nparty) {        // limb planes for the next conv
@@ -525,43 +604,28 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, const __grid_const
 }
 
 
-// Lagrange weights at 0 of ids[0..cnt)
-static void lagrange0(u64 *row, const u64 *ids, int cnt, u64 p) {
-    for (int i = 0; i < cnt; i++) {
-        unsigned __int128 num = 1, den = 1;
-        for (int j = 0; j < cnt; j++)
-            if (j != i) {
-                num = num * (ids[j] % p) % p;
-                den = den * ((ids[j] % p + p - ids[i] % p) % p) % p;
-            }
-        row[i] = (u64)(num * inv_host((u64)den, p) % p);
-    }
-}
+static u64 mulmod_host(u64 a, u64 b, u64 p) { return (u64)((unsigned __int128)a * b % p); }
 
+// 1 if the caller's protocol constants are the ones the kernels were compiled with: the default
+// prime, party ids 1..n, R^T rows (rt[t*M + j] = R[j][t]) and RS rows (ext[(t-K)*K + i]).  Other
+// id sets / primes run the unfused kernels (ssn_chain_supported says so up front).
 template <int K, int N>
-int build_tables(STables<K, N> &tb, const u64 *ids, const u64 *rt, const u64 *ext, u64 p) {
+int check_consts(const u64 *ids, const u64 *rt, const u64 *ext, u64 p) {
+    using CC = ChainConsts<K, N>;
     constexpr int M = 2 * K - 1;
     const SsnField f = ssn_make_field(p);
     if (p != PP || !f.pm || !f.near) return 0;      // kernels are specialised to the default prime
-    int ok = 1;
-    u64 row[SSN_MAXJ];
-    lagrange0(row, ids, K, p);
-    ok &= make_srow<K>(tb.wf, row, K, p);
-    lagrange0(row, ids, M, p);
-    ok &= make_srow<M>(tb.wp, row, M, p);
-    for (int t = 0; t < N; t++) {
-        if (rt) ok &= make_srow<M>(tb.rt[t], rt + (u64)t * M, M, p);
-        u64 zero[SSN_MAXJ] = {0};
-        if (t >= K && ext) ok &= make_srow<K>(tb.ext[t], ext + (u64)(t - K) * K, K, p);
-        else make_srow<K>(tb.ext[t], zero, K, p);
-        unsigned __int128 acc = 1;
-        for (int e = 0; e < K - 1; e++) {
-            acc = acc * (ids[t] % p) % p;
-            ok &= acc < (1u << 13);
-            tb.pw[t][e] = (uint32_t)acc;
-        }
-    }
-    return ok;
+    for (int t = 0; t < N; t++)
+        if (ids[t] != (u64)(t + 1)) return 0;
+    if (rt)
+        for (int t = 0; t < N; t++)
+            for (int j = 0; j < M; j++)
+                if (rt[(u64)t * M + j] != mulmod_host(cmod(CC::rt(t, j)), CC::rt_dinv(t), p)) return 0;
+    if (ext)
+        for (int t = K; t < N; t++)
+            for (int i = 0; i < K; i++)
+                if (ext[(u64)(t - K) * K + i] != cmod(CC::ext(t, i))) return 0;
+    return 1;
 }
 
 // Grid cap for the grid-stride chain kernels: SSN_CHAIN_WAVES (default 8) x the resident-block
@@ -599,14 +663,14 @@ static u64 chain_grid_cap(KernT kern, int threads) {
 
 // the kernel launches of one chain (HF: host-fed reference-stream masks)
 template <int K, int N, bool HF>
-int launch_kernels(const ChainArgs &a, const STables<K, N> &tb, const SsnField &f, const ssn_chain_desc *d,
+int launch_kernels(const ChainArgs &a, const SsnField &f, const ssn_chain_desc *d,
                    cudaStream_t st) {
     if (!d->nonlin) {
         u64 blocks = (a.nel + PLAIN_THREADS - 1) / PLAIN_THREADS;
         const u64 cap = chain_grid_cap(k_chain_plain<K, N, HF>, PLAIN_THREADS);
         if (blocks > cap) blocks = cap;
         SSN_COUNT_LAUNCH();
-        k_chain_plain<K, N, HF><<<(unsigned)blocks, PLAIN_THREADS, 0, st>>>(a, tb, f);
+        k_chain_plain<K, N, HF><<<(unsigned)blocks, PLAIN_THREADS, 0, st>>>(a, f);
     } else {
         const u64 n_out = (u64)d->nb * d->c * (d->h / d->kh) * (d->w / d->kw);
         u64 blocks = (n_out + CHAIN_THREADS * WPT - 1) / (CHAIN_THREADS * WPT);
@@ -617,7 +681,7 @@ int launch_kernels(const ChainArgs &a, const STables<K, N> &tb, const SsnField &
         if (d->nonlin_only) {
             // a standalone masked nonlinearity: acc holds the n parties' input shares
             SSN_COUNT_LAUNCH();
-            k_chain_nonlin<K, N, true, HF><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a, tb, f);
+            k_chain_nonlin<K, N, true, HF><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a, f);
         } else if (d->scratch) {
             // split: reshare + truncation (+ add) into scratch [n][nel], then the nonlinearity
             ChainArgs a1 = a;
@@ -628,15 +692,15 @@ int launch_kernels(const ChainArgs &a, const STables<K, N> &tb, const SsnField &
             const u64 cap1 = chain_grid_cap(k_chain_plain<K, N, HF>, PLAIN_THREADS);
             if (b1 > cap1) b1 = cap1;
             SSN_COUNT_LAUNCH();
-            k_chain_plain<K, N, HF><<<(unsigned)b1, PLAIN_THREADS, 0, st>>>(a1, tb, f);
+            k_chain_plain<K, N, HF><<<(unsigned)b1, PLAIN_THREADS, 0, st>>>(a1, f);
             ChainArgs a2 = a;
             a2.acc = d->scratch;
             a2.acc_ps = a.nel;
             SSN_COUNT_LAUNCH();
-            k_chain_nonlin<K, N, true, HF><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a2, tb, f);
+            k_chain_nonlin<K, N, true, HF><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a2, f);
         } else {
             SSN_COUNT_LAUNCH();
-            k_chain_nonlin<K, N, false, HF><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a, tb, f);
+            k_chain_nonlin<K, N, false, HF><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a, f);
         }
     }
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
@@ -645,16 +709,15 @@ int launch_kernels(const ChainArgs &a, const STables<K, N> &tb, const SsnField &
 template <int K, int N>
 int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
     const u64 p = d->p;
-    // the protocol constants depend only on (ids, R, RS rows, p): rebuilt (rational
-    // reconstruction, inverses) only when they change -- host time per launch matters, a
-    // ResNet-152 step makes ~300 launches
+    // the protocol constants depend only on (ids, R, RS rows, p): checked against the compiled
+    // ones only when they change -- host time per launch matters, a ResNet-152 step makes ~300
+    // launches
     constexpr int M = 2 * K - 1;
     struct Key {
         u64 ids[N], rt[N * M], ext[N * K], p;
         int has_ext;
     };
     static thread_local Key last_key;
-    static thread_local STables<K, N> last_tb;
     static thread_local bool have = false;
     Key key;
     memset(&key, 0, sizeof(key));
@@ -665,14 +728,13 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
         for (int t = 0; t < (N - K) * K; t++) key.ext[t] = d->ext[t];
     key.p = p;
     if (!have || memcmp(&key, &last_key, sizeof(key)) != 0) {
-        if (!build_tables<K, N>(last_tb, d->ids, d->rt, d->ext, p)) {
+        if (!check_consts<K, N>(d->ids, d->rt, d->ext, p)) {
             have = false;
             return SSN_ERR_UNSUPPORTED;
         }
         last_key = key;
         have = true;
     }
-    const STables<K, N> &tb = last_tb;
     const SsnField f = ssn_make_field(p);
     ChainArgs a;
     a.acc = d->acc;
@@ -757,14 +819,12 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
     }
     if (a.planes && (!d->nonlin || a.pl_copies < 1 || a.pl_nparty < 1 || a.pl_nparty > N)) return SSN_ERR_ARG;
     if (a.senders > a.nout) return SSN_ERR_ARG;
-    return hf ? launch_kernels<K, N, true>(a, tb, f, d, st) : launch_kernels<K, N, false>(a, tb, f, d, st);
+    return hf ? launch_kernels<K, N, true>(a, f, d, st) : launch_kernels<K, N, false>(a, f, d, st);
 }
 
 template <int K, int N>
 int supported(const u64 *ids, u64 p) {
-    STables<K, N> tb;
-    u64 rt[N * (2 * K - 1)] = {0};
-    return build_tables<K, N>(tb, ids, rt, nullptr, p);
+    return check_consts<K, N>(ids, nullptr, nullptr, p);
 }
 
 }  // namespace

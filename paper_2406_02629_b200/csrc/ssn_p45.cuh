@@ -26,7 +26,16 @@ constexpr u64 PHALF = (PP - 1) / 2;
 // Intermediates are kept LAZY: any representative below 2^46 (not necessarily < p); only
 // compared and stored values are canonicalised.
 // lz: any x < 2^64 -> < 2^46, since (x >> 45) * 55 < 2^25.
-__device__ __forceinline__ u64 lz(u64 x) { return (x >> PS) * PC + (x & PMASK); }
+// The fold multiplies q = x >> 45 (< 2^19) by 55 in ONE 32-bit IMAD and adds with an
+// add/add-with-carry pair: the u64 form compiles to IMAD.WIDE, which occupies the FMA-heavy pipe
+// (the chain kernels' bottleneck) twice as long.
+__device__ __forceinline__ u64 lz(u64 x) {
+    uint32_t lo = (uint32_t)x, hi = (uint32_t)(x >> 32);
+    const uint32_t t = (hi >> (PS - 32)) * (uint32_t)PC;
+    hi &= (1u << (PS - 32)) - 1;
+    asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+r"(lo), "+r"(hi) : "r"(t));
+    return ((u64)hi << 32) | lo;
+}
 // canon: x < 2^64 -> [0, p) ((x >> 45) * 55 + low < 2^45 + 2^25 < 2p)
 __device__ __forceinline__ u64 canon(u64 x) {
     const u64 t = lz(x);
@@ -37,9 +46,16 @@ __device__ __forceinline__ u64 addm(u64 a, u64 b) {
     const u64 s = a + b;
     return s >= PP ? s - PP : s;
 }
-// a * b < 2^103: q = prod >> 45 < 2^58, q*55 + low < 2^64 -> lazy result
+// a, b < 2^52 (a * b < 2^103): q = prod >> 45 < 2^58, q*55 + low < 2^64 -> lazy result
+// Schoolbook on 32-bit halves: three 32x32->64 products for a, b < 2^52 (the middle pair summed
+// in one u64, < 2^53) instead of the 64x64 low half plus __umul64hi.
 __device__ __forceinline__ u64 mulm(u64 a, u64 b) {
-    const u64 lo = a * b, hi = __umul64hi(a, b);
+    const uint32_t al = (uint32_t)a, ah = (uint32_t)(a >> 32), bl = (uint32_t)b, bh = (uint32_t)(b >> 32);
+    const u64 p0 = (u64)al * bl;
+    const u64 p1 = (u64)al * bh + (u64)ah * bl;
+    const u64 p2 = (u64)ah * bh;
+    const u64 lo = p0 + (p1 << 32);
+    const u64 hi = p2 + (p1 >> 32) + (lo < p0);
     const u64 q = (hi << (64 - PS)) | (lo >> PS);
     return lz(q * PC + (lo & PMASK));
 }
