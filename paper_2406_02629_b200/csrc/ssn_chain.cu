@@ -414,7 +414,7 @@ __global__ void SSN_PLAIN_BOUNDS k_chain_plain(ChainArgs a, SsnField f) {
 }
 
 // exclusive prefix (up) / suffix (down) products across the warp; inactive lanes hold 1
-__device__ __forceinline__ u64 warp_excl_prefix(u64 v, int lane) {
+__device__ __noinline__ u64 warp_excl_prefix(u64 v, int lane) {
     u64 incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -424,7 +424,7 @@ __device__ __forceinline__ u64 warp_excl_prefix(u64 v, int lane) {
     const u64 ex = __shfl_up_sync(0xffffffffu, incl, 1);
     return lane ? ex : 1;
 }
-__device__ __forceinline__ u64 warp_excl_suffix(u64 v, int lane) {
+__device__ __noinline__ u64 warp_excl_suffix(u64 v, int lane) {
     u64 incl = v;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -447,34 +447,96 @@ __device__ __noinline__ void emit_planes(uint8_t *row, u64 v, int xq, int copies
     }
 }
 
-// masked nonlinearity fused after the chain: one thread per output window, WPT windows per
-// thread (a block-stride apart, coalesced).  beta^-1 of all 32*WPT windows of a warp comes
-// from ONE Fermat inversion: per-thread running products over its WPT windows, warp-shuffle
-// exclusive prefix/suffix products across lanes (Montgomery's batch trick), then a backward
-// pass.  No block barrier: warps never wait for each other.
+// a * b mod p (lazy) for a < 2^46 and b < 2^32 (beta, a running product times beta): two
+// 32x32->64 products instead of three
+__device__ __forceinline__ u64 mulm32(u64 a, uint32_t b) {
+    const u64 p0 = (u64)(uint32_t)a * b;
+    const u64 p1 = (u64)(uint32_t)(a >> 32) * b;          // < 2^46
+    const u64 lo = p0 + (p1 << 32);
+    const u64 hi = (p1 >> 32) + (lo < p0);
+    const u64 q = (hi << (64 - PS)) | (lo >> PS);          // < 2^33
+    return lz(q * PC + (lo & PMASK));
+}
+
+// NONLIN_PLAIN * (beta^-1 share), canonical: the elite's plaintext f(x * beta) is a signed value
+// with |f(x * beta)| < p/2 by the choice of bmax (S/masks.py:57-64), encoded, times the share.
+__device__ __forceinline__ u64 mul_plain(i64 sv, u64 b) {
+    const u64 pl = sv < 0 ? (u64)((i64)PP + sv) : (u64)sv;
+    return canon(mulm(pl, b));
+}
+
+// run^-1 for every thread of the block from ONE Fermat inversion (Montgomery's batch trick):
+// warp-shuffle exclusive prefix/suffix products, warp totals through shared memory, warp 0
+// inverts the block total.  Out of line: it runs once per block iteration, and inlined it
+// pushed the per-window loops out of the instruction cache.
+__device__ __noinline__ u64 block_batch_inverse(u64 run, int lane, int warp, u64 *s_tot, u64 *s_inv) {
+    constexpr int NW = CHAIN_THREADS / 32;
+    const u64 wpre = warp_excl_prefix(run, lane);
+    const u64 wsuf = warp_excl_suffix(run, lane);
+    const u64 wtot = __shfl_sync(0xffffffffu, mulm(wpre, run), 31);
+    if (lane == 0) s_tot[warp] = wtot;
+    __syncthreads();
+    if (warp == 0) {
+        const u64 v = lane < NW ? s_tot[lane] : 1;
+        const u64 bp = warp_excl_prefix(v, lane), bs = warp_excl_suffix(v, lane);
+        const u64 tot = __shfl_sync(0xffffffffu, mulm(bp, v), 31);
+        const u64 ti = invm(tot);
+        if (lane < NW) s_inv[lane] = mulm(mulm(ti, bp), bs);              // = warp total^-1
+    }
+    __syncthreads();
+    return mulm(mulm(s_inv[warp], wpre), wsuf);                            // = run^-1
+}
+
+// masked nonlinearity fused after the chain.  Each thread owns WPT output windows, in groups of G
+// ADJACENT windows (a group never crosses a limb-plane row), so the next conv's u8 limb planes
+// are written G bytes per store.  beta^-1 of all CHAIN_THREADS*WPT windows of a block iteration
+// comes from ONE Fermat inversion (Montgomery's batch trick): per-thread running products,
+// warp-shuffle exclusive prefix/suffix products, one inversion of the block total by warp 0,
+// then a backward pass.
 constexpr int WPT = 8;
+constexpr int NWARP = CHAIN_THREADS / 32;
+
+// byte l of each of the G values, packed little-endian (window g -> byte g)
+template <int G>
+__device__ __forceinline__ uint32_t pack_limb(const u64 (&v)[G], int l) {
+    const int w = l >> 2, s = l & 3;
+    auto word = [&](int g) { return (uint32_t)(v[g] >> (32 * w)); };
+    if constexpr (G == 1) {
+        return (word(0) >> (8 * s)) & 0xffu;
+    } else if constexpr (G == 2) {
+        return __byte_perm(word(0), word(1), (uint32_t)(s | ((4 + s) << 4)));
+    } else {
+        const uint32_t sel = (uint32_t)(s | ((4 + s) << 4));
+        return __byte_perm(__byte_perm(word(0), word(1), sel), __byte_perm(word(2), word(3), sel), 0x5410);
+    }
+}
 
 // SPLIT: the reshare/truncation/add part already ran (k_chain_plain into a.acc = its n-party
 // output) and this kernel only runs the masked nonlinearity, reading each party's share.
 // Two kernels of half the code each run faster than one that overflows the instruction cache.
-template <int K, int N, bool SPLIT, bool HF>
+template <int K, int N, bool SPLIT, bool HF, int G>
 __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
     constexpr int M = 2 * K - 1;
+    static_assert(WPT % G == 0, "groups tile a thread's windows");
+    __shared__ u64 s_tot[NWARP], s_inv[NWARP];
     unsigned long long bad = 0;
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t oh = a.h / a.kh, ow = a.w / a.kw;
     const uint32_t hw = oh * ow, chw = (uint32_t)a.c * hw;
     const uint32_t n_out = (uint32_t)a.nb * chw;
     const bool pooled = a.kh != 1 || a.kw != 1;
+    const bool batch_inv = !HF && !a.inv_table;
     const uint32_t span = CHAIN_THREADS * WPT;
 #pragma unroll 1
     for (uint32_t base = blockIdx.x * span; base < n_out; base += gridDim.x * span) {
-        u64 plain[WPT], beta[WPT], pre[WPT];
+        i64 plain[WPT];
+        u64 beta[WPT], pre[WPT];
         u64 run = 1;
 #pragma unroll 1
         for (int q = 0; q < WPT; q++) {
-            const uint32_t o = base + q * CHAIN_THREADS + threadIdx.x;
-            u64 pl = 0, bt = 1;
+            const uint32_t o = base + ((q / G) * CHAIN_THREADS + threadIdx.x) * G + (q % G);
+            i64 pl = 0;
+            u64 bt = 1;
             if (o < n_out) {
                 if constexpr (!HF) bt = 1 + ssn_rand_range(a.sseed, a.sstream + 4, o, 0, a.bmax);  // window-constant beta
                 uint32_t base_in = o;
@@ -529,7 +591,7 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
                         if (a.pool_kind == 1) acc = sv > acc ? sv : acc;
                         else acc += sv;
                     }
-                pl = acc < 0 ? (u64)((i64)PP + acc) : (u64)acc;                  // encode_signed (NONLIN_PLAIN)
+                pl = acc;                                          // NONLIN_PLAIN (signed; encoded at use)
             }
             plain[q] = pl;
             beta[q] = bt;
@@ -539,64 +601,93 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
                 pre[q] = a.inv_table[bt];           // source's beta^-1 from the inverse table
             } else {
                 pre[q] = run;                       // product of this thread's earlier betas
-                run = mulm(run, bt);
+                run = mulm32(run, (uint32_t)bt);
             }
         }
-        // source: beta^-1 for every window of the warp from one inversion (no table)
+        // source: beta^-1 for every window of the block iteration from ONE inversion
         u64 inv = 0;
-        if (!HF && !a.inv_table) {
-            const u64 wpre = warp_excl_prefix(run, lane);
-            const u64 wsuf = warp_excl_suffix(run, lane);
-            const u64 total = __shfl_sync(0xffffffffu, mulm(wpre, run), 31);
-            inv = mulm(mulm(invm(total), wpre), wsuf);      // = run^-1
-        }
+        if (batch_inv) inv = block_batch_inverse(run, lane, warp, s_tot, s_inv);
 #pragma unroll 1
-        for (int q = WPT - 1; q >= 0; q--) {
-            const uint32_t o = base + q * CHAIN_THREADS + threadIdx.x;
-            u64 binv = 0;
-            if constexpr (!HF) {
-                if (a.inv_table) {
-                    binv = pre[q];
-                } else {
-                    binv = mulm(inv, pre[q]);
-                    inv = mulm(inv, beta[q]);
+        for (int gq = WPT / G - 1; gq >= 0; gq--) {
+            const uint32_t o0 = base + (gq * CHAIN_THREADS + threadIdx.x) * G;
+            u64 binv[G];
+#pragma unroll
+            for (int g = G - 1; g >= 0; g--) {
+                const int q = gq * G + g;
+                binv[g] = 0;
+                if constexpr (!HF) {
+                    if (a.inv_table) {
+                        binv[g] = pre[q];
+                    } else {
+                        binv[g] = mulm(inv, pre[q]);
+                        inv = mulm32(inv, (uint32_t)beta[q]);
+                    }
                 }
             }
-            if (o < n_out) {
-                u64 cbi[K - 1];
-                uint32_t oo = 0;
-                if constexpr (HF) oo = o - fdiv(o, a.f_per_out) * (uint32_t)a.per_out;
-                else coeffs<K>(cbi, a.sseed, a.sstream + 6, o);
+            if (o0 < n_out) {                                // n_out % G == 0: the whole group
+                u64 cbi[G][K - 1];
+                uint32_t oo[G];
+#pragma unroll
+                for (int g = 0; g < G; g++) {
+                    if constexpr (HF) oo[g] = (o0 + g) - fdiv(o0 + g, a.f_per_out) * (uint32_t)a.per_out;
+                    else coeffs<K>(cbi[g], a.sseed, a.sstream + 6, o0 + g);
+                }
                 uint8_t *pb = nullptr;
                 int xq = 0;
                 if (a.planes) {
-                    const uint32_t img = fdiv(o, a.f_chw), rem = o - img * chw;
+                    const uint32_t img = fdiv(o0, a.f_chw), rem = o0 - img * chw;
                     const uint32_t ci = fdiv(rem, a.f_hw), pix = rem - ci * hw;
                     const uint32_t y = fdiv(pix, a.f_ow);
                     xq = (int)(pix - y * ow);
                     pb = a.planes + (u64)ci * a.pl_cs + (u64)img * a.pl_is + (u64)y * a.pl_wp;
                 }
+                // out ranks in a rolled loop (party-id powers at run time): the G-window body
+                // unrolled over the n ranks overflowed the instruction cache
+                u64 *op = a.out + o0;
+                uint8_t *dst = pb + xq;
+                uint32_t pw[K - 1];
 #pragma unroll
-                for (int t = 0; t < N; t++)
-                    if (t < a.fan) {
+                for (int e = 0; e < K - 1; e++) pw[e] = 1;
+#pragma unroll 1
+                for (int t = 0; t < a.fan; t++) {
+#pragma unroll
+                    for (int e = 0; e < K - 1; e++) pw[e] = e == 0 ? (uint32_t)(t + 1) : pw[e - 1] * (uint32_t)(t + 1);
+                    u64 v[G];
+#pragma unroll
+                    for (int g = 0; g < G; g++) {
                         u64 bis;
-                        if constexpr (HF) bis = a.h_binv[(u64)t * a.per_out + oo];
-                        else bis = poly_at<K>(binv, cbi, t + 1);
-                        const u64 v = canon(mulm(plain[q], bis));
-                        a.out[(u64)t * a.out_ps + o] = v;
-                        if (pb != nullptr && t < a.pl_nparty) {        // limb planes for the next conv
-                            if (SPLIT && a.pl_copies == 1) {
-                                // inline single copy: offsets t*ps + l*ls are warp-uniform
-                                uint8_t *dst = pb + xq;
+                        if constexpr (HF) {
+                            bis = a.h_binv[(u64)t * a.per_out + oo[g]];
+                        } else {
+                            bis = binv[g];
 #pragma unroll
-                                for (int l = 0; l < 6; l++)
-                                    dst[(u64)t * a.pl_ps + (u64)l * a.pl_ls] = (uint8_t)(v >> (8 * l));
-                            } else {
-                                emit_planes(pb + (u64)t * a.pl_ps, v, xq, a.pl_copies, a.pl_nparty * a.pl_ps,
-                                            a.pl_ls, a.pl_wp);
-                            }
+                            for (int e = 0; e < K - 1; e++) bis += mul_small(cbi[g][e], pw[e]);
                         }
+                        v[g] = mul_plain(plain[gq * G + g], bis);
                     }
+                    if constexpr (G == 1) {
+                        op[0] = v[0];
+                    } else {
+#pragma unroll
+                        for (int g = 0; g < G; g += 2) *reinterpret_cast<ulonglong2 *>(op + g) = make_ulonglong2(v[g], v[g + 1]);
+                    }
+                    op += a.out_ps;
+                    if (pb != nullptr && t < a.pl_nparty) {        // limb planes for the next conv
+                        if (a.pl_copies == 1) {
+                            // offsets l*ls are warp-uniform; G adjacent windows per store
+#pragma unroll
+                            for (int l = 0; l < 6; l++) {
+                                const uint32_t w = pack_limb<G>(v, l);
+                                if constexpr (G == 4) *reinterpret_cast<uint32_t *>(dst + (u64)l * a.pl_ls) = w;
+                                else if constexpr (G == 2) *reinterpret_cast<uint16_t *>(dst + (u64)l * a.pl_ls) = (uint16_t)w;
+                                else dst[(u64)l * a.pl_ls] = (uint8_t)w;
+                            }
+                        } else if constexpr (G == 1) {
+                            emit_planes(dst - xq, v[0], xq, a.pl_copies, a.pl_nparty * a.pl_ps, a.pl_ls, a.pl_wp);
+                        }
+                        dst += a.pl_ps;
+                    }
+                }
             }
         }
     }
@@ -661,6 +752,36 @@ static u64 chain_grid_cap(KernT kern, int threads) {
     return cap;
 }
 
+// Windows per output group of the nonlinearity kernel: G adjacent windows share one G-byte
+// limb-plane store and one 16-byte share store, when every G-group stays inside a plane row
+// (G | OW) or a contiguous channel plane (1x1 layout, G | OH*OW) and all strides keep it aligned.
+static int nonlin_group(const ChainArgs &a, const ssn_chain_desc *d, u64 n_out) {
+    const u64 oh = d->h / d->kh, ow = d->w / d->kw;
+    static const int gmax = getenv("SSN_NONLIN_GMAX") ? atoi(getenv("SSN_NONLIN_GMAX")) : 4;
+    for (int g = 4; g > 1; g /= 2) {
+        if (g > gmax || WPT % g || n_out % g || a.out_ps % 2 || ((uintptr_t)a.out & 15)) continue;
+        if (a.planes) {
+            const bool rows = ow % g == 0;
+            const bool contig = (u64)a.pl_wp == ow && a.pl_is == oh * ow && (oh * ow) % g == 0;
+            if (!(rows || contig) || a.pl_copies != 1 || a.pl_ps % g || a.pl_ls % g || a.pl_cs % g ||
+                a.pl_is % g || (u64)a.pl_wp % g || ((uintptr_t)a.planes % g))
+                continue;
+        }
+        return g;
+    }
+    return 1;
+}
+
+template <int K, int N, bool SPLIT, bool HF, int G>
+static void launch_nonlin(const ChainArgs &a, const SsnField &f, u64 n_out, cudaStream_t st) {
+    u64 blocks = (n_out + CHAIN_THREADS * WPT - 1) / (CHAIN_THREADS * WPT);
+    const u64 cap = chain_grid_cap(k_chain_nonlin<K, N, SPLIT, HF, G>, CHAIN_THREADS);
+    if (blocks > cap) blocks = cap;
+    if (blocks < 1) blocks = 1;
+    SSN_COUNT_LAUNCH();
+    k_chain_nonlin<K, N, SPLIT, HF, G><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a, f);
+}
+
 // the kernel launches of one chain (HF: host-fed reference-stream masks)
 template <int K, int N, bool HF>
 int launch_kernels(const ChainArgs &a, const SsnField &f, const ssn_chain_desc *d,
@@ -673,16 +794,9 @@ int launch_kernels(const ChainArgs &a, const SsnField &f, const ssn_chain_desc *
         k_chain_plain<K, N, HF><<<(unsigned)blocks, PLAIN_THREADS, 0, st>>>(a, f);
     } else {
         const u64 n_out = (u64)d->nb * d->c * (d->h / d->kh) * (d->w / d->kw);
-        u64 blocks = (n_out + CHAIN_THREADS * WPT - 1) / (CHAIN_THREADS * WPT);
-        const u64 cap = d->scratch || d->nonlin_only ? chain_grid_cap(k_chain_nonlin<K, N, true, HF>, CHAIN_THREADS)
-                                                     : chain_grid_cap(k_chain_nonlin<K, N, false, HF>, CHAIN_THREADS);
-        if (blocks > cap) blocks = cap;
-        if (blocks < 1) blocks = 1;
-        if (d->nonlin_only) {
-            // a standalone masked nonlinearity: acc holds the n parties' input shares
-            SSN_COUNT_LAUNCH();
-            k_chain_nonlin<K, N, true, HF><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a, f);
-        } else if (d->scratch) {
+        const bool split = d->scratch || d->nonlin_only;
+        const int G = split ? nonlin_group(a, d, n_out) : 1;
+        if (split && !d->nonlin_only) {
             // split: reshare + truncation (+ add) into scratch [n][nel], then the nonlinearity
             ChainArgs a1 = a;
             a1.out = d->scratch;
@@ -693,14 +807,19 @@ int launch_kernels(const ChainArgs &a, const SsnField &f, const ssn_chain_desc *
             if (b1 > cap1) b1 = cap1;
             SSN_COUNT_LAUNCH();
             k_chain_plain<K, N, HF><<<(unsigned)b1, PLAIN_THREADS, 0, st>>>(a1, f);
-            ChainArgs a2 = a;
+        }
+        ChainArgs a2 = a;
+        if (split && !d->nonlin_only) {
             a2.acc = d->scratch;
             a2.acc_ps = a.nel;
-            SSN_COUNT_LAUNCH();
-            k_chain_nonlin<K, N, true, HF><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a2, f);
+        }
+        // a standalone masked nonlinearity (nonlin_only): acc holds the n parties' input shares
+        if (split) {
+            if (G == 4) launch_nonlin<K, N, true, HF, 4>(a2, f, n_out, st);
+            else if (G == 2) launch_nonlin<K, N, true, HF, 2>(a2, f, n_out, st);
+            else launch_nonlin<K, N, true, HF, 1>(a2, f, n_out, st);
         } else {
-            SSN_COUNT_LAUNCH();
-            k_chain_nonlin<K, N, false, HF><<<(unsigned)blocks, CHAIN_THREADS, 0, st>>>(a, f);
+            launch_nonlin<K, N, false, HF, 1>(a2, f, n_out, st);
         }
     }
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
