@@ -64,6 +64,11 @@ struct RtRow {        // column T of the reducing matrix times D_T: out rank T <
     static constexpr int len = 2 * K - 1;
     SSN_CC static int64_t c(int j) { return ChainConsts<K, N>::rt(T, j); }
 };
+template <int K, int N, int C>
+struct ViRow {        // column C of the inverse participant Vandermonde matrix times D_v
+    static constexpr int len = 2 * K - 1;
+    SSN_CC static int64_t c(int j) { return ChainConsts<K, N>::vi(C, j); }
+};
 template <int K, int N>
 struct WfRow {        // Lagrange weights at 0 of the front ids 1..k
     static constexpr int len = K;
@@ -351,17 +356,56 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
     }
     const uint32_t bq = fdiv(i, a.bias_div);
     const uint32_t ch = bq - fdiv(bq, a.bias_mod) * a.bias_mod.d;
-    // ---- step 2 (RESHARE_BACK): front fr applies R^T; step 3: out rank t reconstructs,
-    //      + zero share (rerand) + bias share + alpha share (TRUNC_MASKED)
+    // ---- step 2 (RESHARE_BACK): front fr sends rank t  sum_j R[j][t] sub[fr][j].  R is the
+    //      rank-k product B^-1[:, :k] B_ext[:k, :] (S/sss.py:197-210), so the front evaluates it as
+    //      sum_c id_t^c w[fr][c] with w[fr][c] = sum_j B^-1[j][c] sub[fr][j]: k*m multiplies by
+    //      small integers (held as D_v * w) instead of n*m by R's wide numerators.
+    //      step 3: out rank t reconstructs (Lagrange over the front), x D_v^-1, + zero share
+    //      (rerand) + bias share + alpha share (TRUNC_MASKED)
+    // k = 2 keeps the direct form (measured: the factored one saves nothing at m = n = 3)
+    constexpr bool FACTOR = K >= 3;
+    constexpr bool LZSUB = XB_SUB > 50;                       // k = 4: fold the sub-shares first
+    constexpr int XB_W = LZSUB ? 46 : XB_SUB;
+    u64 w[K][K];                                              // D_v * w[fr][c], lazy
+    if constexpr (FACTOR) {
+#pragma unroll
+        for (int fr = 0; fr < K; fr++) {
+            if constexpr (LZSUB) {
+#pragma unroll
+                for (int j = 0; j < M; j++) sub[fr][j] = lz(sub[fr][j]);
+            }
+            sfor<0, K>([&](auto cc_) {
+                constexpr int c = decltype(cc_)::value;
+                w[fr][c] = clin<ViRow<K, N, c>, XB_W>(sub[fr]);
+            });
+        }
+    }
+    constexpr int XB_BACK = poly_bits(K, N) + 1;              // sum_c id^c w_c, w_c < 2^46
     u64 masked[N];
     sfor<0, N>([&](auto tc) {
         constexpr int t = decltype(tc)::value;
         if (t < a.senders) {
-            u64 back[K];                                   // D_t * RESHARE_BACK[fr -> t]
+            u64 y;
+            if constexpr (FACTOR) {
+                u64 back[K];                                   // D_v * RESHARE_BACK[fr -> t]
 #pragma unroll
-            for (int fr = 0; fr < K; fr++) back[fr] = clin<RtRow<K, N, t>, XB_SUB>(sub[fr]);
-            u64 y = clin<WfRow<K, N>, 46>(back);
-            if constexpr (CC::rt_den(t) != 1) y = mulm(y, CC::rt_dinv(t));
+                for (int fr = 0; fr < K; fr++) {
+                    u64 acc = w[fr][0], pw = 1;
+#pragma unroll
+                    for (int c = 1; c < K; c++) {
+                        pw *= (u64)(t + 1);
+                        acc += w[fr][c] * pw;
+                    }
+                    back[fr] = acc;
+                }
+                y = mulm(clin<WfRow<K, N>, XB_BACK>(back), CC::vi_dinv);
+            } else {
+                u64 back[K];                                   // D_t * RESHARE_BACK[fr -> t]
+#pragma unroll
+                for (int fr = 0; fr < K; fr++) back[fr] = clin<RtRow<K, N, t>, XB_SUB>(sub[fr]);
+                y = clin<WfRow<K, N>, 46>(back);
+                if constexpr (CC::rt_den(t) != 1) y = mulm(y, CC::rt_dinv(t));
+            }
             y += a.bias[(u64)t * a.bias_ps + ch];
             if constexpr (HF) y += a.h_zero[(u64)t * a.per + ii] + a.h_alpha[(u64)t * a.per + ii];
             else y += poly_at<K>(alpha, za, t + 1);

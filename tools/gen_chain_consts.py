@@ -5,6 +5,10 @@ chain kernels for the default party ids 1..n, as exact rationals (compile-time i
   wp[j]      Lagrange weight at 0 of participant id j+1 over ids 1..2k-1
   rt[t][j]   D_t * R[j][t]: column t of the reducing matrix (S/sss.py:197-210) scaled by its
              common denominator D_t; rt_dinv[t] = D_t^-1 mod p
+  vi[c][j]   D_v * B^-1[j][c] (c < k): the first k columns of the inverse Vandermonde matrix of
+             the participant ids, scaled by their common denominator D_v (vi_dinv = D_v^-1 mod p).
+             R = B^-1[:, :k] @ B_ext[:k, :] (S/sss.py:197-210), so a front's RESHARE_BACK row to
+             rank t is  sum_c id_t^c * (sum_j B^-1[j][c] sub_j)
   ext[t][i]  Reed-Solomon row: share at id t+1 (t >= k) from the front shares (Lagrange basis of
              ids 1..k evaluated at t+1)
 
@@ -37,9 +41,8 @@ def as_int(v):
     return int(v)
 
 
-def reducing_columns(k, n):
-    """R[j][t] = sum_{c<k} Binv[j][c] * id_t^c (Vandermonde of the 2k-1 participant ids)."""
-    m = 2 * k - 1
+def inverse_vandermonde(m):
+    """B^-1 over Q for B[i][j] = id_j^i, ids 1..m."""
     ids = list(range(1, m + 1))
     # B[i][j] = id_j^i; B^-1 by Gauss-Jordan over Q
     B = [[Fraction(pid) ** i for pid in ids] for i in range(m)]
@@ -57,8 +60,14 @@ def reducing_columns(k, n):
                 g = A[r][col]
                 A[r] = [a - g * b for a, b in zip(A[r], A[col])]
                 inv[r] = [a - g * b for a, b in zip(inv[r], inv[col])]
-    R = [[sum(inv[j][c] * Fraction(t + 1) ** c for c in range(k)) for t in range(n)] for j in range(m)]
-    return R
+    return inv
+
+
+def reducing_columns(k, n):
+    """R[j][t] = sum_{c<k} Binv[j][c] * id_t^c (Vandermonde of the 2k-1 participant ids)."""
+    m = 2 * k - 1
+    inv = inverse_vandermonde(m)
+    return [[sum(inv[j][c] * Fraction(t + 1) ** c for c in range(k)) for t in range(n)] for j in range(m)]
 
 
 def check_against_package(k, n, R):
@@ -87,6 +96,9 @@ def emit(k, n):
         D = lcm(*[R[j][t].denominator for j in range(m)])
         rt.append([as_int(R[j][t] * D) for j in range(m)])
         dens.append(D)
+    inv = inverse_vandermonde(m)
+    Dv = lcm(*[inv[j][c].denominator for j in range(m) for c in range(k)])
+    vi = [[as_int(inv[j][c] * Dv) for j in range(m)] for c in range(k)]
     ext = []
     for t in range(n):
         ext.append([as_int(v) for v in lagrange_at(list(range(1, k + 1)), t + 1)] if t >= k else [0] * k)
@@ -108,6 +120,12 @@ def emit(k, n):
     lines.append(f"        constexpr uint64_t a[{n}] = {{{', '.join(f'{x}ull' for x in dinv)}}};")
     lines.append("        return a[t];")
     lines.append("    }")
+    lines.append(f"    SSN_CC static int64_t vi(int c, int j) {{")
+    lines.append(f"        constexpr int64_t a[{k}][{m}] = {{{', '.join(arr(r) for r in vi)}}};")
+    lines.append("        return a[c][j];")
+    lines.append("    }")
+    lines.append(f"    static constexpr uint64_t vi_den = {Dv};")
+    lines.append(f"    static constexpr uint64_t vi_dinv = {pow(Dv, P45 - 2, P45)}ull;")
     lines.append(f"    SSN_CC static int64_t ext(int t, int i) {{")
     lines.append(f"        constexpr int64_t a[{n}][{k}] = {{{', '.join(arr(r) for r in ext)}}};")
     lines.append("        return a[t][i];")
