@@ -210,8 +210,14 @@ constexpr int PLAIN_THREADS = 256;
 #else
 constexpr int CHAIN_THREADS = 128;
 constexpr int PLAIN_THREADS = 128;
-#define SSN_PLAIN_BOUNDS __launch_bounds__(PLAIN_THREADS, 4)
-#define SSN_NONLIN_BOUNDS __launch_bounds__(CHAIN_THREADS, 6)
+#ifndef SSN_PLAIN_MINB
+#define SSN_PLAIN_MINB 6
+#endif
+#ifndef SSN_NONLIN_MINB
+#define SSN_NONLIN_MINB 7
+#endif
+#define SSN_PLAIN_BOUNDS __launch_bounds__(PLAIN_THREADS, SSN_PLAIN_MINB)
+#define SSN_NONLIN_BOUNDS __launch_bounds__(CHAIN_THREADS, SSN_NONLIN_MINB)
 #endif
 
 __device__ __forceinline__ u64 sqn(u64 x, int n) {
