@@ -292,6 +292,10 @@ int ssn_gemm_tc_subshares(const uint8_t *a_planes, const uint8_t *b_planes, int 
  * resident shared-memory tiles; *ms = device time of that launch, *int8_ops = 2*M*N*K*iters*ctas.
  * The share GEMM's roofline (bench.py) divides by this measured peak.  Synchronises `stream`. */
 int ssn_mma_peak(int iters, int ctas, float *ms, double *int8_ops, void *stream);
+/* Measurement only: the share GEMM's MMA issue pattern from resident shared memory (mode 0: one
+ * 128 x n x 32 MMA back to back; mode 1: 6 A limb tiles x stacked B, D at column 32 i, as in
+ * k_gemm_p45w).  Same outputs as ssn_mma_peak. */
+int ssn_mma_probe(int mode, int n, int iters, int ctas, float *ms, double *int8_ops, void *stream);
 
 #ifdef __cplusplus
 }

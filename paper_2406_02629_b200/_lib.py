@@ -80,6 +80,7 @@ _SIGS = {
     "ssn_gemm_tc_conv": [_P, _I32, _I32, _I32, _I32, _I32, _I32, _P, _I32, _I32, _P, _U64, _U64, _P],
     "ssn_planes_shift": [_P, _U64, _I32, _P],
     "ssn_mma_peak": [_I32, _I32, _P, _P, _P],
+    "ssn_mma_probe": [_I32, _I32, _I32, _I32, _P, _P, _P],
     "ssn_gemm_tc_subshares": [_P, _P, _I32, _I32, _I32, _U64, _U64, _P, _U64, _P],
     "ssn_planes_cn": [_P, _I32, _I32, _I32, _I32, _I32, _I32, _I32, _P, _U64, _I32, _P],
     "ssn_chain_supported": [_I32, _I32, _P, _U64],
@@ -137,7 +138,11 @@ def load(require_cuda=True):
                                  "(there is no CPU fallback)")
         L = ctypes.CDLL(LIB_PATH)
         for name, args in _SIGS.items():
-            fn = getattr(L, name)
+            fn = getattr(L, name, None)
+            if fn is None and os.environ.get("SSN_LIB"):     # an older experimental build
+                continue
+            if fn is None:
+                raise SsnUnavailable(f"{LIB_PATH} does not export {name}: rebuild it")
             fn.argtypes = args
             fn.restype = ctypes.c_uint64 if name == "ssn_kernel_launches" else ctypes.c_int
         _lib = L

@@ -72,6 +72,28 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *map, u
         : "memory");
 }
 
+// TMA loads multicast to the CTAs of ctaMask: the box lands at the same shared-memory offset in
+// each of them and completes bytes on the mbarrier at the same offset in each.
+__device__ __forceinline__ void tma_load_4d_mc(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                               int c2, int c3, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_3d_mc(void *dst, const CUtensorMap *map, uint64_t *bar, int c0, int c1,
+                                               int c2, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;"
+        ::"r"(smem_u32(dst)), "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // UMMA shared-memory descriptor for an MN-major (M contiguous) operand, 128-byte swizzle:
 // each K row holds 128 M-bytes, 8-row (1 KB) swizzle atoms stacked along K (SBO = 1 KB).
 __device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t saddr) {
@@ -112,6 +134,13 @@ __device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
                  : "memory");
+}
+
+// arrive on the mbarrier at this offset in every CTA of ctaMask once the issued MMAs complete
+__device__ __forceinline__ void mma_commit_mc(uint64_t *bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+        ::"r"(smem_u32(bar)), "h"(mask) : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
@@ -368,7 +397,12 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[NC]) 
     }
 }
 
-template <int AMODE, int BN, bool SUB = false>
+// CL = 2: a cluster of two CTAs works on the two N tiles of one 128-row A tile in lockstep; each
+// CTA loads three of the six A limb planes and multicasts them to both, halving the A operand's
+// L2 -> SM traffic (A is 48 of the 60 KB a stage moves; at the tensor pipe's rate the unshared
+// stream needs ~50 B/clk per SM, above the L2's share per SM).  The stage's `empty` barrier then
+// waits for both CTAs' MMA warps (commit multicast to the pair).
+template <int AMODE, int BN, bool SUB = false, int CL = 1>
 __global__ void SSN_GEMM_W_BOUNDS
 k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, u64 *__restrict__ out,
             u64 out_pstride, uint32_t ohw, int O, int M, int nkb, int ntm, int ntn, int ntiles, ConvGeom geo,
@@ -384,10 +418,16 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + NBUF);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+    // 1-D grid, clusters of CL consecutive CTAs: the cluster rank is blockIdx.x % CL (read where it
+    // is used: a rank held in a local also defeated the uniform datapath), and CTA b
+    // takes tiles b, b + grid, ... -- the CL CTAs of a cluster hold the CL consecutive N tiles of
+    // one A tile (ntn % CL == 0, grid % CL == 0).  The loops below start at blockIdx.x itself: a
+    // copy in a local made ptxas treat the loop state as non-uniform (R2UR waterfalls around
+    // every tcgen05.mma, 8% slower).
     if (threadIdx.x == 0) {
         for (int s = 0; s < STW; s++) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], CL);
         }
         for (int b = 0; b < NBUF; b++) {
             mbar_init(&tfull[b], 1);
@@ -401,6 +441,7 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    if constexpr (CL > 1) cluster_sync_all();           // the peer's barriers exist before any multicast
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     const uint32_t tmem = *tmem_slot;
 
@@ -414,18 +455,28 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     mbar_wait(&empty[s], ((it / STW) & 1) ^ 1);
                     mbar_arrive_expect_tx(&full[s], STAGE_W);
                     uint8_t *sa = base + s * STAGE_W;
+                    // CL = 2: this CTA's half of the limb planes, multicast to the pair
+                    constexpr int LH = L / CL;
+                    const int l0 = CL > 1 ? (int)(blockIdx.x % CL) * LH : 0;
+                    uint8_t *sah = sa + l0 * BM * BK;
                     if (AMODE == 0) {
-                        tma_load_4d(sa, &tmA, &full[s], kb * BK, mt * BM, 0, party);
+                        if constexpr (CL > 1) tma_load_4d_mc(sah, &tmA, &full[s], kb * BK, mt * BM, l0, party, 3);
+                        else tma_load_4d(sa, &tmA, &full[s], kb * BK, mt * BM, 0, party);
                     } else if (AMODE == 1) {
-                        tma_load_3d(sa, &tmA, &full[s], mt * BM, kb * BK, party * L);
+                        if constexpr (CL > 1) tma_load_3d_mc(sah, &tmA, &full[s], mt * BM, kb * BK, party * L + l0, 3);
+                        else tma_load_3d(sa, &tmA, &full[s], mt * BM, kb * BK, party * L);
                     } else {
                         const int tap = kb / geo.cblocks, cb = kb - tap * geo.cblocks;
                         const int dy = tap / 3, dx = tap - dy * 3;
                         const int img = mt / geo.ntf, ft = mt - img * geo.ntf;
                         // column shift dx - 1 comes from the dx-th pre-shifted copy (TMA inner
                         // coordinates must stay 16-byte aligned); the row shift is (dy - 1) * Wp
-                        tma_load_4d(sa, &tmA, &full[s], ft * BM + (dy - 1) * geo.Wp, img, cb * BK,
-                                    (dx * geo.nparty + party) * L);
+                        if constexpr (CL > 1)
+                            tma_load_4d_mc(sah, &tmA, &full[s], ft * BM + (dy - 1) * geo.Wp, img, cb * BK,
+                                           (dx * geo.nparty + party) * L + l0, 3);
+                        else
+                            tma_load_4d(sa, &tmA, &full[s], ft * BM + (dy - 1) * geo.Wp, img, cb * BK,
+                                        (dx * geo.nparty + party) * L);
                     }
                     tma_load_4d(sa + A_BYTES, &tmB, &full[s], kb * BK, nt * BN, 0, party);
                 }
@@ -468,7 +519,8 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                             }
                         }
                     }
-                    mma_commit(&empty[s]);
+                    if constexpr (CL > 1) mma_commit_mc(&empty[s], 3);
+                    else mma_commit(&empty[s]);
                 }
                 mma_commit(&tfull[buf]);
             }
@@ -585,6 +637,8 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    // no CTA of a pair leaves while the other may still multicast into its shared memory
+    if constexpr (CL > 1) cluster_sync_all();
     if (warp == 1) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 }  // namespace wide
@@ -600,27 +654,55 @@ static int p45_bn() {
     return bn;
 }
 
-template <int AMODE, int BN, bool SUB = false>
+template <int AMODE, int BN, bool SUB = false, int CL = 1>
 static int launch_wide_bn(int grid, cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb, u64 *out,
                           u64 out_pstride, uint32_t ohw, int O, int M, int nkb, int ntm, int ntn, int ntiles,
                           p45::wide::ConvGeom geo, const p45::wide::EpiSub &es) {
     using namespace p45::wide;
+    auto kern = k_gemm_p45w<AMODE, BN, SUB, CL>;
     static bool attr = false;
     if (!attr) {
-        if (cudaFuncSetAttribute(k_gemm_p45w<AMODE, BN, SUB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Cfg<BN>::SMEM) != cudaSuccess)
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM) != cudaSuccess)
             return SSN_ERR_CUDA;
         attr = true;
     }
     SSN_COUNT_LAUNCH();
-    k_gemm_p45w<AMODE, BN, SUB><<<grid, THREADS_W, Cfg<BN>::SMEM, st>>>(ma, mb, out, out_pstride, ohw, O, M, nkb,
-                                                                       ntm, ntn, ntiles, geo, es);
+    if constexpr (CL == 1) {
+        kern<<<grid, THREADS_W, Cfg<BN>::SMEM, st>>>(ma, mb, out, out_pstride, ohw, O, M, nkb, ntm, ntn, ntiles, geo, es);
+    } else {
+        cudaLaunchConfig_t cfg = {};
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CL;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.gridDim = dim3((unsigned)(grid - grid % CL));
+        cfg.blockDim = dim3(THREADS_W);
+        cfg.dynamicSmemBytes = Cfg<BN>::SMEM;
+        cfg.stream = st;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        if (cudaLaunchKernelEx(&cfg, kern, ma, mb, out, out_pstride, ohw, O, M, nkb, ntm, ntn, ntiles, geo, es) !=
+            cudaSuccess)
+            return SSN_ERR_CUDA;
+    }
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
 
+// A-operand multicast across a 2-CTA cluster (SSN_GEMM_CLUSTER=1 disables): needs an even number of
+// N tiles (the pair shares the A tile) and the plain (non-fused) epilogue
+static int p45_cluster() {
+    static int cl = 0;
+    if (!cl) {
+        const char *e = getenv("SSN_GEMM_CLUSTER");
+        cl = (e && atoi(e) == 1) ? 1 : 2;
+    }
+    return cl;
+}
+
 template <int AMODE>
-static int launch_wide(int bn, int grid, cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb, u64 *out,
-                       u64 out_pstride, uint32_t ohw, int O, int M, int nkb, int ntm, int ntn, int ntiles,
+static int launch_wide(int bn, int cl, int grid, cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb,
+                       u64 *out, u64 out_pstride, uint32_t ohw, int O, int M, int nkb, int ntm, int ntn, int ntiles,
                        p45::wide::ConvGeom geo, const p45::wide::EpiSub *es = nullptr) {
     const p45::wide::EpiSub none{};
     if (es) {                          // fused RESHARE_OUT epilogue: 128 x 32 tiles, K-major A only
@@ -629,6 +711,11 @@ static int launch_wide(int bn, int grid, cudaStream_t st, const CUtensorMap &ma,
                                                geo, *es);
         return SSN_ERR_UNSUPPORTED;
     }
+    if (cl == 2)
+        return bn == 16 ? launch_wide_bn<AMODE, 16, false, 2>(grid, st, ma, mb, out, out_pstride, ohw, O, M, nkb, ntm,
+                                                              ntn, ntiles, geo, none)
+                        : launch_wide_bn<AMODE, 32, false, 2>(grid, st, ma, mb, out, out_pstride, ohw, O, M, nkb, ntm,
+                                                              ntn, ntiles, geo, none);
     return bn == 16 ? launch_wide_bn<AMODE, 16>(grid, st, ma, mb, out, out_pstride, ohw, O, M, nkb, ntm, ntn, ntiles,
                                                 geo, none)
                     : launch_wide_bn<AMODE, 32>(grid, st, ma, mb, out, out_pstride, ohw, O, M, nkb, ntm, ntn, ntiles,
@@ -647,12 +734,13 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     return fn;
 }
 
-int make_map(CUtensorMap *map, const uint8_t *planes, int Kpad, int rows, int L, int P, int box_rows) {
+int make_map(CUtensorMap *map, const uint8_t *planes, int Kpad, int rows, int L, int P, int box_rows,
+             int box_limbs = 0) {
     auto enc = get_encode();
     if (!enc) return SSN_ERR_CUDA;
     cuuint64_t dims[4] = {(cuuint64_t)Kpad, (cuuint64_t)rows, (cuuint64_t)L, (cuuint64_t)P};
     cuuint64_t strides[3] = {(cuuint64_t)Kpad, (cuuint64_t)Kpad * rows, (cuuint64_t)Kpad * rows * L};
-    cuuint32_t box[4] = {(cuuint32_t)BK, (cuuint32_t)box_rows, (cuuint32_t)L, 1};
+    cuuint32_t box[4] = {(cuuint32_t)BK, (cuuint32_t)box_rows, (cuuint32_t)(box_limbs ? box_limbs : L), 1};
     cuuint32_t estr[4] = {1, 1, 1, 1};
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t *>(planes), dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -691,10 +779,12 @@ int launch_p45(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int
                u64 ohw, cudaStream_t st, const p45::wide::EpiSub *es = nullptr) {
     using namespace p45;
     const int bn = es ? 32 : p45_bn();
-    CUtensorMap ma, mb;
-    if (make_map(&ma, a, Kpad, M, L, nparty, BM) || make_map(&mb, b, Kpad, O, L, nparty, bn)) return SSN_ERR_CUDA;
-    if (ohw >= (1ull << 32) || (u64)M * 1 >= (1ull << 31)) return SSN_ERR_UNSUPPORTED;
     const int ntm = (M + BM - 1) / BM, ntn = (O + bn - 1) / bn;
+    const int cl = (!es && ntn % 2 == 0) ? p45_cluster() : 1;
+    CUtensorMap ma, mb;
+    if (make_map(&ma, a, Kpad, M, L, nparty, BM, L / cl) || make_map(&mb, b, Kpad, O, L, nparty, bn))
+        return SSN_ERR_CUDA;
+    if (ohw >= (1ull << 32) || (u64)M * 1 >= (1ull << 31)) return SSN_ERR_UNSUPPORTED;
     const long long ntiles = (long long)ntm * ntn * nparty;
     if (ntiles >= (1ll << 31)) return SSN_ERR_UNSUPPORTED;
     static int nsm = 0;
@@ -704,7 +794,7 @@ int launch_p45(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
     const int grid = (int)(ntiles < nsm ? ntiles : nsm);
-    return launch_wide<0>(bn, grid, st, ma, mb, out, out_pstride, (uint32_t)ohw, O, M, (Kpad + BK - 1) / BK, ntm, ntn,
+    return launch_wide<0>(bn, cl, grid, st, ma, mb, out, out_pstride, (uint32_t)ohw, O, M, (Kpad + BK - 1) / BK, ntm, ntn,
                           (int)ntiles, wide::ConvGeom{}, es);
 }
 
@@ -727,6 +817,8 @@ int launch_cn(const uint8_t *a, int mode, int nimg, int C, int H, int W, int Wp,
     if (C % BK) return SSN_ERR_UNSUPPORTED;
     const int taps = mode == 2 ? 9 : 1;
     const int Kpad = taps * C;
+    const int bn = p45_bn();
+    const int cl = ((O + bn - 1) / bn) % 2 == 0 ? p45_cluster() : 1;
     CUtensorMap ma, mb;
     const cuuint64_t PL = (cuuint64_t)nparty * L;
     CUresult r;
@@ -735,7 +827,7 @@ int launch_cn(const uint8_t *a, int mode, int nimg, int C, int H, int W, int Wp,
         if (bhw % 16) return SSN_ERR_UNSUPPORTED;
         cuuint64_t dims[3] = {bhw, (cuuint64_t)C, PL};
         cuuint64_t strides[2] = {bhw, bhw * C};
-        cuuint32_t box[3] = {(cuuint32_t)BM, (cuuint32_t)BK, (cuuint32_t)L};
+        cuuint32_t box[3] = {(cuuint32_t)BM, (cuuint32_t)BK, (cuuint32_t)(L / cl)};
         cuuint32_t estr[3] = {1, 1, 1};
         r = enc(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<uint8_t *>(a), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -745,14 +837,13 @@ int launch_cn(const uint8_t *a, int mode, int nimg, int C, int H, int W, int Wp,
         const cuuint64_t hw = (cuuint64_t)H * Wp;
         cuuint64_t dims[4] = {hw, (cuuint64_t)nimg, (cuuint64_t)C, 3 * PL};
         cuuint64_t strides[3] = {hw, hw * nimg, hw * nimg * C};
-        cuuint32_t box[4] = {(cuuint32_t)BM, 1, (cuuint32_t)BK, (cuuint32_t)L};
+        cuuint32_t box[4] = {(cuuint32_t)BM, 1, (cuuint32_t)BK, (cuuint32_t)(L / cl)};
         cuuint32_t estr[4] = {1, 1, 1, 1};
         r = enc(&ma, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<uint8_t *>(a), dims, strides, box, estr,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     }
     if (r != CUDA_SUCCESS) return SSN_ERR_CUDA;
-    const int bn = p45_bn();
     if (make_map(&mb, b, Kpad, O, L, nparty, bn)) return SSN_ERR_CUDA;
     wide::ConvGeom geo{C, H, W, Wp, C / BK, 0, nparty};
     const int M = nimg * H * W;
@@ -769,9 +860,9 @@ int launch_cn(const uint8_t *a, int mode, int nimg, int C, int H, int W, int Wp,
     const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
     const uint32_t ohw = (uint32_t)(H * W);
     if (mode == 1)
-        return launch_wide<1>(bn, grid, st, ma, mb, out, out_pstride, ohw, O, M, taps * geo.cblocks, ntm, ntn,
+        return launch_wide<1>(bn, cl, grid, st, ma, mb, out, out_pstride, ohw, O, M, taps * geo.cblocks, ntm, ntn,
                               (int)ntiles, geo);
-    return launch_wide<2>(bn, grid, st, ma, mb, out, out_pstride, ohw, O, M, taps * geo.cblocks, ntm, ntn, (int)ntiles,
+    return launch_wide<2>(bn, cl, grid, st, ma, mb, out, out_pstride, ohw, O, M, taps * geo.cblocks, ntm, ntn, (int)ntiles,
                           geo);
 }
 
@@ -816,6 +907,63 @@ __global__ void __launch_bounds__(128, 1) k_mma_peak(int iters, unsigned long lo
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
+}
+
+// Measurement only: the MMA issue pattern of the share GEMM from resident shared memory (no TMA,
+// no epilogue).  mode 0: one A tile x one B tile (N = n) back to back into one accumulator;
+// mode 1: the wide GEMM's K slice -- per 32-deep slice, 6 MMAs of 128 x n x 32, A limb i (six
+// distinct 128 x 64 B tiles) against the stacked B limbs, D at TMEM column 32 i.
+__global__ void __launch_bounds__(128, 1) k_mma_probe(int mode, int n, int iters, unsigned long long *sink) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *base = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    constexpr int AB = 6 * 128 * 64, BB = 256 * 64;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(base + AB + BB);
+    uint32_t *slot = reinterpret_cast<uint32_t *>(bar + 1);
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < (AB + BB) / 4; i += blockDim.x) reinterpret_cast<uint32_t *>(base)[i] = i * 2654435761u;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *slot;
+    if (threadIdx.x == 0) {
+        const uint32_t sa = smem_u32(base), sb = smem_u32(base + AB);
+        const uint32_t id = idesc_i8(n);
+        if (mode == 0) {
+            const uint64_t ad = umma_desc_sw64(sa), bd = umma_desc_sw64(sb);
+            for (int i = 0; i < iters; i++) mma_i8(tmem, ad, bd, id, i > 0 ? 1u : 0u);
+        } else {
+            for (int it = 0; it < iters; it += 12) {
+#pragma unroll
+                for (int kk = 0; kk < 2; kk++) {
+                    const uint64_t bd = umma_desc_sw64(sb + kk * 32);
+#pragma unroll
+                    for (int i = 0; i < 6; i++)
+                        mma_i8(tmem + (uint32_t)(i * 32), umma_desc_sw64(sa + i * 128 * 64 + kk * 32), bd, id,
+                               it > 0 ? 1u : 0u);
+                }
+            }
+        }
+        mma_commit(bar);
+        mbar_wait(bar, 0);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t r[8];
+        tmem_ld8(tmem + ((uint32_t)(threadIdx.x & 31) << 16), r);
+        if (threadIdx.x == 0) atomicAdd(sink, (unsigned long long)r[0]);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
 // ---------------------------------------------------------------- operand preparation
@@ -1114,5 +1262,32 @@ extern "C" int ssn_mma_peak(int iters, int ctas, float *ms, double *int8_ops, vo
     cudaEventDestroy(e1);
     cudaFreeAsync(sink, st);
     *int8_ops = 2.0 * 128 * 256 * 32 * (double)iters * ctas;
+    return cudaStreamSynchronize(st) == cudaSuccess ? 0 : SSN_ERR_CUDA;
+}
+
+extern "C" int ssn_mma_probe(int mode, int n, int iters, int ctas, float *ms, double *int8_ops, void *stream) {
+    if (iters < 12 || ctas < 1 || !ms || !int8_ops || n < 16 || n > 256 || n % 16 || (mode == 1 && n > 192))
+        return SSN_ERR_ARG;
+    iters -= iters % 12;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int smem = 6 * 128 * 64 + 256 * 64 + 1024 + 64;
+    if (cudaFuncSetAttribute(k_mma_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+        return SSN_ERR_CUDA;
+    unsigned long long *sink = nullptr;
+    if (cudaMallocAsync(&sink, sizeof(*sink), st) != cudaSuccess) return SSN_ERR_CUDA;
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k_mma_probe<<<ctas, 128, smem, st>>>(mode, n, 12, sink);          // warm-up
+    cudaEventRecord(e0, st);
+    SSN_COUNT_LAUNCH();
+    k_mma_probe<<<ctas, 128, smem, st>>>(mode, n, iters, sink);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(ms, e0, e1);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFreeAsync(sink, st);
+    *int8_ops = 2.0 * 128 * n * 32 * (double)iters * ctas;
     return cudaStreamSynchronize(st) == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
