@@ -255,10 +255,12 @@ def load_traffic():
         return {}
 
 
-# executed thread instructions per chain element, by (k, n): ncu smsp__thread_inst_executed over
-# the chain kernels of one step / the step's chain elements (tools/chain_alu.py, the ncu lists in
-# profiles/r01/alu/: ResNet-152 5PC and ResNet-50 3PC); other schemes: not calibrated
-CHAIN_ALU = {(3, 5): 3328, (2, 3): 1573}
+# executed thread instructions and FMA-heavy pipe cycles (per SM, 4 pipe slots per SM per cycle) per
+# chain element, by (k, n): ncu smsp__thread_inst_executed / sm__pipe_fmaheavy_cycles_active over the
+# chain kernels of one ResNet-152 step (batch 32) / the step's chain elements (tools/chain_alu.py,
+# profiles/r02/alu/).  The chain kernels are bound by the FMA-heavy pipe that executes IMAD.
+CHAIN_ALU = {(3, 5): 2443, (2, 3): 1498}
+CHAIN_HEAVY = {(3, 5): 91.0, (2, 3): 51.9}
 
 
 def roofline(kstats, eng, dev_ms, bf16, hbm, src):
@@ -301,6 +303,14 @@ def roofline(kstats, eng, dev_ms, bf16, hbm, src):
                 r["alu_issue"] = {"thread_instr_per_elem": alu, "calibration": "ncu count, tools/chain_alu.py",
                                   "achieved_tinstr_per_s": float(f"{rate:.4g}"),
                                   "peak_tinstr_per_s": float(f"{peak_i:.4g}"), "frac": round(rate / peak_i, 4)}
+                hv = CHAIN_HEAVY.get((eng.k, eng.n))
+                if hv:
+                    # FMA-heavy pipe: hv SM-cycles per element (4 slots per SM per cycle) vs 148 SMs x clock
+                    hrate = hv * st["elems_per_launch"] / sec
+                    peak_h = 148 * 4 * 1.965e9
+                    r["fma_heavy_pipe"] = {"slot_cycles_per_elem": hv, "achieved_per_s": float(f"{hrate:.4g}"),
+                                           "peak_per_s": float(f"{peak_h:.4g}"), "frac": round(hrate / peak_h, 4),
+                                           "note": "the chain's binding pipe (IMAD / IMAD.WIDE)"}
         t = traffic.get(cls)
         r["traffic"] = round(t) if t else None
         r["kernel"] = st["kernel"]
