@@ -503,20 +503,26 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     for (int kk = 0; kk < BK / UK; kk++) {
                         const uint64_t bdesc = umma_desc_sw64(sb + kk * UK);
                         const bool first = kb == 0 && kk == 0;
+                        auto adesc_of = [&](int i) {
+                            return AMODE ? umma_desc_sw128_mn(sa + i * BM * BK + kk * UK * BM)
+                                         : umma_desc_sw64(sa + i * BM * BK + kk * UK);
+                        };
+                        if (!first) {
 #pragma unroll
-                        for (int i = 0; i < L; i++) {
-                            const uint64_t adesc = AMODE ? umma_desc_sw128_mn(sa + i * BM * BK + kk * UK * BM)
-                                                         : umma_desc_sw64(sa + i * BM * BK + kk * UK);
-                            const uint32_t d = dbase + (uint32_t)(i * BN);
-                            if (!first) {
-                                mma_i8(d, adesc, bdesc, ID_ALL, 1u);
-                            } else if (i == 0) {
-                                mma_i8(d, adesc, bdesc, ID_ALL, 0u);
-                            } else {
-                                mma_i8(d, adesc, bdesc, ID_HEAD, 1u);
-                                mma_i8(d + (uint32_t)((L - 1) * BN), adesc,
-                                       umma_desc_sw64(sb + (L - 1) * BN * BK + kk * UK), ID_ONE, 0u);
-                            }
+                            for (int i = 0; i < L; i++)
+                                mma_i8(dbase + (uint32_t)(i * BN), adesc_of(i), bdesc, ID_ALL, 1u);
+                        } else {
+                            // first K slice: the accumulators start undefined.  Limb 0 initialises
+                            // diagonals 0..L-1; limb L-1 then adds to diagonal L-1 (B limb 0, N = BN)
+                            // and initialises L..2L-2 (B limbs 1.., N = (L-1) BN); limbs 1..L-2
+                            // accumulate over fully initialised columns.  7 MMAs, one narrow.
+                            mma_i8(dbase, adesc_of(0), bdesc, ID_ALL, 0u);
+                            const uint64_t a5 = adesc_of(L - 1);
+                            mma_i8(dbase + (uint32_t)((L - 1) * BN), a5, bdesc, ID_ONE, 1u);
+                            mma_i8(dbase + (uint32_t)(L * BN), a5, umma_desc_sw64(sb + BN * BK + kk * UK), ID_HEAD, 0u);
+#pragma unroll
+                            for (int i = 1; i < L - 1; i++)
+                                mma_i8(dbase + (uint32_t)(i * BN), adesc_of(i), bdesc, ID_ALL, 1u);
                         }
                     }
                     if constexpr (CL > 1) mma_commit_mc(&empty[s], 3);
@@ -644,14 +650,19 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
 }  // namespace wide
 }  // namespace p45
 
-// tile width of the p45 share GEMM: SSN_GEMM_BN=16 (double-buffered TMEM) or 32
-static int p45_bn() {
-    static int bn = 0;
-    if (!bn) {
+// tile width of the p45 share GEMM for a K of `kpad` bytes: SSN_GEMM_BN=16 / 32 forces one;
+// otherwise BN = 16 (two 176-column TMEM accumulators: the MMAs of tile t+1 run while the
+// epilogue drains tile t) when K <= SSN_GEMM_BN16_K (default 0: off), else BN = 32.
+static int p45_bn(int kpad) {
+    static int bn = -1, kmax = 0;
+    if (bn < 0) {
         const char *e = getenv("SSN_GEMM_BN");
-        bn = (e && atoi(e) == 32) ? 32 : (e && atoi(e) == 16) ? 16 : SSN_GEMM_BN_DEFAULT;
+        bn = (e && atoi(e) == 32) ? 32 : (e && atoi(e) == 16) ? 16 : 0;
+        const char *k = getenv("SSN_GEMM_BN16_K");
+        kmax = k ? atoi(k) : 0;
     }
-    return bn;
+    if (bn) return bn;
+    return kpad <= kmax ? 16 : SSN_GEMM_BN_DEFAULT;
 }
 
 template <int AMODE, int BN, bool SUB = false, int CL = 1>
@@ -778,7 +789,7 @@ int launch_tc(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int 
 int launch_p45(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int Kpad, u64 *out, u64 out_pstride,
                u64 ohw, cudaStream_t st, const p45::wide::EpiSub *es = nullptr) {
     using namespace p45;
-    const int bn = es ? 32 : p45_bn();
+    const int bn = es ? 32 : p45_bn(Kpad);
     const int ntm = (M + BM - 1) / BM, ntn = (O + bn - 1) / bn;
     const int cl = (!es && ntn % 2 == 0) ? p45_cluster() : 1;
     CUtensorMap ma, mb;
@@ -817,7 +828,7 @@ int launch_cn(const uint8_t *a, int mode, int nimg, int C, int H, int W, int Wp,
     if (C % BK) return SSN_ERR_UNSUPPORTED;
     const int taps = mode == 2 ? 9 : 1;
     const int Kpad = taps * C;
-    const int bn = p45_bn();
+    const int bn = p45_bn(Kpad);
     const int cl = ((O + bn - 1) / bn) % 2 == 0 ? p45_cluster() : 1;
     CUtensorMap ma, mb;
     const cuuint64_t PL = (cuuint64_t)nparty * L;
