@@ -584,9 +584,11 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                     }
 #pragma unroll
                     for (int c = 0; c < ECOLS; c++) {
-                        u64 acc = 0;
+                        // diagonal dd = 0 of the group enters as a plain add: the epilogue is bound
+                        // by the FMA-heavy pipe (IMAD.WIDE) on short-K tiles
+                        u64 acc = r[0][c];
 #pragma unroll
-                        for (int dd = 0; dd < 4; dd++)
+                        for (int dd = 1; dd < 4; dd++)
                             if (grp * 4 + dd < ND) acc = mad_wide(r[dd][c], 1u << (8 * dd), acc);
                         // acc carries weight 2^(32 grp): combine()'s fold, one group at a time
                         if (grp == 0) {
