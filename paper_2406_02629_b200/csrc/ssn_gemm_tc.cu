@@ -350,7 +350,10 @@ struct Cfg {
 constexpr int EPI_W = 4, EPI_COLS = 8;
 #define SSN_GEMM_W_BOUNDS __maxnreg__(80)
 #else
-constexpr int EPI_W = 8, EPI_COLS = 16;
+#ifndef SSN_GEMM_EPI_W
+#define SSN_GEMM_EPI_W 8
+#endif
+constexpr int EPI_W = SSN_GEMM_EPI_W, EPI_COLS = 16;
 #define SSN_GEMM_W_BOUNDS __maxnreg__(112)
 #endif
 constexpr int THREADS_W = 64 + 32 * EPI_W;              // TMA, MMA, epilogue warps
@@ -539,7 +542,7 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         constexpr int CPW = BN / (EPI_W / 4);               // columns per epilogue warp
         constexpr int ECOLS = EPI_COLS < CPW ? EPI_COLS : CPW;
         constexpr int NPASS = CPW / ECOLS;
-        const int colbase = EPI_W == 8 ? ((warp - 2) >> 2) * CPW : 0;
+        const int colbase = ((warp - 2) >> 2) * CPW;           // EPI_W / 4 warps per lane quarter
         int lt = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
             const int nt = t % ntn, mt = (t / ntn) % ntm, party = t / (ntn * ntm);
@@ -788,6 +791,19 @@ int launch_tc(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int 
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
 }
 
+static int num_sms() {
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        // experiments: cap the persistent GEMM's CTAs (leaves SMs to concurrent chain kernels)
+        const char *e = getenv("SSN_GEMM_GRID");
+        if (e && atoi(e) >= 2 && atoi(e) < nsm) nsm = atoi(e) & ~1;
+    }
+    return nsm;
+}
+
 int launch_p45(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int Kpad, u64 *out, u64 out_pstride,
                u64 ohw, cudaStream_t st, const p45::wide::EpiSub *es = nullptr) {
     using namespace p45;
@@ -800,26 +816,12 @@ int launch_p45(const uint8_t *a, const uint8_t *b, int nparty, int M, int O, int
     if (ohw >= (1ull << 32) || (u64)M * 1 >= (1ull << 31)) return SSN_ERR_UNSUPPORTED;
     const long long ntiles = (long long)ntm * ntn * nparty;
     if (ntiles >= (1ll << 31)) return SSN_ERR_UNSUPPORTED;
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
+    const int nsm = num_sms();
     const int grid = (int)(ntiles < nsm ? ntiles : nsm);
     return launch_wide<0>(bn, cl, grid, st, ma, mb, out, out_pstride, (uint32_t)ohw, O, M, (Kpad + BK - 1) / BK, ntm, ntn,
                           (int)ntiles, wide::ConvGeom{}, es);
 }
 
-static int num_sms() {
-    static int nsm = 0;
-    if (!nsm) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    }
-    return nsm;
-}
 
 // Implicit-GEMM convolution from channel-major limb planes (modes 1 and 2 of k_gemm_p45w).
 int launch_cn(const uint8_t *a, int mode, int nimg, int C, int H, int W, int Wp, const uint8_t *b, int nparty, int O,
