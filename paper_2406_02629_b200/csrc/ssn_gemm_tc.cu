@@ -16,6 +16,7 @@
 // weights once per model, dense activations) and ssn_im2col_limbs (implicit conv unfold
 // S/model.py:354-371 fused with the limb split, shared-memory transposed so both the gather
 // and the plane writes are coalesced).
+#include <cstdio>
 #include <cstdlib>
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -685,6 +686,10 @@ static int launch_wide_bn(int grid, cudaStream_t st, const CUtensorMap &ma, cons
     SSN_COUNT_LAUNCH();
     if constexpr (CL == 1) {
         kern<<<grid, THREADS_W, Cfg<BN>::SMEM, st>>>(ma, mb, out, out_pstride, ohw, O, M, nkb, ntm, ntn, ntiles, geo, es);
+        const cudaError_t e = cudaPeekAtLastError();
+        if (e != cudaSuccess && getenv("SSN_DEBUG"))
+            fprintf(stderr, "k_gemm_p45w<%d,%d,%d,%d> grid %d x %d smem %d: %s\n", AMODE, BN, (int)SUB, CL, grid,
+                    THREADS_W, Cfg<BN>::SMEM, cudaGetErrorString(e));
     } else {
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute at[1];

@@ -1,7 +1,7 @@
 # A/B a list of env settings on the bench: bash tools/ab_env.sh TAG WORKLOAD "ENV1" "ENV2" ...
 T=$1; W=$2; shift 2; O=gpurun_out/$T; mkdir -p $O
 for e in "$@"; do
-  n=$(echo "$e" | tr ' =' '__')
+  n=$(echo "$e" | tr ' =/' '___')
   env $e python bench.py --workload $W --no-cpu-baseline --steps 5 > $O/$n.json 2> $O/$n.err
   python -c "
 import json,sys

@@ -5,5 +5,5 @@ for e in "$@"; do
   n=$(echo "$e" | tr ' =/' '___')
   env $e ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
       --log-file $O/$n.csv python tools/profile_step.py $W $B > $O/$n.log 2>&1
-  echo "== $e"; python tools/kernel_table.py $O/$n.csv 2>/dev/null | grep -E "chain|TOTAL"
+  echo "== $e"; python tools/kernel_table.py $O/$n.csv 2>/dev/null | grep -E "chain|gemm|TOTAL"
 done
