@@ -354,8 +354,11 @@ constexpr int EPI_W = 4, EPI_COLS = 8;
 #ifndef SSN_GEMM_EPI_W
 #define SSN_GEMM_EPI_W 8
 #endif
+#ifndef SSN_GEMM_MAXNREG
+#define SSN_GEMM_MAXNREG 112
+#endif
 constexpr int EPI_W = SSN_GEMM_EPI_W, EPI_COLS = 16;
-#define SSN_GEMM_W_BOUNDS __maxnreg__(112)
+#define SSN_GEMM_W_BOUNDS __maxnreg__(SSN_GEMM_MAXNREG)
 #endif
 constexpr int THREADS_W = 64 + 32 * EPI_W;              // TMA, MMA, epilogue warps
 #ifndef SSN_GEMM_BN_DEFAULT
