@@ -581,14 +581,32 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
     for (uint32_t base = blockIdx.x * span; base < n_out; base += gridDim.x * span) {
         i64 plain[WPT];
         u64 beta[WPT], pre[WPT];
+        u64 cbis[WPT][K - 1];                // unpooled: beta^-1 sharing coefficients, drawn up front
         u64 run = 1;
 #pragma unroll 1
         for (int q = 0; q < WPT; q++) {
             const uint32_t o = base + ((q / G) * CHAIN_THREADS + threadIdx.x) * G + (q % G);
             i64 pl = 0;
             u64 bt = 1;
+            u64 cb1[K - 1];                  // unpooled: the window's beta-share coefficients
             if (o < n_out) {
-                if constexpr (!HF) bt = 1 + ssn_rand_range(a.sseed, a.sstream + 4, o, 0, a.bmax);  // window-constant beta
+                if constexpr (!HF) {
+                    if (!pooled) {
+                        // one dense reservoir per window: 64 bits for beta, then the beta and the
+                        // beta^-1 sharing coefficients (2 Philox calls for (3,5) instead of 3)
+                        constexpr int NCB = (64 + 2 * 45 * (K - 1) + 127) / 128;
+                        Reservoir<NCB> rb;
+                        fill<NCB>(rb, a.sseed, a.sstream + 4, o, 0x900u);
+                        bt = 1 + __umul64hi(take64<NCB>(rb, 0), a.bmax);     // U[1, bmax], bias <= bmax / 2^64
+#pragma unroll
+                        for (int e = 0; e < K - 1; e++) {
+                            cb1[e] = take45<NCB>(rb, 64 + 45 * e);
+                            cbis[q][e] = take45<NCB>(rb, 64 + 45 * (K - 1 + e));
+                        }
+                    } else {
+                        bt = 1 + ssn_rand_range(a.sseed, a.sstream + 4, o, 0, a.bmax);  // window-constant beta
+                    }
+                }
                 uint32_t base_in = o;
                 uint32_t src_base = 0;
                 int sy0 = 0, sx0 = 0;
@@ -631,7 +649,12 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
                             for (int j = 0; j < M; j++) mk[j] = mulm(x[j], a.h_beta[(u64)j * a.per_in + ii]);
                         } else {
                             u64 cb[K - 1];
-                            coeffs<K>(cb, a.sseed, a.sstream + 5, i);
+                            if (pooled) {
+                                coeffs<K>(cb, a.sseed, a.sstream + 5, i);
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < K - 1; e++) cb[e] = cb1[e];
+                            }
 #pragma unroll
                             for (int j = 0; j < M; j++) mk[j] = mulm(x[j], poly_at<K>(bt, cb, j + 1));
                         }
@@ -680,7 +703,11 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
 #pragma unroll
                 for (int g = 0; g < G; g++) {
                     if constexpr (HF) oo[g] = (o0 + g) - fdiv(o0 + g, a.f_per_out) * (uint32_t)a.per_out;
-                    else coeffs<K>(cbi[g], a.sseed, a.sstream + 6, o0 + g);
+                    else if (pooled) coeffs<K>(cbi[g], a.sseed, a.sstream + 6, o0 + g);
+                    else {
+#pragma unroll
+                        for (int e = 0; e < K - 1; e++) cbi[g][e] = cbis[gq * G + g][e];
+                    }
                 }
                 uint8_t *pb = nullptr;
                 int xq = 0;
