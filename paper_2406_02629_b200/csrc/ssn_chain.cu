@@ -387,11 +387,23 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
         }
     }
     constexpr int XB_BACK = poly_bits(K, N) + 1;              // sum_c id^c w_c, w_c < 2^46
-    u64 masked[N];
+    // TRUNC_MASKED travels scaled by S (the common denominator of the reshare: D_v, or the lcm
+    // of R's column denominators for k = 2): rank t sends S * masked_t, the elite reconstructs
+    // S * v and multiplies by S^-1 ONCE -- instead of every rank paying a full field multiply
+    // to undo its D.  The RS check is linear, so it holds on the scaled shares as well.
+    constexpr u64 S = FACTOR ? CC::vi_den : CC::rt_lcm;
+    constexpr u64 SINV = FACTOR ? CC::vi_dinv : CC::rt_lcm_inv;
+    u64 alpha_s = 0, za_s[K - 1];
+    if constexpr (!HF) {
+        alpha_s = lz(alpha * S);
+#pragma unroll
+        for (int e = 0; e < K - 1; e++) za_s[e] = lz(za[e] * S);
+    }
+    u64 masked[N];                                            // S * TRUNC_MASKED[t]
     sfor<0, N>([&](auto tc) {
         constexpr int t = decltype(tc)::value;
         if (t < a.senders) {
-            u64 y;
+            u64 y;                                             // S * (reshared share of rank t)
             if constexpr (FACTOR) {
                 u64 back[K];                                   // D_v * RESHARE_BACK[fr -> t]
 #pragma unroll
@@ -404,26 +416,28 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
                     }
                     back[fr] = acc;
                 }
-                y = mulm(clin<WfRow<K, N>, XB_BACK>(back), CC::vi_dinv);
+                y = clin<WfRow<K, N>, XB_BACK>(back);
             } else {
                 u64 back[K];                                   // D_t * RESHARE_BACK[fr -> t]
 #pragma unroll
                 for (int fr = 0; fr < K; fr++) back[fr] = clin<RtRow<K, N, t>, XB_SUB>(sub[fr]);
                 y = clin<WfRow<K, N>, 46>(back);
-                if constexpr (CC::rt_den(t) != 1) y = mulm(y, CC::rt_dinv(t));
+                if constexpr (S / CC::rt_den(t) != 1) y = lz(y * (S / CC::rt_den(t)));
             }
-            y += a.bias[(u64)t * a.bias_ps + ch];
-            if constexpr (HF) y += a.h_zero[(u64)t * a.per + ii] + a.h_alpha[(u64)t * a.per + ii];
-            else y += poly_at<K>(alpha, za, t + 1);
-            if (t == a.fault_rank && i == 0) y += 1;                                        // test hook
+            u64 add = a.bias[(u64)t * a.bias_ps + ch];
+            if constexpr (HF) add += a.h_zero[(u64)t * a.per + ii] + a.h_alpha[(u64)t * a.per + ii];
+            if (t == a.fault_rank && i == 0) add += 1;                                      // test hook
+            y += add * S;                                                                   // < 2^47 * S
+            if constexpr (!HF) y += poly_at<K>(alpha_s, za_s, t + 1);
             masked[t] = lz(y);
         }
     });
-    // ---- truncation elite: rec over the front, RS check of the extra points, decode/floor/round
+    // ---- truncation elite: rec over the front (x S^-1), RS check of the extra points,
+    //      decode/floor/round
     u64 front[K];
 #pragma unroll
     for (int j = 0; j < K; j++) front[j] = masked[j];
-    const u64 v = canon(clin<WfRow<K, N>, 46>(front));
+    const u64 v = canon(mulm(clin<WfRow<K, N>, 46>(front), SINV));
     sfor<K, N>([&](auto tc) {
         constexpr int t = decltype(tc)::value;
         if (t < a.senders) bad += (canon(clin<ExtRow<K, N, t>, 46>(front)) != canon(masked[t]));

@@ -120,6 +120,9 @@ def emit(k, n):
     lines.append(f"        constexpr uint64_t a[{n}] = {{{', '.join(f'{x}ull' for x in dinv)}}};")
     lines.append("        return a[t];")
     lines.append("    }")
+    Dr = lcm(*dens)
+    lines.append(f"    static constexpr uint64_t rt_lcm = {Dr};             // common denominator of R's columns")
+    lines.append(f"    static constexpr uint64_t rt_lcm_inv = {pow(Dr, P45 - 2, P45)}ull;")
     lines.append(f"    SSN_CC static int64_t vi(int c, int j) {{")
     lines.append(f"        constexpr int64_t a[{k}][{m}] = {{{', '.join(arr(r) for r in vi)}}};")
     lines.append("        return a[c][j];")
