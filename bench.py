@@ -259,8 +259,8 @@ def load_traffic():
 # chain element, by (k, n): ncu smsp__thread_inst_executed / sm__pipe_fmaheavy_cycles_active over the
 # chain kernels of one ResNet-152 step (batch 32) / the step's chain elements (tools/chain_alu.py,
 # profiles/r02/alu/).  The chain kernels are bound by the FMA-heavy pipe that executes IMAD.
-CHAIN_ALU = {(3, 5): 2443, (2, 3): 1498}
-CHAIN_HEAVY = {(3, 5): 91.0, (2, 3): 51.9}
+CHAIN_ALU = {(3, 5): 2451, (2, 3): 1521}
+CHAIN_HEAVY = {(3, 5): 89.3, (2, 3): 49.6}
 
 
 def roofline(kstats, eng, dev_ms, bf16, hbm, src):

@@ -39,9 +39,16 @@ for lid, m in per_launch.items():
     a[0] += 1
     a[1] += m.get("dram__bytes_read.sum", 0) + m.get("dram__bytes_write.sum", 0)
     a[2] += m.get("gpu__time_duration.sum", 0)
+# a protocol-chain CALL (ssn_layer_chain) is one k_chain_plain and, for a nonlinear chain, one
+# k_chain_nonlin; every call follows exactly one share GEMM, so per call = per GEMM launch
+per_launch_bytes = {c: a[1] / a[0] for c, a in agg.items()}
+if "chain" in agg and "gemm" in agg:
+    per_launch_bytes["chain"] = agg["chain"][1] / agg["gemm"][0]
 out = {"how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum over one "
-              "warm step (tools/profile_step.py); cold-cache, serialised launches",
-       "bytes_per_launch": {c: a[1] / a[0] for c, a in agg.items()},
+              "warm step (tools/profile_step.py); cold-cache, serialised launches; chain: per chain call "
+              "(plain + nonlinearity kernel), i.e. per share-GEMM launch",
+       "bytes_per_launch": per_launch_bytes,
+       "bytes_per_step": {c: a[1] for c, a in agg.items()},
        "launches": {c: a[0] for c, a in agg.items()},
        "ms_total": {c: a[2] / 1e6 for c, a in agg.items()}}
 print(json.dumps(out, indent=1))
