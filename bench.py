@@ -241,16 +241,20 @@ def cpu_baseline_sample(model, k, n, verify, budget_s=20.0):
             "s_per_image": s_per_img}
 
 
-def load_traffic():
+def load_traffic(workload=None):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch, averaged per kernel class over
-    one full step, from the committed ncu capture (profiles/<round>/traffic.json), or None."""
+    one full step, from the committed ncu capture (profiles/<round>/traffic.json), or {} when the
+    capture is of another workload."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*", "traffic.json")))
     if not files:
         return {}
     try:
         with open(files[-1]) as fh:
-            return json.load(fh).get("bytes_per_launch", {})
+            d = json.load(fh)
+        if workload is not None and d.get("workload", "resnet152-5pc") != workload:
+            return {}
+        return d.get("bytes_per_launch", {})
     except (OSError, ValueError):
         return {}
 
@@ -263,12 +267,12 @@ CHAIN_ALU = {(3, 5): 2451, (2, 3): 1521}
 CHAIN_HEAVY = {(3, 5): 89.3, (2, 3): 49.6}
 
 
-def roofline(kstats, eng, dev_ms, bf16, hbm, src):
+def roofline(kstats, eng, dev_ms, bf16, hbm, src, workload=None):
     """Roofline of the dominant kernel class of the step (by device time), plus every class.
     gemm: int8 tensor ops = L^2 * 2 * field MACs (L = 6 u8 limbs per 45-bit share) against the
     int8 peak, 2 x measured dense bf16 (sustained: the GEMM runs inside a long step).
     chain / im2col: algorithmic HBM bytes against the measured copy bandwidth."""
-    traffic = load_traffic()
+    traffic = load_traffic(workload)
     L2 = eng.limb_products()
     i8 = measured_int8()
     if i8:                       # measured int8 tensor peak (sustained: the GEMM runs inside a long step)
@@ -300,7 +304,8 @@ def roofline(kstats, eng, dev_ms, bf16, hbm, src):
                 # element (ncu, profiles/r01/README.md) x elements / time vs the SM issue peak
                 rate = alu * st["elems_per_launch"] / sec
                 peak_i = 148 * 128 * 1.965e9
-                r["alu_issue"] = {"thread_instr_per_elem": alu, "calibration": "ncu count, tools/chain_alu.py",
+                r["alu_issue"] = {"thread_instr_per_elem": alu,
+                                  "calibration": "ncu count, tools/chain_alu.py on ResNet-152 (batch 32) for this (k, n)",
                                   "achieved_tinstr_per_s": float(f"{rate:.4g}"),
                                   "peak_tinstr_per_s": float(f"{peak_i:.4g}"), "frac": round(rate / peak_i, 4)}
                 hv = CHAIN_HEAVY.get((eng.k, eng.n))
@@ -996,7 +1001,7 @@ def main():
     e2e = imgs / (e2e_ms / 1000.0)
     hbm, bf16, src = measured_peaks()
     online, offline = eng.comm_per_image()
-    roof, by_kernel = roofline(kstats, eng, dev_ms, bf16, hbm, src)
+    roof, by_kernel = roofline(kstats, eng, dev_ms, bf16, hbm, src, workload=args.workload)
     cpu = None
     if not args.no_cpu_baseline and world == 1:          # the CPU baseline is an N=1 figure
         try:

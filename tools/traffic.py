@@ -1,6 +1,6 @@
 """Aggregate an ncu --csv launch list with dram__bytes_{read,write}.sum and
 gpu__time_duration.sum into per-kernel-class DRAM traffic per launch (bench.py's
-roofline.traffic).  Usage: python tools/traffic.py launches.csv > profiles/rNN/traffic.json"""
+roofline.traffic).  Usage: python tools/traffic.py launches.csv [workload] > profiles/rNN/traffic.json"""
 import csv
 import json
 import sys
@@ -47,6 +47,7 @@ if "chain" in agg and "gemm" in agg:
 out = {"how": "ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum over one "
               "warm step (tools/profile_step.py); cold-cache, serialised launches; chain: per chain call "
               "(plain + nonlinearity kernel), i.e. per share-GEMM launch",
+       "workload": sys.argv[2] if len(sys.argv) > 2 else "resnet152-5pc",
        "bytes_per_launch": per_launch_bytes,
        "bytes_per_step": {c: a[1] for c, a in agg.items()},
        "launches": {c: a[0] for c, a in agg.items()},
