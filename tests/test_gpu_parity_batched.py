@@ -88,6 +88,14 @@ def test_verified_run_shares_equal_reference(P, fuse):
     _check(P, _models(P)["tiny-resnet"], 3, 5, fuse=fuse, verify=True)
 
 
+@pytest.mark.parametrize("verify", [False, True])
+def test_fused_chain_4_7_shares_equal_reference(P, verify):
+    """(4,7): the chain's factored reshare (wide R numerators, sub-shares folded before the
+    B^-1 columns) and its 720-scaled TRUNC_MASKED, against the reference stream."""
+    eng, cap = _check(P, _models(P)["tiny-resnet"], 4, 7, fuse=True, verify=verify, B=2)
+    assert any(ch[-1] in cap for ch in eng.chains.values())
+
+
 # ---------------------------------------------------------------- reference-composed fixtures
 import json  # noqa: E402
 import os  # noqa: E402
