@@ -27,11 +27,12 @@
 // followed by k_chain_nonlin<SPLIT> -- two kernels of half the code each beat one kernel that
 // overflows the instruction cache (profiles/r01/README.md).
 //
-// The kernels are specialised to keep their SASS small (they are instruction-fetch bound
-// otherwise): the field must be pseudo-Mersenne with masked uniform draws (the default
-// p = 2^45 - 55, S/field.py:21) and every protocol constant must be a small rational (true
-// for the default party ids 1..n).  ssn_chain_supported() tells the host; other schemes use
-// the unfused kernels of ssn_elementwise.cu.
+// The kernels are specialised to the default field p = 2^45 - 55 (S/field.py:21, pseudo-Mersenne
+// with masked uniform draws) and to the default party ids 1..n, whose protocol constants are
+// compile-time integers (ssn_chain_consts.cuh).  They are bound by the FMA-heavy pipe (IMAD), so
+// the arithmetic is arranged to spend as few IMAD / IMAD.WIDE as possible.
+// ssn_chain_supported() tells the host; other schemes use the unfused kernels of
+// ssn_elementwise.cu.
 #include <cstdlib>
 #include <cstring>
 #include "ssn.h"
@@ -192,7 +193,8 @@ struct ChainArgs {
     int gather, gh, gw, gs, gp;
 };
 
-// Co-scheduling with the persistent share GEMM (SSN_COSCHED, default on): the chain kernels are
+// Co-scheduling with the persistent share GEMM (-DSSN_COSCHED=1, off: measured slower,
+// profiles/r02/README.md): the chain kernels are
 // shaped so that AT MOST TWO of their blocks fit on an SM and two always leave room for one GEMM
 // CTA (192 threads x 80 registers + its shared memory).  Whatever order the block scheduler sees
 // the launches of the two CUDA streams in, a GEMM CTA never waits for chain blocks to drain, so
@@ -210,6 +212,7 @@ constexpr int PLAIN_THREADS = 256;
 #else
 constexpr int CHAIN_THREADS = 128;
 constexpr int PLAIN_THREADS = 128;
+// default: k_chain_plain at 6 CTAs/SM (80 registers, no spill), k_chain_nonlin at 7
 #ifndef SSN_PLAIN_MINB
 #define SSN_PLAIN_MINB 6
 #endif
