@@ -360,7 +360,7 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
         // e = 1 + U[0, emax) by multiply-shift of 64 random bits (bias <= emax / 2^64 <= 2^-32)
         const u64 e = 1 + __umul64hi(take64<NCS>(rs, 45 * 3 * (K - 1)), a.emax);
         const u64 em = red64(e);
-        alpha = mulm(em, a.stepm);
+        alpha = mulm_hs(em, a.stepm);                        // both canonical
         comp = em ? PP - em : 0;
     }
     const uint32_t bq = fdiv(i, a.bias_div);
@@ -440,7 +440,7 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
     u64 front[K];
 #pragma unroll
     for (int j = 0; j < K; j++) front[j] = masked[j];
-    const u64 v = canon(mulm(clin<WfRow<K, N>, 46>(front), SINV));
+    const u64 v = canon(mulm_hs(clin<WfRow<K, N>, 46>(front), SINV));      // lazy x canonical
     sfor<K, N>([&](auto tc) {
         constexpr int t = decltype(tc)::value;
         if (t < a.senders) bad += (canon(clin<ExtRow<K, N, t>, 46>(front)) != canon(masked[t]));
@@ -527,9 +527,10 @@ __device__ __forceinline__ u64 mulm32(u64 a, uint32_t b) {
 
 // NONLIN_PLAIN * (beta^-1 share), canonical: the elite's plaintext f(x * beta) is a signed value
 // with |f(x * beta)| < p/2 by the choice of bmax (S/masks.py:57-64), encoded, times the share.
+template <bool HS>
 __device__ __forceinline__ u64 mul_plain(i64 sv, u64 b) {
-    const u64 pl = sv < 0 ? (u64)((i64)PP + sv) : (u64)sv;
-    return canon(mulm(pl, b));
+    const u64 pl = sv < 0 ? (u64)((i64)PP + sv) : (u64)sv;     // < p < 2^45
+    return canon(HS ? mulm_hs(pl, b) : mulm(pl, b));
 }
 
 // run^-1 for every thread of the block from ONE Fermat inversion (Montgomery's batch trick):
@@ -663,7 +664,7 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
                         if constexpr (HF) {
                             const uint32_t ii = i - fdiv(i, a.f_per_in) * (uint32_t)a.per_in;
 #pragma unroll
-                            for (int j = 0; j < M; j++) mk[j] = mulm(x[j], a.h_beta[(u64)j * a.per_in + ii]);
+                            for (int j = 0; j < M; j++) mk[j] = mulm_hs(x[j], a.h_beta[(u64)j * a.per_in + ii]);
                         } else {
                             u64 cb[K - 1];
                             if (pooled) {
@@ -673,7 +674,11 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
                                 for (int e = 0; e < K - 1; e++) cb[e] = cb1[e];
                             }
 #pragma unroll
-                            for (int j = 0; j < M; j++) mk[j] = mulm(x[j], poly_at<K>(bt, cb, j + 1));
+                            for (int j = 0; j < M; j++) {
+                                // x canonical (< 2^45), the beta share < 2^50 for k <= 3
+                                if constexpr (K <= 3) mk[j] = mulm_hs(x[j], poly_at<K>(bt, cb, j + 1));
+                                else mk[j] = mulm(x[j], poly_at<K>(bt, cb, j + 1));
+                            }
                         }
                         const u64 v = canon(clin<WpRow<K, N>, 46>(mk));
                         i64 sv = v > PHALF ? (i64)v - (i64)PP : (i64)v;
@@ -709,7 +714,7 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
                     if (a.inv_table) {
                         binv[g] = pre[q];
                     } else {
-                        binv[g] = mulm(inv, pre[q]);
+                        binv[g] = mulm_hs(inv, pre[q]);            // both lazy, < 2^46
                         inv = mulm32(inv, (uint32_t)beta[q]);
                     }
                 }
@@ -757,7 +762,8 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
 #pragma unroll
                             for (int e = 0; e < K - 1; e++) bis += mul_small(cbi[g][e], pw[e]);
                         }
-                        v[g] = mul_plain(plain[gq * G + g], bis);
+                        // the beta^-1 share: canonical (host-fed) or < 2^50 for k <= 3
+                        v[g] = mul_plain<HF || K <= 3>(plain[gq * G + g], bis);
                     }
                     if constexpr (G == 1) {
                         op[0] = v[0];

@@ -59,6 +59,18 @@ __device__ __forceinline__ u64 mulm(u64 a, u64 b) {
     const u64 q = (hi << (64 - PS)) | (lo >> PS);
     return lz(q * PC + (lo & PMASK));
 }
+// mulm for operands whose high halves multiply below 2^32 ((a >> 32) * (b >> 32) < 2^32, e.g.
+// a < 2^45 and b < 2^51): the top partial product is one 32-bit IMAD instead of an IMAD.WIDE
+__device__ __forceinline__ u64 mulm_hs(u64 a, u64 b) {
+    const uint32_t al = (uint32_t)a, ah = (uint32_t)(a >> 32), bl = (uint32_t)b, bh = (uint32_t)(b >> 32);
+    const u64 p0 = (u64)al * bl;
+    const u64 p1 = (u64)al * bh + (u64)ah * bl;
+    const uint32_t p2 = ah * bh;
+    const u64 lo = p0 + (p1 << 32);
+    const u64 hi = (u64)p2 + (p1 >> 32) + (lo < p0);
+    const u64 q = (hi << (64 - PS)) | (lo >> PS);
+    return lz(q * PC + (lo & PMASK));
+}
 // sum_j n_j x_j / D for lazy x_j (< 2^46), |n_j| < 2^13, M <= 7.  With non-negative
 // nn_j = n_j + off the products split into 32-bit halves: sum nn_j lo_j (< 2^49, one
 // IMAD.WIDE each) + (sum nn_j hi_j) << 32 (hi < 2^14, < 2^31) -- then subtract off * sum x_j.
