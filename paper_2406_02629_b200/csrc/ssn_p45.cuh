@@ -59,18 +59,31 @@ __device__ __forceinline__ u64 mulm(u64 a, u64 b) {
     const u64 q = (hi << (64 - PS)) | (lo >> PS);
     return lz(q * PC + (lo & PMASK));
 }
-// mulm for operands whose high halves multiply below 2^32 ((a >> 32) * (b >> 32) < 2^32, e.g.
-// a < 2^45 and b < 2^51): the top partial product is one 32-bit IMAD instead of an IMAD.WIDE
+// mulm for a * b < 2^96 (e.g. a < 2^45 and b < 2^51, or both < 2^48): the product's top word
+// fits 32 bits, so its partial products are three 32x32->64 multiplies and one 32-bit
+// multiply-add-with-carry, and the fold is  (lo mod 2^45) + 55 (lo >> 45) + 55 * 2^19 * hi.
+// Written in PTX: the C form compiled to ~30% more FMA-heavy pipe work (extra VIADD/IMAD.MOV).
 __device__ __forceinline__ u64 mulm_hs(u64 a, u64 b) {
     const uint32_t al = (uint32_t)a, ah = (uint32_t)(a >> 32), bl = (uint32_t)b, bh = (uint32_t)(b >> 32);
-    const u64 p0 = (u64)al * bl;
-    const u64 p1 = (u64)al * bh + (u64)ah * bl;
-    const uint32_t p2 = ah * bh;
-    const u64 lo = p0 + (p1 << 32);
-    const u64 hi = (u64)p2 + (p1 >> 32) + (lo < p0);
-    const u64 q = (hi << (64 - PS)) | (lo >> PS);
-    return lz(q * PC + (lo & PMASK));
+    uint32_t lo_lo, lo_hi, hi;
+    asm("{\n\t.reg .u32 p0l, p0h, p1l, p1h, p2;\n\t.reg .u64 p0, p1;\n\t"
+        "mul.wide.u32 p0, %3, %5;\n\t"
+        "mul.wide.u32 p1, %3, %6;\n\t"
+        "mad.wide.u32 p1, %4, %5, p1;\n\t"
+        "mul.lo.u32 p2, %4, %6;\n\t"
+        "mov.b64 {p0l, p0h}, p0;\n\t"
+        "mov.b64 {p1l, p1h}, p1;\n\t"
+        "mov.u32 %0, p0l;\n\t"
+        "add.cc.u32 %1, p0h, p1l;\n\t"
+        "addc.u32 %2, p1h, p2;\n\t}"
+        : "=r"(lo_lo), "=r"(lo_hi), "=r"(hi)
+        : "r"(al), "r"(ah), "r"(bl), "r"(bh));
+    const uint32_t t1 = (lo_hi >> (PS - 32)) * (uint32_t)PC;                 // 55 (lo >> 45) < 2^25
+    const u64 t2 = (u64)hi * (PC << (64 - PS));                             // 55 2^19 hi < 2^57
+    const u64 low = ((u64)(lo_hi & ((1u << (PS - 32)) - 1)) << 32) | lo_lo;  // lo mod 2^45
+    return lz(low + t1 + t2);
 }
+
 // sum_j n_j x_j / D for lazy x_j (< 2^46), |n_j| < 2^13, M <= 7.  With non-negative
 // nn_j = n_j + off the products split into 32-bit halves: sum nn_j lo_j (< 2^49, one
 // IMAD.WIDE each) + (sum nn_j hi_j) << 32 (hi < 2^14, < 2^31) -- then subtract off * sum x_j.
