@@ -516,14 +516,7 @@ __device__ __noinline__ void emit_planes(uint8_t *row, u64 v, int xq, int copies
 
 // a * b mod p (lazy) for a < 2^46 and b < 2^32 (beta, a running product times beta): two
 // 32x32->64 products instead of three
-__device__ __forceinline__ u64 mulm32(u64 a, uint32_t b) {
-    const u64 p0 = (u64)(uint32_t)a * b;
-    const u64 p1 = (u64)(uint32_t)(a >> 32) * b;          // < 2^46
-    const u64 lo = p0 + (p1 << 32);
-    const u64 hi = (p1 >> 32) + (lo < p0);
-    const u64 q = (hi << (64 - PS)) | (lo >> PS);          // < 2^33
-    return lz(q * PC + (lo & PMASK));
-}
+__device__ __forceinline__ u64 mulm32(u64 a, uint32_t b) { return mulm_s32(a, b); }
 
 // NONLIN_PLAIN * (beta^-1 share), canonical: the elite's plaintext f(x * beta) is a signed value
 // with |f(x * beta)| < p/2 by the choice of bmax (S/masks.py:57-64), encoded, times the share.

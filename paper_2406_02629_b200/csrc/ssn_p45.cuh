@@ -84,6 +84,27 @@ __device__ __forceinline__ u64 mulm_hs(u64 a, u64 b) {
     return lz(low + t1 + t2);
 }
 
+// a * b mod p (lazy) for a < 2^64 / b < 2^32 with a * b < 2^96: two 32x32->64 multiplies, the
+// mulm_hs fold
+__device__ __forceinline__ u64 mulm_s32(u64 a, uint32_t b) {
+    const uint32_t al = (uint32_t)a, ah = (uint32_t)(a >> 32);
+    uint32_t lo_lo, lo_hi, hi;
+    asm("{\n\t.reg .u32 p0l, p0h, p1l, p1h;\n\t.reg .u64 p0, p1;\n\t"
+        "mul.wide.u32 p0, %3, %5;\n\t"
+        "mul.wide.u32 p1, %4, %5;\n\t"
+        "mov.b64 {p0l, p0h}, p0;\n\t"
+        "mov.b64 {p1l, p1h}, p1;\n\t"
+        "mov.u32 %0, p0l;\n\t"
+        "add.cc.u32 %1, p0h, p1l;\n\t"
+        "addc.u32 %2, p1h, 0;\n\t}"
+        : "=r"(lo_lo), "=r"(lo_hi), "=r"(hi)
+        : "r"(al), "r"(ah), "r"(b));
+    const uint32_t t1 = (lo_hi >> (PS - 32)) * (uint32_t)PC;
+    const u64 t2 = (u64)hi * (PC << (64 - PS));
+    const u64 low = ((u64)(lo_hi & ((1u << (PS - 32)) - 1)) << 32) | lo_lo;
+    return lz(low + t1 + t2);
+}
+
 // sum_j n_j x_j / D for lazy x_j (< 2^46), |n_j| < 2^13, M <= 7.  With non-negative
 // nn_j = n_j + off the products split into 32-bit halves: sum nn_j lo_j (< 2^49, one
 // IMAD.WIDE each) + (sum nn_j hi_j) << 32 (hi < 2^14, < 2^31) -- then subtract off * sum x_j.
