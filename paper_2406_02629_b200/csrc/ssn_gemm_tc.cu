@@ -360,7 +360,6 @@ constexpr int EPI_W = 4, EPI_COLS = 8;
 constexpr int EPI_W = SSN_GEMM_EPI_W, EPI_COLS = 16;
 #define SSN_GEMM_W_BOUNDS __maxnreg__(SSN_GEMM_MAXNREG)
 #endif
-constexpr int THREADS_W = 64 + 32 * EPI_W;              // TMA, MMA, epilogue warps
 #ifndef SSN_GEMM_BN_DEFAULT
 #define SSN_GEMM_BN_DEFAULT 32
 #endif
@@ -409,7 +408,7 @@ __device__ __forceinline__ void tmem_ld_cols(uint32_t taddr, uint32_t (&r)[NC]) 
 // L2 -> SM traffic (A is 48 of the 60 KB a stage moves; at the tensor pipe's rate the unshared
 // stream needs ~50 B/clk per SM, above the L2's share per SM).  The stage's `empty` barrier then
 // waits for both CTAs' MMA warps (commit multicast to the pair).
-template <int AMODE, int BN, bool SUB = false, int CL = 1>
+template <int AMODE, int BN, bool SUB = false, int CL = 1, int EW = EPI_W>
 __global__ void SSN_GEMM_W_BOUNDS
 k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, u64 *__restrict__ out,
             u64 out_pstride, uint32_t ohw, int O, int M, int nkb, int ntm, int ntn, int ntiles, ConvGeom geo,
@@ -438,7 +437,7 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         }
         for (int b = 0; b < NBUF; b++) {
             mbar_init(&tfull[b], 1);
-            mbar_init(&tempty[b], EPI_W);
+            mbar_init(&tempty[b], EW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -543,10 +542,10 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
         // 16-column half each, with 4 warps one warp drains all 32 columns, EPI_COLS per pass
         const int q = warp & 3;
         const uint32_t lane_off = (uint32_t)(q * 32) << 16;
-        constexpr int CPW = BN / (EPI_W / 4);               // columns per epilogue warp
+        constexpr int CPW = BN / (EW / 4);                  // columns per epilogue warp
         constexpr int ECOLS = EPI_COLS < CPW ? EPI_COLS : CPW;
         constexpr int NPASS = CPW / ECOLS;
-        const int colbase = ((warp - 2) >> 2) * CPW;           // EPI_W / 4 warps per lane quarter
+        const int colbase = ((warp - 2) >> 2) * CPW;           // EW / 4 warps per lane quarter
         int lt = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, lt++) {
             const int nt = t % ntn, mt = (t / ntn) % ntm, party = t / (ntn * ntm);
@@ -674,12 +673,13 @@ static int p45_bn(int kpad) {
     return kpad <= kmax ? 16 : SSN_GEMM_BN_DEFAULT;
 }
 
-template <int AMODE, int BN, bool SUB = false, int CL = 1>
+template <int AMODE, int BN, bool SUB = false, int CL = 1, int EW = p45::wide::EPI_W>
 static int launch_wide_bn(int grid, cudaStream_t st, const CUtensorMap &ma, const CUtensorMap &mb, u64 *out,
                           u64 out_pstride, uint32_t ohw, int O, int M, int nkb, int ntm, int ntn, int ntiles,
                           p45::wide::ConvGeom geo, const p45::wide::EpiSub &es) {
     using namespace p45::wide;
-    auto kern = k_gemm_p45w<AMODE, BN, SUB, CL>;
+    auto kern = k_gemm_p45w<AMODE, BN, SUB, CL, EW>;
+    constexpr int THREADS = 64 + 32 * EW;             // TMA, MMA, epilogue warps
     static bool attr = false;
     if (!attr) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg<BN>::SMEM) != cudaSuccess)
@@ -688,11 +688,11 @@ static int launch_wide_bn(int grid, cudaStream_t st, const CUtensorMap &ma, cons
     }
     SSN_COUNT_LAUNCH();
     if constexpr (CL == 1) {
-        kern<<<grid, THREADS_W, Cfg<BN>::SMEM, st>>>(ma, mb, out, out_pstride, ohw, O, M, nkb, ntm, ntn, ntiles, geo, es);
+        kern<<<grid, THREADS, Cfg<BN>::SMEM, st>>>(ma, mb, out, out_pstride, ohw, O, M, nkb, ntm, ntn, ntiles, geo, es);
         const cudaError_t e = cudaPeekAtLastError();
         if (e != cudaSuccess && getenv("SSN_DEBUG"))
             fprintf(stderr, "k_gemm_p45w<%d,%d,%d,%d> grid %d x %d smem %d: %s\n", AMODE, BN, (int)SUB, CL, grid,
-                    THREADS_W, Cfg<BN>::SMEM, cudaGetErrorString(e));
+                    THREADS, Cfg<BN>::SMEM, cudaGetErrorString(e));
     } else {
         cudaLaunchConfig_t cfg = {};
         cudaLaunchAttribute at[1];
@@ -701,7 +701,7 @@ static int launch_wide_bn(int grid, cudaStream_t st, const CUtensorMap &ma, cons
         at[0].val.clusterDim.y = 1;
         at[0].val.clusterDim.z = 1;
         cfg.gridDim = dim3((unsigned)(grid - grid % CL));
-        cfg.blockDim = dim3(THREADS_W);
+        cfg.blockDim = dim3(THREADS);
         cfg.dynamicSmemBytes = Cfg<BN>::SMEM;
         cfg.stream = st;
         cfg.attrs = at;
@@ -735,11 +735,20 @@ static int launch_wide(int bn, int cl, int grid, cudaStream_t st, const CUtensor
                                                geo, *es);
         return SSN_ERR_UNSUPPORTED;
     }
-    if (cl == 2)
+    if (cl == 2) {
+        // the 3x3 implicit GEMMs are MMA-bound (epilogue warps idle ~85%): with SSN_GEMM_EW2=4 they
+        // run 4 epilogue warps, a smaller CTA that leaves room for co-resident chain blocks
+        if constexpr (AMODE == 2) {
+            static const int ew2 = getenv("SSN_GEMM_EW2") ? atoi(getenv("SSN_GEMM_EW2")) : 8;
+            if (ew2 == 4 && bn == 32)
+                return launch_wide_bn<AMODE, 32, false, 2, 4>(grid, st, ma, mb, out, out_pstride, ohw, O, M, nkb, ntm,
+                                                              ntn, ntiles, geo, none);
+        }
         return bn == 16 ? launch_wide_bn<AMODE, 16, false, 2>(grid, st, ma, mb, out, out_pstride, ohw, O, M, nkb, ntm,
                                                               ntn, ntiles, geo, none)
                         : launch_wide_bn<AMODE, 32, false, 2>(grid, st, ma, mb, out, out_pstride, ohw, O, M, nkb, ntm,
                                                               ntn, ntiles, geo, none);
+    }
     return bn == 16 ? launch_wide_bn<AMODE, 16>(grid, st, ma, mb, out, out_pstride, ohw, O, M, nkb, ntm, ntn, ntiles,
                                                 geo, none)
                     : launch_wide_bn<AMODE, 32>(grid, st, ma, mb, out, out_pstride, ohw, O, M, nkb, ntm, ntn, ntiles,
