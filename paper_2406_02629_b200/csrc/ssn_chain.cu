@@ -834,7 +834,11 @@ static u64 chain_grid_cap(KernT kern, int threads) {
             return cache[e].cap;
     int nsm = 0, per_sm = 0;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    ssn_prefer_max_smem(kern);
+    // shared-memory carveout: the driver's default leaves the L1 large enough to keep the
+    // nonlinearity's G-strided scratch loads (G = 4 kernels -11%, step +1%); SSN_CHAIN_CARVEOUT=1
+    // asks for the maximum (a 185 KB share-GEMM CTA then co-resides without an SM reconfiguration)
+    static const int carve = getenv("SSN_CHAIN_CARVEOUT") ? atoi(getenv("SSN_CHAIN_CARVEOUT")) : 0;
+    if (carve) ssn_prefer_max_smem(kern);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, 0) != cudaSuccess || per_sm < 1)
         per_sm = 4;
     const char *env = getenv("SSN_CHAIN_WAVES");
