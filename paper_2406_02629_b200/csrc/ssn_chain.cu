@@ -319,7 +319,9 @@ __device__ __forceinline__ u64 trunc_val(u64 v, const ChainArgs &a) {
 //    row paying one full modular multiply;
 //  * a rank adds the zero share and the alpha share it receives as one polynomial evaluation of
 //    the summed coefficients (the same integer), likewise the fresh truncation share and comp.
-template <int K, int N, bool HF>
+// RAW: leave the outputs unreduced (< 2^58; the caller canonicalises them for the store) instead
+// of lazily reduced (< 2^46, the nonlinearity's multiply operands)
+template <int K, int N, bool HF, bool RAW = false>
 __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (&x)[N], unsigned long long &bad) {
     constexpr int M = 2 * K - 1;
     using CC = ChainConsts<K, N>;
@@ -462,7 +464,7 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
         if constexpr (HF) s = poly_at<K>(tm, g, t + 1) + a.h_comp[(u64)t * a.per + ii];
         else s = poly_at<K>(tm + comp, g, t + 1);
         if (a.other) s += a.other[(u64)t * a.other_ps + i];                              // residual add
-        x[t] = lz(s);                                                                   // lazy
+        x[t] = RAW ? s : lz(s);
     }
 }
 
@@ -473,7 +475,7 @@ __global__ void SSN_PLAIN_BOUNDS k_chain_plain(ChainArgs a, SsnField f) {
 #pragma unroll 1
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nel; i += gridDim.x * blockDim.x) {
         u64 x[N];
-        chain_elem<K, N, HF>(a, i, x, bad);
+        chain_elem<K, N, HF, true>(a, i, x, bad);
 #pragma unroll
         for (int t = 0; t < N; t++) a.out[(u64)t * a.out_ps + i] = canon(x[t]);
     }
