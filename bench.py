@@ -260,11 +260,11 @@ def load_traffic(workload=None):
 
 
 # executed thread instructions and FMA-heavy pipe cycles (per SM, 4 pipe slots per SM per cycle) per
-# chain element, by (k, n): ncu smsp__thread_inst_executed / sm__pipe_fmaheavy_cycles_active over the
+# chain element, by workload: ncu smsp__thread_inst_executed / sm__pipe_fmaheavy_cycles_active over the
 # chain kernels of one ResNet-152 step (batch 32) / the step's chain elements (tools/chain_alu.py,
 # profiles/r02/alu/).  The chain kernels are bound by the FMA-heavy pipe that executes IMAD.
-CHAIN_ALU = {(3, 5): 2451, (2, 3): 1521}
-CHAIN_HEAVY = {(3, 5): 89.3, (2, 3): 49.6}
+CHAIN_ALU = {"resnet152-5pc": 2263, "resnet152-3pc": 1388}
+CHAIN_HEAVY = {"resnet152-5pc": 82.7, "resnet152-3pc": 44.9}
 
 
 def roofline(kstats, eng, dev_ms, bf16, hbm, src, workload=None):
@@ -298,17 +298,17 @@ def roofline(kstats, eng, dev_ms, bf16, hbm, src, workload=None):
             r = {"bound": "hbm", "achieved": round(achieved, 1), "peak": round(hbm, 1), "unit": "GB/s",
                  "frac": round(achieved / hbm, 4),
                  "note": "algorithmic bytes per launch (DESIGN.md section 3) / CUDA-event launch time"}
-            alu = CHAIN_ALU.get((eng.k, eng.n)) if cls == "chain" else None
+            alu = CHAIN_ALU.get(workload) if cls == "chain" else None      # calibrated per workload
             if alu and st.get("elems_per_launch"):
                 # the fused protocol chain is integer-ALU bound: executed thread instructions per
                 # element (ncu, profiles/r01/README.md) x elements / time vs the SM issue peak
                 rate = alu * st["elems_per_launch"] / sec
                 peak_i = 148 * 128 * 1.965e9
                 r["alu_issue"] = {"thread_instr_per_elem": alu,
-                                  "calibration": "ncu count, tools/chain_alu.py on ResNet-152 (batch 32) for this (k, n)",
+                                  "calibration": "ncu count, tools/chain_alu.py on this workload (batch 32)",
                                   "achieved_tinstr_per_s": float(f"{rate:.4g}"),
                                   "peak_tinstr_per_s": float(f"{peak_i:.4g}"), "frac": round(rate / peak_i, 4)}
-                hv = CHAIN_HEAVY.get((eng.k, eng.n))
+                hv = CHAIN_HEAVY.get(workload)
                 if hv:
                     # FMA-heavy pipe: hv SM-cycles per element (4 slots per SM per cycle) vs 148 SMs x clock
                     hrate = hv * st["elems_per_launch"] / sec
