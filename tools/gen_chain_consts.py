@@ -137,7 +137,7 @@ def emit(k, n):
     return "\n".join(lines)
 
 
-def main():
+def render():
     body = [
         "// ssn_chain_consts.cuh -- GENERATED by tools/gen_chain_consts.py; do not edit.",
         "// Protocol constants of the fused chain kernels for the default party ids 1..n as exact",
@@ -151,10 +151,16 @@ def main():
     for k, n in SCHEMES:
         body.append(emit(k, n))
     body.append("}  // namespace ssn45")
-    path = os.path.join(ROOT, "paper_2406_02629_b200", "csrc", "ssn_chain_consts.cuh")
-    with open(path, "w") as f:
-        f.write("\n".join(body) + "\n")
-    print("wrote", path)
+    return "\n".join(body) + "\n"
+
+
+PATH = os.path.join(ROOT, "paper_2406_02629_b200", "csrc", "ssn_chain_consts.cuh")
+
+
+def main():
+    with open(PATH, "w") as f:
+        f.write(render())
+    print("wrote", PATH)
 
 
 if __name__ == "__main__":
