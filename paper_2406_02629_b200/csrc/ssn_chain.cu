@@ -33,6 +33,7 @@
 // the arithmetic is arranged to spend as few IMAD / IMAD.WIDE as possible.
 // ssn_chain_supported() tells the host; other schemes use the unfused kernels of
 // ssn_elementwise.cu.
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include "ssn.h"
@@ -862,8 +863,10 @@ static int nonlin_group(const ChainArgs &a, const ssn_chain_desc *d, u64 n_out) 
         if (a.planes) {
             const bool rows = ow % g == 0;
             const bool contig = (u64)a.pl_wp == ow && a.pl_is == oh * ow && (oh * ow) % g == 0;
+            // the row pitch matters only when groups stay inside rows; a contiguous channel plane
+            // (1x1 layout) needs only the group start aligned (pix0 % g == 0)
             if (!(rows || contig) || a.pl_copies != 1 || a.pl_ps % g || a.pl_ls % g || a.pl_cs % g ||
-                a.pl_is % g || (u64)a.pl_wp % g || ((uintptr_t)a.planes % g))
+                a.pl_is % g || (!contig && (u64)a.pl_wp % g) || ((uintptr_t)a.planes % g))
                 continue;
         }
         return g;
@@ -895,6 +898,9 @@ int launch_kernels(const ChainArgs &a, const SsnField &f, const ssn_chain_desc *
         const u64 n_out = (u64)d->nb * d->c * (d->h / d->kh) * (d->w / d->kw);
         const bool split = d->scratch || d->nonlin_only;
         const int G = split ? nonlin_group(a, d, n_out) : 1;
+        if (getenv("SSN_DEBUG"))
+            fprintf(stderr, "chain nonlin G=%d c=%d h=%d w=%d kh=%d planes=%d wp=%d is=%llu copies=%d\n", G, d->c, d->h,
+                    d->w, d->kh, a.planes != nullptr, a.pl_wp, (unsigned long long)a.pl_is, a.pl_copies);
         if (split && !d->nonlin_only) {
             // split: reshare + truncation (+ add) into scratch [n][nel], then the nonlinearity
             ChainArgs a1 = a;
