@@ -557,7 +557,10 @@ __device__ __noinline__ u64 block_batch_inverse(u64 run, int lane, int warp, u64
 // comes from ONE Fermat inversion (Montgomery's batch trick): per-thread running products,
 // warp-shuffle exclusive prefix/suffix products, one inversion of the block total by warp 0,
 // then a backward pass.
-constexpr int WPT = 8;
+#ifndef SSN_WPT
+#define SSN_WPT 8
+#endif
+constexpr int WPT = SSN_WPT;
 constexpr int NWARP = CHAIN_THREADS / 32;
 
 // byte l of each of the G values, packed little-endian (window g -> byte g)
