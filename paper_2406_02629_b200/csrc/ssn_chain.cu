@@ -192,6 +192,9 @@ struct ChainArgs {
     // (y0, x0) element (wy, wx) is source element (y0*gs - gp + wy, x0*gs - gp + wx) of the
     // (c, gh, gw) chain output, or a zero share outside it
     int gather, gh, gw, gs, gp;
+    // element / window range of this launch (a chain split into L2-sized chunks: the nonlinearity
+    // of a chunk reads the scratch its plain kernel just wrote while it is still in L2)
+    uint32_t r_lo, r_hi;
 };
 
 // Co-scheduling with the persistent share GEMM (-DSSN_COSCHED=1, off: measured slower,
@@ -472,9 +475,9 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
 template <int K, int N, bool HF>
 __global__ void SSN_PLAIN_BOUNDS k_chain_plain(ChainArgs a, SsnField f) {
     unsigned long long bad = 0;
-    const uint32_t nel = (uint32_t)a.nel;
+    const uint32_t nel = (uint32_t)a.nel < a.r_hi ? (uint32_t)a.nel : a.r_hi;
 #pragma unroll 1
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nel; i += gridDim.x * blockDim.x) {
+    for (uint32_t i = a.r_lo + blockIdx.x * blockDim.x + threadIdx.x; i < nel; i += gridDim.x * blockDim.x) {
         u64 x[N];
         chain_elem<K, N, HF, true>(a, i, x, bad);
 #pragma unroll
@@ -590,12 +593,13 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t oh = a.h / a.kh, ow = a.w / a.kw;
     const uint32_t hw = oh * ow, chw = (uint32_t)a.c * hw;
-    const uint32_t n_out = (uint32_t)a.nb * chw;
+    const uint32_t n_all = (uint32_t)a.nb * chw;
+    const uint32_t n_out = n_all < a.r_hi ? n_all : a.r_hi;   // end of this launch's window range
     const bool pooled = a.kh != 1 || a.kw != 1;
     const bool batch_inv = !HF && !a.inv_table;
     const uint32_t span = CHAIN_THREADS * WPT;
 #pragma unroll 1
-    for (uint32_t base = blockIdx.x * span; base < n_out; base += gridDim.x * span) {
+    for (uint32_t base = a.r_lo + blockIdx.x * span; base < n_out; base += gridDim.x * span) {
         i64 plain[WPT];
         u64 beta[WPT], pre[WPT];
         u64 cbis[WPT][K - 1];                // unpooled: beta^-1 sharing coefficients, drawn up front
@@ -904,30 +908,47 @@ int launch_kernels(const ChainArgs &a, const SsnField &f, const ssn_chain_desc *
         if (getenv("SSN_DEBUG"))
             fprintf(stderr, "chain nonlin G=%d c=%d h=%d w=%d kh=%d planes=%d wp=%d is=%llu copies=%d\n", G, d->c, d->h,
                     d->w, d->kh, a.planes != nullptr, a.pl_wp, (unsigned long long)a.pl_is, a.pl_copies);
-        if (split && !d->nonlin_only) {
-            // split: reshare + truncation (+ add) into scratch [n][nel], then the nonlinearity
-            ChainArgs a1 = a;
-            a1.out = d->scratch;
-            a1.out_ps = a.nel;
-            a1.planes = nullptr;
-            u64 b1 = (a.nel + PLAIN_THREADS - 1) / PLAIN_THREADS;
-            const u64 cap1 = chain_grid_cap(k_chain_plain<K, N, HF>, PLAIN_THREADS);
-            if (b1 > cap1) b1 = cap1;
-            SSN_COUNT_LAUNCH();
-            k_chain_plain<K, N, HF><<<(unsigned)b1, PLAIN_THREADS, 0, st>>>(a1, f);
-        }
-        ChainArgs a2 = a;
-        if (split && !d->nonlin_only) {
-            a2.acc = d->scratch;
-            a2.acc_ps = a.nel;
-        }
-        // a standalone masked nonlinearity (nonlin_only): acc holds the n parties' input shares
-        if (split) {
-            if (G == 4) launch_nonlin<K, N, true, HF, 4>(a2, f, n_out, st);
-            else if (G == 2) launch_nonlin<K, N, true, HF, 2>(a2, f, n_out, st);
-            else launch_nonlin<K, N, true, HF, 1>(a2, f, n_out, st);
-        } else {
-            launch_nonlin<K, N, false, HF, 1>(a2, f, n_out, st);
+        // SSN_CHAIN_CHUNK=E: element-wise chains (no pooling window, no gather) in chunks of E
+        // elements -- plain(chunk) then nonlinearity(chunk), the scratch round trip staying in L2.
+        // Off by default: measured slower (2^21: 263.9 vs 264.0 img/s, 2^20: 252.4, 2^19: 230.6;
+        // the chunks' partial waves cost more than the L2 hits save)
+        const bool chunkable = split && !d->nonlin_only && d->kh == 1 && d->kw == 1 && !d->gather;
+        static const u64 chunk_env = getenv("SSN_CHAIN_CHUNK") ? strtoull(getenv("SSN_CHAIN_CHUNK"), nullptr, 10) : 0;
+        const u64 span = (u64)CHAIN_THREADS * WPT;
+        const u64 chunk = chunkable && chunk_env ? (chunk_env + span - 1) / span * span : a.nel;
+        for (u64 lo = 0; lo < (chunkable ? a.nel : 1); lo += chunk) {
+            const u64 hi = chunkable ? (lo + chunk < a.nel ? lo + chunk : a.nel) : a.nel;
+            if (split && !d->nonlin_only) {
+                // split: reshare + truncation (+ add) into scratch [n][nel], then the nonlinearity
+                ChainArgs a1 = a;
+                a1.out = d->scratch;
+                a1.out_ps = a.nel;
+                a1.planes = nullptr;
+                a1.r_lo = (uint32_t)(chunkable ? lo : 0);
+                a1.r_hi = (uint32_t)(chunkable ? hi : a.nel);
+                u64 b1 = (a1.r_hi - a1.r_lo + PLAIN_THREADS - 1) / PLAIN_THREADS;
+                const u64 cap1 = chain_grid_cap(k_chain_plain<K, N, HF>, PLAIN_THREADS);
+                if (b1 > cap1) b1 = cap1;
+                if (b1 < 1) b1 = 1;
+                SSN_COUNT_LAUNCH();
+                k_chain_plain<K, N, HF><<<(unsigned)b1, PLAIN_THREADS, 0, st>>>(a1, f);
+            }
+            ChainArgs a2 = a;
+            if (split && !d->nonlin_only) {
+                a2.acc = d->scratch;
+                a2.acc_ps = a.nel;
+            }
+            a2.r_lo = (uint32_t)(chunkable ? lo : 0);
+            a2.r_hi = chunkable ? (uint32_t)hi : 0xffffffffu;
+            const u64 nwin = chunkable ? hi - lo : n_out;
+            // a standalone masked nonlinearity (nonlin_only): acc holds the n parties' input shares
+            if (split) {
+                if (G == 4) launch_nonlin<K, N, true, HF, 4>(a2, f, nwin, st);
+                else if (G == 2) launch_nonlin<K, N, true, HF, 2>(a2, f, nwin, st);
+                else launch_nonlin<K, N, true, HF, 1>(a2, f, nwin, st);
+            } else {
+                launch_nonlin<K, N, false, HF, 1>(a2, f, nwin, st);
+            }
         }
     }
     return cudaGetLastError() == cudaSuccess ? 0 : SSN_ERR_CUDA;
@@ -1030,6 +1051,8 @@ int launch_chain(const ssn_chain_desc *d, cudaStream_t st) {
     a.per_out = d->h_period_out;
     a.per_in = d->h_period_in ? d->h_period_in : d->h_period;
     a.gather = d->gather;
+    a.r_lo = 0;
+    a.r_hi = 0xffffffffu;
     a.gh = d->gather_h;
     a.gw = d->gather_w;
     a.gs = d->gather_stride;
