@@ -846,6 +846,7 @@ class StreamPipelinedEngine:
                                                 share_weights_with=first, **kw) for i in range(1, streams)]
         self.streams = [torch.cuda.Stream() for _ in range(streams)]
         self.scheme, self.ops = scheme, first.ops
+        self._warm = False
 
     def __getattr__(self, name):                  # out_shape, comm_per_image, limb_products, ...
         return getattr(self.engines[0], name)
@@ -861,6 +862,11 @@ class StreamPipelinedEngine:
         x = x_int.to(device=self.engines[0].dev, dtype=torch.int64)
         cur = torch.cuda.current_stream()
         parts = x.chunk(self.nstreams)
+        if not self._warm:
+            # the weight limb planes are built lazily by the first GEMM that needs them and are
+            # shared by all sub-batches: the first run goes stream after stream, so no sub-batch
+            # reads planes another stream has not finished writing
+            serial, self._warm = True, True
         outs = []
         prev = cur
         for eng, st, xp in zip(self.engines, self.streams, parts):
