@@ -334,8 +334,9 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
 #pragma unroll
     for (int j = 0; j < M; j++) acc[j] = a.acc[(u64)j * a.acc_ps + i];
     // ---- reshare step 1 (RESHARE_OUT): participant j sub-shares its local product to the front
-    // (the participants' M*(K-1) polynomial coefficients sliced from one Philox reservoir)
-    constexpr int NCR = (45 * M * (K - 1) + 127) / 128;
+    // (the participants' M*(K-1) polynomial coefficients, then the elite's K-1 fresh truncation
+    // share coefficients, sliced from one party-randomness Philox reservoir)
+    constexpr int NCR = (45 * (M + (HF ? 0 : 1)) * (K - 1) + 127) / 128;
     Reservoir<NCR> rr;
     fill<NCR>(rr, a.pseed, a.pstream, i, 0x900u);
     u64 sub[K][M];
@@ -347,24 +348,28 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
 #pragma unroll
         for (int fr = 0; fr < K; fr++) sub[fr][j] = poly_at<K>(acc[j], c, fr + 1);
     }
-    // source: zero shares (gen_zero_shares) and the truncation masks (gen_additive_mask)
-    // (zero, alpha and comp coefficients + the 64 bits of e from one source reservoir)
+    // source: zero shares (gen_zero_shares) and the truncation masks (gen_additive_mask).
+    // A rank receives its zero share and its alpha share and only ever uses their sum, the share
+    // of the summed polynomial alpha + sum_e (z_e + a_e) x^e; z_e + a_e of two independent uniform
+    // coefficients is one uniform coefficient, so the source draws the sum directly (same joint
+    // distribution of every rank's view).  za, the comp coefficients and the 64 bits of e come
+    // from one source reservoir (2 Philox calls for k = 3 instead of 3).
     u64 za[K - 1], cc[K - 1];        // zero + alpha coefficients, comp coefficients
     u64 alpha = 0, comp = 0;
     uint32_t ii = 0;
     if constexpr (HF) {
         ii = i - fdiv(i, a.f_per) * (uint32_t)a.per;
     } else {
-        constexpr int NCS = (45 * 3 * (K - 1) + 64 + 127) / 128;
+        constexpr int NCS = (45 * 2 * (K - 1) + 64 + 127) / 128;
         Reservoir<NCS> rs;
         fill<NCS>(rs, a.sseed, a.sstream, i, 0x900u);
 #pragma unroll
         for (int e = 0; e < K - 1; e++) {
-            za[e] = take45<NCS>(rs, 45 * e) + take45<NCS>(rs, 45 * (K - 1 + e));
-            cc[e] = take45<NCS>(rs, 45 * (2 * (K - 1) + e));
+            za[e] = take45<NCS>(rs, 45 * e);
+            cc[e] = take45<NCS>(rs, 45 * (K - 1 + e));
         }
         // e = 1 + U[0, emax) by multiply-shift of 64 random bits (bias <= emax / 2^64 <= 2^-32)
-        const u64 e = 1 + __umul64hi(take64<NCS>(rs, 45 * 3 * (K - 1)), a.emax);
+        const u64 e = 1 + __umul64hi(take64<NCS>(rs, 45 * 2 * (K - 1)), a.emax);
         const u64 em = red64(e);
         alpha = mulm_hs(em, a.stepm);                        // both canonical
         comp = em ? PP - em : 0;
@@ -435,12 +440,17 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
             }
             u64 add = a.bias[(u64)t * a.bias_ps + ch];
             if constexpr (HF) add += a.h_zero[(u64)t * a.per + ii] + a.h_alpha[(u64)t * a.per + ii];
-            if (t == a.fault_rank && i == 0) add += 1;                                      // test hook
             y += add * S;                                                                   // < 2^47 * S
             if constexpr (!HF) y += poly_at<K>(alpha_s, za_s, t + 1);
             masked[t] = lz(y);
         }
     });
+    if (i == 0 && a.fault_rank >= 0) {                      // test hook: corrupt one rank's message
+        sfor<0, N>([&](auto tc) {
+            constexpr int t = decltype(tc)::value;
+            if (t == a.fault_rank && t < a.senders) masked[t] = lz(masked[t] + S);
+        });
+    }
     // ---- truncation elite: rec over the front (x S^-1), RS check of the extra points,
     //      decode/floor/round
     u64 front[K];
@@ -458,9 +468,8 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
 #pragma unroll
         for (int e = 0; e < K - 1; e++) g[e] = a.h_tcoef[(u64)e * a.per + ii];
     } else {
-        coeffs<K>(g, a.pseed, a.pstream + M, i);
 #pragma unroll
-        for (int e = 0; e < K - 1; e++) g[e] += cc[e];
+        for (int e = 0; e < K - 1; e++) g[e] = take45<NCR>(rr, 45 * (M * (K - 1) + e)) + cc[e];
     }
 #pragma unroll
     for (int t = 0; t < N; t++) {
