@@ -541,6 +541,18 @@ __device__ __forceinline__ u64 mul_plain(i64 sv, u64 b) {
     return canon(HS ? mulm_hs(pl, b) : mulm(pl, b));
 }
 
+// d-th forward difference of id^e at id = 1: sum_i (-1)^(d-i) C(d, i) (1 + i)^e (>= 0)
+SSN_CC u64 fdiff_coef(int d, int e) {
+    int64_t s = 0, c = 1;                                   // c = C(d, i)
+    for (int i = 0; i <= d; i++) {
+        int64_t pw = 1;
+        for (int k = 0; k < e; k++) pw *= 1 + i;
+        s += ((d - i) % 2 ? -c : c) * pw;
+        c = c * (d - i) / (i + 1);
+    }
+    return (u64)s;
+}
+
 // run^-1 for every thread of the block from ONE Fermat inversion (Montgomery's batch trick):
 // warp-shuffle exclusive prefix/suffix products, warp totals through shared memory, warp 0
 // inverts the block total.  Out of line: it runs once per block iteration, and inlined it
@@ -752,30 +764,49 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
                     xq = (int)(pix - y * ow);
                     pb = a.planes + (u64)ci * a.pl_cs + (u64)img * a.pl_is + (u64)y * a.pl_wp;
                 }
-                // out ranks in a rolled loop (party-id powers at run time): the G-window body
-                // unrolled over the n ranks overflowed the instruction cache
+                // out ranks in a rolled loop: the G-window body unrolled over the n ranks
+                // overflowed the instruction cache.  Speed mode: rank t's share of the output is
+                // plain * (binv + sum_e cbi_e id^(e+1)) = sum_e P_e id^e with P_0 = plain * binv,
+                // P_e = plain * cbi_(e-1): K full multiplies per window, and the polynomial in id
+                // walks the ranks by forward differences of its exact integer value (K - 1 adds
+                // per rank, no multiply) instead of a multiply per rank
                 u64 *op = a.out + o0;
                 uint8_t *dst = pb + xq;
-                uint32_t pw[K - 1];
+                u64 fd[G][K];                                 // fd[g][d] = Delta^d f_g at the current id
+                if constexpr (!HF) {
 #pragma unroll
-                for (int e = 0; e < K - 1; e++) pw[e] = 1;
+                    for (int g = 0; g < G; g++) {
+                        const i64 sv = plain[gq * G + g];
+                        const u64 pl = sv < 0 ? (u64)((i64)PP + sv) : (u64)sv;      // < p
+                        u64 P[K];
+                        P[0] = mulm_hs(pl, binv[g]);
+#pragma unroll
+                        for (int e = 1; e < K; e++) P[e] = mulm_hs(pl, cbi[g][e - 1]);
+                        sfor<0, K>([&](auto dc) {
+                            constexpr int d = decltype(dc)::value;
+                            u64 acc = 0;
+                            sfor<d, K>([&](auto ec) {
+                                constexpr int e = decltype(ec)::value;
+                                constexpr u64 c = fdiff_coef(d, e);
+                                if constexpr (c == 1) acc += P[e];
+                                else if constexpr (c != 0) acc += P[e] * c;
+                            });
+                            fd[g][d] = acc;
+                        });
+                    }
+                }
 #pragma unroll 1
                 for (int t = 0; t < a.fan; t++) {
-#pragma unroll
-                    for (int e = 0; e < K - 1; e++) pw[e] = e == 0 ? (uint32_t)(t + 1) : pw[e - 1] * (uint32_t)(t + 1);
                     u64 v[G];
 #pragma unroll
                     for (int g = 0; g < G; g++) {
-                        u64 bis;
                         if constexpr (HF) {
-                            bis = a.h_binv[(u64)t * a.per_out + oo[g]];
+                            v[g] = mul_plain<true>(plain[gq * G + g], a.h_binv[(u64)t * a.per_out + oo[g]]);
                         } else {
-                            bis = binv[g];
+                            v[g] = canon(fd[g][0]);
 #pragma unroll
-                            for (int e = 0; e < K - 1; e++) bis += mul_small(cbi[g][e], pw[e]);
+                            for (int d = 0; d + 1 < K; d++) fd[g][d] += fd[g][d + 1];
                         }
-                        // the beta^-1 share: canonical (host-fed) or < 2^50 for k <= 3
-                        v[g] = mul_plain<HF || K <= 3>(plain[gq * G + g], bis);
                     }
                     if constexpr (G == 1) {
                         op[0] = v[0];
