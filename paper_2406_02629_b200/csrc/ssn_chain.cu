@@ -256,6 +256,51 @@ __device__ __forceinline__ u64 poly_at(u64 s, const u64 (&c)[K - 1], int id) {
     return acc;
 }
 
+// d-th forward difference of id^e at id = 1: sum_i (-1)^(d-i) C(d, i) (1 + i)^e (>= 0)
+SSN_CC u64 fdiff_coef(int d, int e) {
+    int64_t s = 0, c = 1;                                   // c = C(d, i)
+    for (int i = 0; i <= d; i++) {
+        int64_t pw = 1;
+        for (int k = 0; k < e; k++) pw *= 1 + i;
+        s += ((d - i) % 2 ? -c : c) * pw;
+        c = c * (d - i) / (i + 1);
+    }
+    return (u64)s;
+}
+
+// f(id) = sum_e P_e id^e (exact integer, unreduced) at id = 1, 2, 3, ... by forward
+// differences: k - 1 adds per point instead of multiplies by the powers of id
+template <int K>
+struct PolyWalk {
+    u64 d[K];                                      // d[j] = Delta^j f at the current id
+    __device__ __forceinline__ void init(const u64 (&P)[K]) {
+        sfor<0, K>([&](auto jc) {
+            constexpr int j = decltype(jc)::value;
+            u64 acc = 0;
+            sfor<j, K>([&](auto ec) {
+                constexpr int e = decltype(ec)::value;
+                constexpr u64 c = fdiff_coef(j, e);
+                if constexpr (c == 1) acc += P[e];
+                else if constexpr (c != 0) acc += P[e] * c;
+            });
+            d[j] = acc;
+        });
+    }
+    // f = s + sum_e c_e id^(e+1): the share polynomial of poly_at
+    __device__ __forceinline__ void init(u64 s, const u64 (&c)[K - 1]) {
+        u64 P[K];
+        P[0] = s;
+#pragma unroll
+        for (int e = 1; e < K; e++) P[e] = c[e - 1];
+        init(P);
+    }
+    __device__ __forceinline__ u64 value() const { return d[0]; }
+    __device__ __forceinline__ void step() {
+#pragma unroll
+        for (int j = 0; j + 1 < K; j++) d[j] += d[j + 1];
+    }
+};
+
 // K-1 uniform field elements: masked 45-bit Philox words.  Values in [p, 2^45) are lazy
 // representatives of [0, 55), exactly the distribution of the conditional-subtract form.
 template <int K>
@@ -345,8 +390,10 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
         u64 c[K - 1];
 #pragma unroll
         for (int e = 0; e < K - 1; e++) c[e] = take45<NCR>(rr, 45 * (j * (K - 1) + e));
+        PolyWalk<K> pw;
+        pw.init(acc[j], c);
 #pragma unroll
-        for (int fr = 0; fr < K; fr++) sub[fr][j] = poly_at<K>(acc[j], c, fr + 1);
+        for (int fr = 0; fr < K; fr++, pw.step()) sub[fr][j] = pw.value();
     }
     // source: zero shares (gen_zero_shares) and the truncation masks (gen_additive_mask).
     // A rank receives its zero share and its alpha share and only ever uses their sum, the share
@@ -414,6 +461,13 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
         for (int e = 0; e < K - 1; e++) za_s[e] = lz(za[e] * S);
     }
     u64 masked[N];                                            // S * TRUNC_MASKED[t]
+    PolyWalk<K> aw;                                           // S * (alpha + zero) share polynomial
+    if constexpr (!HF) aw.init(alpha_s, za_s);
+    PolyWalk<K> bw[K];                                        // front fr's D_v * RESHARE_BACK row polynomial
+    if constexpr (FACTOR) {
+#pragma unroll
+        for (int fr = 0; fr < K; fr++) bw[fr].init(w[fr]);
+    }
     sfor<0, N>([&](auto tc) {
         constexpr int t = decltype(tc)::value;
         if (t < a.senders) {
@@ -421,15 +475,7 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
             if constexpr (FACTOR) {
                 u64 back[K];                                   // D_v * RESHARE_BACK[fr -> t]
 #pragma unroll
-                for (int fr = 0; fr < K; fr++) {
-                    u64 acc = w[fr][0], pw = 1;
-#pragma unroll
-                    for (int c = 1; c < K; c++) {
-                        pw *= (u64)(t + 1);
-                        acc += w[fr][c] * pw;
-                    }
-                    back[fr] = acc;
-                }
+                for (int fr = 0; fr < K; fr++) back[fr] = bw[fr].value();
                 y = clin<WfRow<K, N>, XB_BACK>(back);
             } else {
                 u64 back[K];                                   // D_t * RESHARE_BACK[fr -> t]
@@ -441,8 +487,13 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
             u64 add = a.bias[(u64)t * a.bias_ps + ch];
             if constexpr (HF) add += a.h_zero[(u64)t * a.per + ii] + a.h_alpha[(u64)t * a.per + ii];
             y += add * S;                                                                   // < 2^47 * S
-            if constexpr (!HF) y += poly_at<K>(alpha_s, za_s, t + 1);
+            if constexpr (!HF) y += aw.value();
             masked[t] = lz(y);
+        }
+        if constexpr (!HF) aw.step();
+        if constexpr (FACTOR) {
+#pragma unroll
+            for (int fr = 0; fr < K; fr++) bw[fr].step();
         }
     });
     if (i == 0 && a.fault_rank >= 0) {                      // test hook: corrupt one rank's message
@@ -471,11 +522,13 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
 #pragma unroll
         for (int e = 0; e < K - 1; e++) g[e] = take45<NCR>(rr, 45 * (M * (K - 1) + e)) + cc[e];
     }
+    PolyWalk<K> fw;
+    if constexpr (HF) fw.init(tm, g);
+    else fw.init(tm + comp, g);
 #pragma unroll
-    for (int t = 0; t < N; t++) {
-        u64 s;
-        if constexpr (HF) s = poly_at<K>(tm, g, t + 1) + a.h_comp[(u64)t * a.per + ii];
-        else s = poly_at<K>(tm + comp, g, t + 1);
+    for (int t = 0; t < N; t++, fw.step()) {
+        u64 s = fw.value();
+        if constexpr (HF) s += a.h_comp[(u64)t * a.per + ii];
         if (a.other) s += a.other[(u64)t * a.other_ps + i];                              // residual add
         x[t] = RAW ? s : lz(s);
     }
@@ -539,18 +592,6 @@ template <bool HS>
 __device__ __forceinline__ u64 mul_plain(i64 sv, u64 b) {
     const u64 pl = sv < 0 ? (u64)((i64)PP + sv) : (u64)sv;     // < p < 2^45
     return canon(HS ? mulm_hs(pl, b) : mulm(pl, b));
-}
-
-// d-th forward difference of id^e at id = 1: sum_i (-1)^(d-i) C(d, i) (1 + i)^e (>= 0)
-SSN_CC u64 fdiff_coef(int d, int e) {
-    int64_t s = 0, c = 1;                                   // c = C(d, i)
-    for (int i = 0; i <= d; i++) {
-        int64_t pw = 1;
-        for (int k = 0; k < e; k++) pw *= 1 + i;
-        s += ((d - i) % 2 ? -c : c) * pw;
-        c = c * (d - i) / (i + 1);
-    }
-    return (u64)s;
 }
 
 // run^-1 for every thread of the block from ONE Fermat inversion (Montgomery's batch trick):
@@ -697,11 +738,13 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
 #pragma unroll
                                 for (int e = 0; e < K - 1; e++) cb[e] = cb1[e];
                             }
+                            PolyWalk<K> bsh;                  // beta share polynomial
+                            bsh.init(bt, cb);
 #pragma unroll
-                            for (int j = 0; j < M; j++) {
+                            for (int j = 0; j < M; j++, bsh.step()) {
                                 // x canonical (< 2^45), the beta share < 2^50 for k <= 3
-                                if constexpr (K <= 3) mk[j] = mulm_hs(x[j], poly_at<K>(bt, cb, j + 1));
-                                else mk[j] = mulm(x[j], poly_at<K>(bt, cb, j + 1));
+                                if constexpr (K <= 3) mk[j] = mulm_hs(x[j], bsh.value());
+                                else mk[j] = mulm(x[j], bsh.value());
                             }
                         }
                         const u64 v = canon(clin<WpRow<K, N>, 46>(mk));
@@ -782,17 +825,10 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
                         P[0] = mulm_hs(pl, binv[g]);
 #pragma unroll
                         for (int e = 1; e < K; e++) P[e] = mulm_hs(pl, cbi[g][e - 1]);
-                        sfor<0, K>([&](auto dc) {
-                            constexpr int d = decltype(dc)::value;
-                            u64 acc = 0;
-                            sfor<d, K>([&](auto ec) {
-                                constexpr int e = decltype(ec)::value;
-                                constexpr u64 c = fdiff_coef(d, e);
-                                if constexpr (c == 1) acc += P[e];
-                                else if constexpr (c != 0) acc += P[e] * c;
-                            });
-                            fd[g][d] = acc;
-                        });
+                        PolyWalk<K> wk;
+                        wk.init(P);
+#pragma unroll
+                        for (int d = 0; d < K; d++) fd[g][d] = wk.d[d];
                     }
                 }
 #pragma unroll 1
