@@ -586,14 +586,6 @@ __device__ __noinline__ void emit_planes(uint8_t *row, u64 v, int xq, int copies
 // 32x32->64 products instead of three
 __device__ __forceinline__ u64 mulm32(u64 a, uint32_t b) { return mulm_s32(a, b); }
 
-// NONLIN_PLAIN * (beta^-1 share), canonical: the elite's plaintext f(x * beta) is a signed value
-// with |f(x * beta)| < p/2 by the choice of bmax (S/masks.py:57-64), encoded, times the share.
-template <bool HS>
-__device__ __forceinline__ u64 mul_plain(i64 sv, u64 b) {
-    const u64 pl = sv < 0 ? (u64)((i64)PP + sv) : (u64)sv;     // < p < 2^45
-    return canon(HS ? mulm_hs(pl, b) : mulm(pl, b));
-}
-
 // run^-1 for every thread of the block from ONE Fermat inversion (Montgomery's batch trick):
 // warp-shuffle exclusive prefix/suffix products, warp totals through shared memory, warp 0
 // inverts the block total.  Out of line: it runs once per block iteration, and inlined it
@@ -662,9 +654,13 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
     const uint32_t span = CHAIN_THREADS * WPT;
 #pragma unroll 1
     for (uint32_t base = a.r_lo + blockIdx.x * span; base < n_out; base += gridDim.x * span) {
-        i64 plain[WPT];
-        u64 beta[WPT], pre[WPT];
-        u64 cbis[WPT][K - 1];                // unpooled: beta^-1 sharing coefficients, drawn up front
+        // per-window state carried from the masking pass to the output pass (local memory, kept
+        // small so the block's footprint stays in L1): the output share polynomial's products
+        // P_e = plain * c_(e-1) (e >= 1, c the beta^-1 sharing coefficients), pp = plain times
+        // the product of the thread's earlier betas (the Montgomery prefix; speed mode) or the
+        // encoded plain itself (host-fed beta^-1 shares), and beta
+        u64 pp[WPT], Pw[WPT][K - 1];
+        uint32_t beta[WPT];
         u64 run = 1;
 #pragma unroll 1
         for (int q = 0; q < WPT; q++) {
@@ -672,6 +668,9 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
             i64 pl = 0;
             u64 bt = 1;
             u64 cb1[K - 1];                  // unpooled: the window's beta-share coefficients
+            u64 cbi[K - 1];                  // its beta^-1 sharing coefficients
+#pragma unroll
+            for (int e = 0; e < K - 1; e++) cbi[e] = 0;
             if (o < n_out) {
                 if constexpr (!HF) {
                     if (!pooled) {
@@ -684,10 +683,11 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
 #pragma unroll
                         for (int e = 0; e < K - 1; e++) {
                             cb1[e] = take45<NCB>(rb, 64 + 45 * e);
-                            cbis[q][e] = take45<NCB>(rb, 64 + 45 * (K - 1 + e));
+                            cbi[e] = take45<NCB>(rb, 64 + 45 * (K - 1 + e));
                         }
                     } else {
                         bt = 1 + ssn_rand_range(a.sseed, a.sstream + 4, o, 0, a.bmax);  // window-constant beta
+                        coeffs<K>(cbi, a.sseed, a.sstream + 6, o);
                     }
                 }
                 uint32_t base_in = o;
@@ -755,15 +755,19 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
                     }
                 pl = acc;                                          // NONLIN_PLAIN (signed; encoded at use)
             }
-            plain[q] = pl;
-            beta[q] = bt;
+            const u64 ple = pl < 0 ? (u64)((i64)PP + pl) : (u64)pl;      // encoded, < p
+            beta[q] = (uint32_t)bt;
             if constexpr (HF) {
-                pre[q] = 0;                         // beta^-1 shares are host-fed
-            } else if (a.inv_table) {
-                pre[q] = a.inv_table[bt];           // source's beta^-1 from the inverse table
+                pp[q] = ple;                        // beta^-1 shares are host-fed
             } else {
-                pre[q] = run;                       // product of this thread's earlier betas
-                run = mulm32(run, (uint32_t)bt);
+#pragma unroll
+                for (int e = 0; e < K - 1; e++) Pw[q][e] = mulm_hs(ple, cbi[e]);
+                if (a.inv_table) {
+                    pp[q] = mulm_hs(ple, a.inv_table[bt]);   // = P_0 (source's beta^-1 from the table)
+                } else {
+                    pp[q] = mulm_hs(ple, run);               // run: product of the earlier betas
+                    run = mulm32(run, (uint32_t)bt);
+                }
             }
         }
         // source: beta^-1 for every window of the block iteration from ONE inversion
@@ -772,31 +776,23 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
 #pragma unroll 1
         for (int gq = WPT / G - 1; gq >= 0; gq--) {
             const uint32_t o0 = base + (gq * CHAIN_THREADS + threadIdx.x) * G;
-            u64 binv[G];
+            u64 P0[G];                                       // plain * beta^-1
 #pragma unroll
             for (int g = G - 1; g >= 0; g--) {
                 const int q = gq * G + g;
-                binv[g] = 0;
+                P0[g] = pp[q];
                 if constexpr (!HF) {
-                    if (a.inv_table) {
-                        binv[g] = pre[q];
-                    } else {
-                        binv[g] = mulm_hs(inv, pre[q]);            // both lazy, < 2^46
-                        inv = mulm32(inv, (uint32_t)beta[q]);
+                    if (!a.inv_table) {
+                        P0[g] = mulm_hs(inv, pp[q]);               // both lazy, < 2^46
+                        inv = mulm32(inv, beta[q]);
                     }
                 }
             }
             if (o0 < n_out) {                                // n_out % G == 0: the whole group
-                u64 cbi[G][K - 1];
                 uint32_t oo[G];
+                if constexpr (HF) {
 #pragma unroll
-                for (int g = 0; g < G; g++) {
-                    if constexpr (HF) oo[g] = (o0 + g) - fdiv(o0 + g, a.f_per_out) * (uint32_t)a.per_out;
-                    else if (pooled) coeffs<K>(cbi[g], a.sseed, a.sstream + 6, o0 + g);
-                    else {
-#pragma unroll
-                        for (int e = 0; e < K - 1; e++) cbi[g][e] = cbis[gq * G + g][e];
-                    }
+                    for (int g = 0; g < G; g++) oo[g] = (o0 + g) - fdiv(o0 + g, a.f_per_out) * (uint32_t)a.per_out;
                 }
                 uint8_t *pb = nullptr;
                 int xq = 0;
@@ -809,8 +805,8 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
                 }
                 // out ranks in a rolled loop: the G-window body unrolled over the n ranks
                 // overflowed the instruction cache.  Speed mode: rank t's share of the output is
-                // plain * (binv + sum_e cbi_e id^(e+1)) = sum_e P_e id^e with P_0 = plain * binv,
-                // P_e = plain * cbi_(e-1): K full multiplies per window, and the polynomial in id
+                // plain * (binv + sum_e c_e id^(e+1)) = sum_e P_e id^e with P_0 = plain * binv,
+                // P_e = plain * c_(e-1): K full multiplies per window, and the polynomial in id
                 // walks the ranks by forward differences of its exact integer value (K - 1 adds
                 // per rank, no multiply) instead of a multiply per rank
                 u64 *op = a.out + o0;
@@ -819,12 +815,10 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
                 if constexpr (!HF) {
 #pragma unroll
                     for (int g = 0; g < G; g++) {
-                        const i64 sv = plain[gq * G + g];
-                        const u64 pl = sv < 0 ? (u64)((i64)PP + sv) : (u64)sv;      // < p
                         u64 P[K];
-                        P[0] = mulm_hs(pl, binv[g]);
+                        P[0] = P0[g];
 #pragma unroll
-                        for (int e = 1; e < K; e++) P[e] = mulm_hs(pl, cbi[g][e - 1]);
+                        for (int e = 1; e < K; e++) P[e] = Pw[gq * G + g][e - 1];
                         PolyWalk<K> wk;
                         wk.init(P);
 #pragma unroll
@@ -837,7 +831,7 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
 #pragma unroll
                     for (int g = 0; g < G; g++) {
                         if constexpr (HF) {
-                            v[g] = mul_plain<true>(plain[gq * G + g], a.h_binv[(u64)t * a.per_out + oo[g]]);
+                            v[g] = canon(mulm_hs(P0[g], a.h_binv[(u64)t * a.per_out + oo[g]]));
                         } else {
                             v[g] = canon(fd[g][0]);
 #pragma unroll
