@@ -95,21 +95,73 @@ SSN_CC int64_t row_sum(int sign) {
 }
 SSN_CC u64 cmod(int64_t c) { return c >= 0 ? (u64)c % PP : PP - (u64)(-c) % PP; }
 
+// Terms of a row with opposite coefficients +c / -c pair up: c * (x_j + B - x_k), B a multiple of
+// p above any input, costs one multiply instead of two (Lagrange rows are full of such pairs:
+// wp = (5, -10, 10, -5, 1), wf = (3, -3, 1), D_v B^-1[:, 0] = 24 wp).
+// pair[j] >= 0: j is the positive member, pair[j] its negative partner; -2: a negative member
+// already paired; -1: unpaired.
+template <class Row>
+struct Pairing {
+    int pair[Row::len];
+};
+template <class Row>
+SSN_CC Pairing<Row> make_pairing() {
+    Pairing<Row> pr{};
+    for (int j = 0; j < Row::len; j++) pr.pair[j] = -1;
+    for (int j = 0; j < Row::len; j++) {
+        if (Row::c(j) <= 0 || pr.pair[j] != -1) continue;
+        for (int k = 0; k < Row::len; k++)
+            if (pr.pair[k] == -1 && Row::c(k) == -Row::c(j)) {
+                pr.pair[j] = k;
+                pr.pair[k] = -2;
+                break;
+            }
+    }
+    return pr;
+}
+template <class Row>
+struct PairOf {
+    static constexpr Pairing<Row> v = make_pairing<Row>();
+};
+// bound weights: sum of c over positive unpaired terms + 3 c over pairs (x + B < 3 * 2^XB), and
+// sum of |c| over negative unpaired terms
+template <class Row>
+SSN_CC int64_t pos_weight() {
+    constexpr Pairing<Row> pr = make_pairing<Row>();
+    int64_t s = 0;
+    for (int j = 0; j < Row::len; j++) {
+        if (pr.pair[j] >= 0) s += 3 * Row::c(j);
+        else if (pr.pair[j] == -1 && Row::c(j) > 0) s += Row::c(j);
+    }
+    return s;
+}
+template <class Row>
+SSN_CC int64_t neg_weight() {
+    constexpr Pairing<Row> pr = make_pairing<Row>();
+    int64_t s = 0;
+    for (int j = 0; j < Row::len; j++)
+        if (pr.pair[j] == -1 && Row::c(j) < 0) s -= Row::c(j);
+    return s;
+}
+
 // sum_j c_j x_j mod p, lazy (< 2^46), for compile-time integer c_j and inputs x_j < 2^XB.
 // Fast form: positive and negative terms in two u64 sums, one fold:  pos < 2^63 and
 // BIAS (a multiple of p above any neg) < 2^63 + p, so pos + BIAS - neg is exact in u64.
 template <class Row, int XB>
 __device__ __forceinline__ u64 clin(const u64 (&x)[Row::len]) {
-    constexpr int64_t P = row_sum<Row>(1), Q = row_sum<Row>(-1);
-    constexpr bool fast = XB < 62 && (u64)P < (1ull << (63 - XB)) && (u64)Q < (1ull << (63 - XB));
+    constexpr int64_t P = pos_weight<Row>(), Q = neg_weight<Row>();
+    constexpr bool fast = XB < 61 && (u64)P < (1ull << (63 - XB)) && (u64)Q < (1ull << (63 - XB));
     if constexpr (fast) {
+        constexpr u64 B = ((1ull << XB) / PP + 1) * PP;        // multiple of p, > any x_j
         u64 pos = 0, neg = 0;
-#pragma unroll
-        for (int j = 0; j < Row::len; j++) {
-            const int64_t c = Row::c(j);
-            if (c > 0) pos += x[j] * (u64)c;
-            else if (c < 0) neg += x[j] * (u64)(-c);
-        }
+        sfor<0, Row::len>([&](auto jc) {
+            constexpr int j = decltype(jc)::value;
+            constexpr int64_t c = Row::c(j);
+            constexpr int pj = PairOf<Row>::v.pair[j];
+            if constexpr (pj >= 0) pos += (x[j] + B - x[pj]) * (u64)c;
+            else if constexpr (pj == -1 && c > 0) pos += x[j] * (u64)c;
+            else if constexpr (pj == -1 && c < 0) neg += x[j] * (u64)(-c);
+        });
         constexpr u64 BIAS = (((u64)Q << XB) / PP + 1) * PP;
         return lz(pos + BIAS - neg);
     } else {
