@@ -281,18 +281,20 @@ constexpr int PLAIN_THREADS = 128;
 
 __device__ __forceinline__ u64 sqn(u64 x, int n) {
 #pragma unroll 1
-    for (int i = 0; i < n; i++) x = mulm(x, x);
+    for (int i = 0; i < n; i++) x = mulm_hs(x, x);
     return x;
 }
-// x^(p-2) = x^(2^45 - 57) by the addition chain x^(2^39-1)^(2^6) * x^7 (52 multiplications)
+// x^(p-2) = x^(2^45 - 57) by the addition chain x^(2^39-1)^(2^6) * x^7 (52 multiplications).
+// Here and in the batch inversion every operand is lazy (< 2^46), so products stay below 2^92 and
+// mulm_hs applies.
 __device__ __noinline__ u64 invm(u64 x) {
-    const u64 x2 = mulm(x, x), x3 = mulm(x2, x), x7 = mulm(mulm(x3, x3), x);
-    const u64 x6b = mulm(sqn(x7, 3), x7);            // x^(2^6-1)
-    const u64 x12 = mulm(sqn(x6b, 6), x6b);          // x^(2^12-1)
-    const u64 x24 = mulm(sqn(x12, 12), x12);         // x^(2^24-1)
-    const u64 x36 = mulm(sqn(x24, 12), x12);         // x^(2^36-1)
-    const u64 x39 = mulm(sqn(x36, 3), x7);           // x^(2^39-1)
-    return mulm(sqn(x39, 6), x7);
+    const u64 x2 = mulm_hs(x, x), x3 = mulm_hs(x2, x), x7 = mulm_hs(mulm_hs(x3, x3), x);
+    const u64 x6b = mulm_hs(sqn(x7, 3), x7);            // x^(2^6-1)
+    const u64 x12 = mulm_hs(sqn(x6b, 6), x6b);          // x^(2^12-1)
+    const u64 x24 = mulm_hs(sqn(x12, 12), x12);         // x^(2^24-1)
+    const u64 x36 = mulm_hs(sqn(x24, 12), x12);         // x^(2^36-1)
+    const u64 x39 = mulm_hs(sqn(x36, 3), x7);           // x^(2^39-1)
+    return mulm_hs(sqn(x39, 6), x7);
 }
 
 // share of s at party id `id` (a compile-time constant after unrolling): s + sum_e c_e id^(e+1),
@@ -606,7 +608,7 @@ __device__ __noinline__ u64 warp_excl_prefix(u64 v, int lane) {
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const u64 t = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl = mulm(incl, t);
+        if (lane >= o) incl = mulm_hs(incl, t);
     }
     const u64 ex = __shfl_up_sync(0xffffffffu, incl, 1);
     return lane ? ex : 1;
@@ -616,7 +618,7 @@ __device__ __noinline__ u64 warp_excl_suffix(u64 v, int lane) {
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
         const u64 t = __shfl_down_sync(0xffffffffu, incl, o);
-        if (lane + o < 32) incl = mulm(incl, t);
+        if (lane + o < 32) incl = mulm_hs(incl, t);
     }
     const u64 ex = __shfl_down_sync(0xffffffffu, incl, 1);
     return lane < 31 ? ex : 1;
@@ -646,18 +648,18 @@ __device__ __noinline__ u64 block_batch_inverse(u64 run, int lane, int warp, u64
     constexpr int NW = CHAIN_THREADS / 32;
     const u64 wpre = warp_excl_prefix(run, lane);
     const u64 wsuf = warp_excl_suffix(run, lane);
-    const u64 wtot = __shfl_sync(0xffffffffu, mulm(wpre, run), 31);
+    const u64 wtot = __shfl_sync(0xffffffffu, mulm_hs(wpre, run), 31);
     if (lane == 0) s_tot[warp] = wtot;
     __syncthreads();
     if (warp == 0) {
         const u64 v = lane < NW ? s_tot[lane] : 1;
         const u64 bp = warp_excl_prefix(v, lane), bs = warp_excl_suffix(v, lane);
-        const u64 tot = __shfl_sync(0xffffffffu, mulm(bp, v), 31);
+        const u64 tot = __shfl_sync(0xffffffffu, mulm_hs(bp, v), 31);
         const u64 ti = invm(tot);
-        if (lane < NW) s_inv[lane] = mulm(mulm(ti, bp), bs);              // = warp total^-1
+        if (lane < NW) s_inv[lane] = mulm_hs(mulm_hs(ti, bp), bs);              // = warp total^-1
     }
     __syncthreads();
-    return mulm(mulm(s_inv[warp], wpre), wsuf);                            // = run^-1
+    return mulm_hs(mulm_hs(s_inv[warp], wpre), wsuf);                            // = run^-1
 }
 
 // masked nonlinearity fused after the chain.  Each thread owns WPT output windows, in groups of G
@@ -1213,7 +1215,7 @@ __global__ void k_inv_table(u64 *__restrict__ t, u64 n) {
     for (int g = 0; g < G; g++) {
         const u64 b = start + g;
         pre[g] = run;
-        if (b > 0 && b < n) run = mulm(run, b);
+        if (b > 0 && b < n) run = mulm_hs(run, b);
     }
     u64 inv = canon(invm(canon(run)));
     for (int g = G - 1; g >= 0; g--) {
@@ -1223,8 +1225,8 @@ __global__ void k_inv_table(u64 *__restrict__ t, u64 n) {
             t[b] = 0;
             continue;
         }
-        t[b] = canon(mulm(inv, pre[g]));
-        inv = mulm(inv, b);
+        t[b] = canon(mulm_hs(inv, pre[g]));
+        inv = mulm_hs(inv, b);
     }
 }
 }  // namespace
