@@ -268,12 +268,12 @@ constexpr int PLAIN_THREADS = 256;
 #else
 constexpr int CHAIN_THREADS = 128;
 constexpr int PLAIN_THREADS = 128;
-// default: k_chain_plain at 6 CTAs/SM (80 registers, no spill), k_chain_nonlin at 7
+// default: k_chain_plain at 6 CTAs/SM (80 registers, no spill), k_chain_nonlin at 6
 #ifndef SSN_PLAIN_MINB
 #define SSN_PLAIN_MINB 6
 #endif
 #ifndef SSN_NONLIN_MINB
-#define SSN_NONLIN_MINB 7
+#define SSN_NONLIN_MINB 6
 #endif
 #define SSN_PLAIN_BOUNDS __launch_bounds__(PLAIN_THREADS, SSN_PLAIN_MINB)
 #define SSN_NONLIN_BOUNDS __launch_bounds__(CHAIN_THREADS, SSN_NONLIN_MINB)
