@@ -266,7 +266,10 @@ constexpr int PLAIN_THREADS = 256;
 #define SSN_PLAIN_BOUNDS __maxnreg__(96)
 #define SSN_NONLIN_BOUNDS __maxnreg__(80)
 #else
-constexpr int CHAIN_THREADS = 128;
+#ifndef SSN_CHAIN_THREADS
+#define SSN_CHAIN_THREADS 128
+#endif
+constexpr int CHAIN_THREADS = SSN_CHAIN_THREADS;
 constexpr int PLAIN_THREADS = 128;
 // default: k_chain_plain at 6 CTAs/SM (80 registers, no spill), k_chain_nonlin at 6
 #ifndef SSN_PLAIN_MINB
