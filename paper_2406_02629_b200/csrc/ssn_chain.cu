@@ -711,8 +711,9 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
     const uint32_t span = CHAIN_THREADS * WPT;
 #pragma unroll 1
     for (uint32_t base = a.r_lo + blockIdx.x * span; base < n_out; base += gridDim.x * span) {
-        // per-window state carried from the masking pass to the output pass (local memory, kept
-        // small so the block's footprint stays in L1): the output share polynomial's products
+        // per-window state carried from the masking pass to the output pass (local memory; the
+        // lines mostly miss L1, so it is kept small -- 28 B per window for (3,5)): the output
+        // share polynomial's products
         // P_e = plain * c_(e-1) (e >= 1, c the beta^-1 sharing coefficients), pp = plain times
         // the product of the thread's earlier betas (the Montgomery prefix; speed mode) or the
         // encoded plain itself (host-fed beta^-1 shares), and beta
