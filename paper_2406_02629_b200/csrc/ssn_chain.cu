@@ -147,10 +147,20 @@ SSN_CC int64_t neg_weight() {
 // sum_j c_j x_j mod p, lazy (< 2^46), for compile-time integer c_j and inputs x_j < 2^XB.
 // Fast form: positive and negative terms in two u64 sums, one fold:  pos < 2^63 and
 // BIAS (a multiple of p above any neg) < 2^63 + p, so pos + BIAS - neg is exact in u64.
+// FOLD = false (fast form only): the unreduced pos + BIAS - neg, below clin_raw_bound<Row, XB>()
 template <class Row, int XB>
+SSN_CC bool clin_fast() {
+    return XB < 61 && (u64)pos_weight<Row>() < (1ull << (63 - XB)) && (u64)neg_weight<Row>() < (1ull << (63 - XB));
+}
+template <class Row, int XB>
+SSN_CC u64 clin_raw_bound() {
+    return (u64)(pos_weight<Row>() + neg_weight<Row>()) * (1ull << XB) + 2 * PP;
+}
+template <class Row, int XB, bool FOLD = true>
 __device__ __forceinline__ u64 clin(const u64 (&x)[Row::len]) {
     constexpr int64_t P = pos_weight<Row>(), Q = neg_weight<Row>();
-    constexpr bool fast = XB < 61 && (u64)P < (1ull << (63 - XB)) && (u64)Q < (1ull << (63 - XB));
+    constexpr bool fast = clin_fast<Row, XB>();
+    static_assert(fast || FOLD, "unreduced combinations need the fast form");
     if constexpr (fast) {
         constexpr u64 B = ((1ull << XB) / PP + 1) * PP;        // multiple of p, > any x_j
         u64 pos = 0, neg = 0;
@@ -163,6 +173,7 @@ __device__ __forceinline__ u64 clin(const u64 (&x)[Row::len]) {
             else if constexpr (pj == -1 && c < 0) neg += x[j] * (u64)(-c);
         });
         constexpr u64 BIAS = (((u64)Q << XB) / PP + 1) * PP;
+        if constexpr (!FOLD) return pos + BIAS - neg;
         return lz(pos + BIAS - neg);
     } else {
         // wide coefficients (k = 4 reducing-matrix columns): full field products
@@ -517,7 +528,16 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
 #pragma unroll
         for (int e = 0; e < K - 1; e++) za_s[e] = lz(za[e] * S);
     }
-    u64 masked[N];                                            // S * TRUNC_MASKED[t]
+    // S * TRUNC_MASKED[t].  k <= 3: left unreduced -- the rank's reconstruction (unfolded, below
+    // clin_raw_bound), + S (bias + 1) < 2^47 S, + the alpha/zero share < 2^46 (1 + n + n^2) --
+    // and the front's Lagrange row and the RS rows take XB_M-bit inputs in their fast form (two
+    // folds fewer per rank); k = 4's RS rows have coefficient sums too wide for that, so it folds
+    constexpr bool MFOLD = !FACTOR || K > 3;
+    constexpr u64 MBOUND = clin_raw_bound<WfRow<K, N>, XB_BACK>() + (S << 47) + (1ull << 46) * (1 + N + N * N);
+    constexpr int XB_M = MFOLD ? 46 : 56;
+    static_assert(MFOLD || MBOUND < (1ull << XB_M), "TRUNC_MASKED bound");
+    static_assert(MFOLD || clin_fast<WfRow<K, N>, XB_M>(), "front row fast form");
+    u64 masked[N];
     PolyWalk<K> aw;                                           // S * (alpha + zero) share polynomial
     if constexpr (!HF) aw.init(alpha_s, za_s);
     PolyWalk<K> bw[K];                                        // front fr's D_v * RESHARE_BACK row polynomial
@@ -533,7 +553,7 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
                 u64 back[K];                                   // D_v * RESHARE_BACK[fr -> t]
 #pragma unroll
                 for (int fr = 0; fr < K; fr++) back[fr] = bw[fr].value();
-                y = clin<WfRow<K, N>, XB_BACK>(back);
+                y = clin<WfRow<K, N>, XB_BACK, MFOLD>(back);
             } else {
                 u64 back[K];                                   // D_t * RESHARE_BACK[fr -> t]
 #pragma unroll
@@ -545,7 +565,7 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
             if constexpr (HF) add += a.h_zero[(u64)t * a.per + ii] + a.h_alpha[(u64)t * a.per + ii];
             y += add * S;                                                                   // < 2^47 * S
             if constexpr (!HF) y += aw.value();
-            masked[t] = lz(y);
+            masked[t] = MFOLD ? lz(y) : y;
         }
         if constexpr (!HF) aw.step();
         if constexpr (FACTOR) {
@@ -556,7 +576,7 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
     if (i == 0 && a.fault_rank >= 0) {                      // test hook: corrupt one rank's message
         sfor<0, N>([&](auto tc) {
             constexpr int t = decltype(tc)::value;
-            if (t == a.fault_rank && t < a.senders) masked[t] = lz(masked[t] + S);
+            if (t == a.fault_rank && t < a.senders) masked[t] = lz(masked[t] + S);          // < 2^46 either way
         });
     }
     // ---- truncation elite: rec over the front (x S^-1), RS check of the extra points,
@@ -564,10 +584,10 @@ __device__ __forceinline__ void chain_elem(const ChainArgs &a, uint32_t i, u64 (
     u64 front[K];
 #pragma unroll
     for (int j = 0; j < K; j++) front[j] = masked[j];
-    const u64 v = canon(mulm_hs(clin<WfRow<K, N>, 46>(front), SINV));      // lazy x canonical
+    const u64 v = canon(mulm_hs(clin<WfRow<K, N>, XB_M>(front), SINV));    // lazy x canonical
     sfor<K, N>([&](auto tc) {
         constexpr int t = decltype(tc)::value;
-        if (t < a.senders) bad += (canon(clin<ExtRow<K, N, t>, 46>(front)) != canon(masked[t]));
+        if (t < a.senders) bad += (canon(clin<ExtRow<K, N, t>, XB_M>(front)) != canon(masked[t]));
     });
     const u64 tm = trunc_val(v, a);
     // fresh (k, n) shares of the truncated value (SHARE_DIST), + comp at every rank
