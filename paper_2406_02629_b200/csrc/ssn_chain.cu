@@ -729,6 +729,12 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
     const bool pooled = a.kh != 1 || a.kw != 1;
     const bool batch_inv = !HF && !a.inv_table;
     const uint32_t span = CHAIN_THREADS * WPT;
+    // the masked products mk: for k = 2 (speed mode) unfolded mulm_hs, < 2^56 (x < 2^45, beta
+    // share < 2^50), into the elite's WpRow fast form -- fewer instructions; for (3,5) the same
+    // change measured 17% slower (nonlinearity kernel), so k >= 3 and host-fed shares fold
+    constexpr bool MK_RAW = K == 2 && !HF;
+    constexpr int MK_XB = MK_RAW ? 56 : 46;
+    static_assert(clin_fast<WpRow<K, N>, MK_XB>(), "WpRow fast form");
 #pragma unroll 1
     for (uint32_t base = a.r_lo + blockIdx.x * span; base < n_out; base += gridDim.x * span) {
         // per-window state carried from the masking pass to the output pass (local memory; the
@@ -820,12 +826,13 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
                             bsh.init(bt, cb);
 #pragma unroll
                             for (int j = 0; j < M; j++, bsh.step()) {
-                                // x canonical (< 2^45), the beta share < 2^50 for k <= 3
-                                if constexpr (K <= 3) mk[j] = mulm_hs(x[j], bsh.value());
+                                // x canonical (< 2^45), the beta share < 2^50 for k <= 3: the
+                                // product < 2^95 (unfolded mulm_hs < 2^56 = MK_XB for k = 2)
+                                if constexpr (K <= 3) mk[j] = mulm_hs<!MK_RAW>(x[j], bsh.value());
                                 else mk[j] = mulm(x[j], bsh.value());
                             }
                         }
-                        const u64 v = canon(clin<WpRow<K, N>, 46>(mk));
+                        const u64 v = canon(clin<WpRow<K, N>, MK_XB>(mk));
                         i64 sv = v > PHALF ? (i64)v - (i64)PP : (i64)v;
                         if (a.relu && sv <= 0) sv = 0;
                         if (a.pool_kind == 1) acc = sv > acc ? sv : acc;

@@ -63,6 +63,7 @@ __device__ __forceinline__ u64 mulm(u64 a, u64 b) {
 // fits 32 bits, so its partial products are three 32x32->64 multiplies and one 32-bit
 // multiply-add-with-carry, and the fold is  (lo mod 2^45) + 55 (lo >> 45) + 55 * 2^19 * hi.
 // Written in PTX: the C form compiled to ~30% more FMA-heavy pipe work (extra VIADD/IMAD.MOV).
+template <bool FOLD = true>
 __device__ __forceinline__ u64 mulm_hs(u64 a, u64 b) {
     const uint32_t al = (uint32_t)a, ah = (uint32_t)(a >> 32), bl = (uint32_t)b, bh = (uint32_t)(b >> 32);
     uint32_t lo_lo, lo_hi, hi;
@@ -81,6 +82,9 @@ __device__ __forceinline__ u64 mulm_hs(u64 a, u64 b) {
     const uint32_t t1 = (lo_hi >> (PS - 32)) * (uint32_t)PC;                 // 55 (lo >> 45) < 2^25
     const u64 t2 = (u64)hi * (PC << (64 - PS));                             // 55 2^19 hi < 2^57
     const u64 low = ((u64)(lo_hi & ((1u << (PS - 32)) - 1)) << 32) | lo_lo;  // lo mod 2^45
+    // FOLD = false: the unreduced low + t1 + t2 < 2^45 + 2^25 + 55 * 2^19 * (a * b >> 64),
+    // e.g. below 2^56 for a * b < 2^95
+    if constexpr (!FOLD) return low + t1 + t2;
     return lz(low + t1 + t2);
 }
 
