@@ -325,34 +325,47 @@ __device__ __forceinline__ u64 poly_at(u64 s, const u64 (&c)[K - 1], int id) {
 }
 
 // d-th forward difference of id^e at id = 1: sum_i (-1)^(d-i) C(d, i) (1 + i)^e (>= 0)
-SSN_CC u64 fdiff_coef(int d, int e) {
+SSN_CC u64 fdiff_coef(int d, int e, int base = 1) {
     int64_t s = 0, c = 1;                                   // c = C(d, i)
     for (int i = 0; i <= d; i++) {
         int64_t pw = 1;
-        for (int k = 0; k < e; k++) pw *= 1 + i;
+        for (int k = 0; k < e; k++) pw *= base + i;
         s += ((d - i) % 2 ? -c : c) * pw;
         c = c * (d - i) / (i + 1);
     }
     return (u64)s;
 }
 
+#ifndef SSN_WALK0
+#define SSN_WALK0 1
+#endif
+SSN_CC int ilog2c(u64 c) {
+    int l = 0;
+    while ((1ull << l) < c) l++;
+    return l;
+}
 // f(id) = sum_e P_e id^e (exact integer, unreduced) at id = 1, 2, 3, ... by forward
 // differences: k - 1 adds per point instead of multiplies by the powers of id
 template <int K>
 struct PolyWalk {
     u64 d[K];                                      // d[j] = Delta^j f at the current id
+    // SSN_WALK0: start from the differences at id = 0 (coefficients j! S(e, j): 1 and 2 for
+    // k = 3, a shift instead of multiplies) and step once to id = 1
     __device__ __forceinline__ void init(const u64 (&P)[K]) {
+        constexpr int BASE = SSN_WALK0 ? 0 : 1;
         sfor<0, K>([&](auto jc) {
             constexpr int j = decltype(jc)::value;
             u64 acc = 0;
             sfor<j, K>([&](auto ec) {
                 constexpr int e = decltype(ec)::value;
-                constexpr u64 c = fdiff_coef(j, e);
+                constexpr u64 c = fdiff_coef(j, e, BASE);
                 if constexpr (c == 1) acc += P[e];
+                else if constexpr (c != 0 && (c & (c - 1)) == 0) acc += P[e] << ilog2c(c);
                 else if constexpr (c != 0) acc += P[e] * c;
             });
             d[j] = acc;
         });
+        if constexpr (SSN_WALK0) step();
     }
     // f = s + sum_e c_e id^(e+1): the share polynomial of poly_at
     __device__ __forceinline__ void init(u64 s, const u64 (&c)[K - 1]) {
