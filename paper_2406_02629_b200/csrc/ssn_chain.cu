@@ -748,6 +748,8 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
     constexpr bool MK_RAW = K == 2 && !HF;
     constexpr int MK_XB = MK_RAW ? 56 : 46;
     static_assert(clin_fast<WpRow<K, N>, MK_XB>(), "WpRow fast form");
+    // unfolded P_0 + P_1 id (k = 2) < (1 + n) 2^57.1 must stay below 2^64 for the output canon
+    static_assert(!MK_RAW || N <= 100, "unfolded output polynomial bound");
 #pragma unroll 1
     for (uint32_t base = a.r_lo + blockIdx.x * span; base < n_out; base += gridDim.x * span) {
         // per-window state carried from the masking pass to the output pass (local memory; the
@@ -859,7 +861,7 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
                 pp[q] = ple;                        // beta^-1 shares are host-fed
             } else {
 #pragma unroll
-                for (int e = 0; e < K - 1; e++) Pw[q][e] = mulm_hs(ple, cbi[e]);
+                for (int e = 0; e < K - 1; e++) Pw[q][e] = mulm_hs<!MK_RAW>(ple, cbi[e]);
                 if (a.inv_table) {
                     pp[q] = mulm_hs(ple, a.inv_table[bt]);   // = P_0 (source's beta^-1 from the table)
                 } else {
@@ -881,7 +883,9 @@ __global__ void SSN_NONLIN_BOUNDS k_chain_nonlin(ChainArgs a, SsnField f) {
                 P0[g] = pp[q];
                 if constexpr (!HF) {
                     if (!a.inv_table) {
-                        P0[g] = mulm_hs(inv, pp[q]);               // both lazy, < 2^46
+                        // both lazy, < 2^46; k = 2: left unfolded (< 2^57.1), the output
+                        // polynomial P_0 + P_1 id stays below 2^59.1 for id <= 3
+                        P0[g] = mulm_hs<!MK_RAW>(inv, pp[q]);
                         inv = mulm32(inv, beta[q]);
                     }
                 }
