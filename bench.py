@@ -263,8 +263,8 @@ def load_traffic(workload=None):
 # chain element, by workload: ncu smsp__thread_inst_executed / sm__pipe_fmaheavy_cycles_active over the
 # chain kernels of one ResNet-152 step (batch 32) / the step's chain elements (tools/chain_alu.py,
 # profiles/r02/alu/).  The chain kernels are bound by the FMA-heavy pipe that executes IMAD.
-CHAIN_ALU = {"resnet152-5pc": 1943, "resnet152-3pc": 1120}
-CHAIN_HEAVY = {"resnet152-5pc": 64.9, "resnet152-3pc": 35.3}
+CHAIN_ALU = {"resnet152-5pc": 1943, "resnet152-3pc": 1111}
+CHAIN_HEAVY = {"resnet152-5pc": 64.9, "resnet152-3pc": 35.0}
 
 
 def roofline(kstats, eng, dev_ms, bf16, hbm, src, workload=None):
