@@ -606,7 +606,8 @@ k_gemm_p45w(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUt
                         } else if (grp == 1) {
                             s[c] += (acc >> 13) * 55 + ((acc & 0x1FFF) << 32);         // acc * 2^32, < 2^50
                         } else {
-                            const u64 z = (acc >> 26) * 55 + ((acc & 0x3FFFFFF) << 19); // acc * 2^19, < 2^45.1
+                            // acc >> 26 < 2^22.1: its product with 55 is a 32-bit IMAD
+                            const u64 z = (u64)((uint32_t)(acc >> 26) * 55u) + ((acc & 0x3FFFFFF) << 19); // acc * 2^19, < 2^45.1
                             const u64 tt = lz(s[c] + z * 55);                          // acc * 2^64; sum < 2^57
                             s[c] = tt >= P ? tt - P : tt;
                         }
